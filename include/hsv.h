@@ -1,0 +1,193 @@
+/*
+ * hsv.h -- C ABI of the B200-native exact sparse state-vector engine
+ * (Hyperion-1 path of arxiv/paper_2604_01176, reference package `svmps`).
+ *
+ * Plain C types only (no torch, no C++ in signatures).  Every entry point
+ * returns an int status (HSV_OK = 0); on failure hsv_last_error() holds a
+ * message whose wording mirrors the reference exception it replaces, and the
+ * Python host layer re-raises the same exception type (ValueError /
+ * RuntimeError / MemoryError).
+ *
+ * Object model (all opaque, device resident, explicitly destroyed):
+ *   hsv_sector  one (n_alpha, n_beta) particle-number sector of an n-qubit
+ *               register: replaces svmps.cibasis.CiBasis / enumerate_basis
+ *               (cibasis.py:98-181).  Reference positions (ascending key
+ *               order) are exposed; internally amplitudes are stored
+ *               alpha-string-major ("HBM layout").
+ *   hsv_op      a real, number-conserving Pauli sum bound to a sector, stored
+ *               matrix-free as x-grouped term tables: replaces the CSR built
+ *               by svmps.svengine.assemble_subspace_hamiltonian
+ *               (svengine.py:115-171) and its validation (odd-Y, sector leak).
+ *   hsv_state   a complex128 amplitude vector over a sector; support is the
+ *               set of exactly-nonzero amplitudes, which is how the reference
+ *               SparseVector (sparse.py:20-70) drops exact zeros.
+ *
+ * Calls are synchronous on return unless named *_async; all device work is
+ * enqueued on the library stream (hsv_set_stream).  Results are bitwise
+ * deterministic run to run (no floating-point atomics).
+ */
+#ifndef HSV_H_
+#define HSV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HSV_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define HSV_API __attribute__((visibility("default")))
+#else
+#define HSV_API
+#endif
+
+enum hsv_status {
+  HSV_OK = 0,
+  HSV_ERR_INVALID = 1,      /* bad argument / dimension mismatch  -> ValueError   */
+  HSV_ERR_SECTOR = 2,       /* configuration outside the sector   -> ValueError   */
+  HSV_ERR_NONREAL = 3,      /* odd-Y Pauli word                   -> ValueError   */
+  HSV_ERR_LEAK = 4,         /* Hamiltonian not spin-conserving    -> ValueError   */
+  HSV_ERR_NORM_DRIFT = 5,   /* QEB rotation norm drift            -> RuntimeError */
+  HSV_ERR_CUDA = 6,         /* CUDA runtime failure               -> RuntimeError */
+  HSV_ERR_OOM = 7,          /* device allocation failed           -> MemoryError  */
+  HSV_ERR_UNSUPPORTED = 8   /* sector too large for dense layout  -> ValueError   */
+};
+
+enum hsv_ordering { HSV_INTERLEAVED = 0, HSV_BLOCKED = 1 };
+
+typedef struct hsv_sector_s* hsv_sector;
+typedef struct hsv_op_s* hsv_op;
+typedef struct hsv_state_s* hsv_state;
+
+/* ---- library / device ------------------------------------------------- */
+HSV_API int hsv_abi_version(void);
+/* Copies the last error message of the calling thread into buf. */
+HSV_API int hsv_last_error(char* buf, size_t n);
+/* Select the CUDA device for subsequent objects (one context per process). */
+HSV_API int hsv_init(int device);
+/* Enqueue all work on this cudaStream_t (0 = library-owned stream). */
+HSV_API int hsv_set_stream(void* cuda_stream);
+HSV_API void* hsv_get_stream(void);
+/* Number of CUDA kernels this library launched since the last reset. */
+HSV_API int64_t hsv_launch_count(int reset);
+HSV_API int hsv_synchronize(void);
+
+/* ---- sector: replaces CiBasis / enumerate_basis (cibasis.py:98-181) ---- */
+HSV_API int hsv_sector_create(int n_qubits, int n_alpha, int n_beta, int ordering,
+                      hsv_sector* out);
+HSV_API int hsv_sector_destroy(hsv_sector s);
+HSV_API int64_t hsv_sector_dim(hsv_sector s);
+/* Alpha-string count and beta-string count (dim = n_alpha_strings * n_beta_strings). */
+HSV_API int hsv_sector_shape(hsv_sector s, int64_t* n_alpha_strings, int64_t* n_beta_strings);
+/* Reference positions of keys (CiBasis.try_positions, cibasis.py:133-138):
+ * pos[i] = -1 when keys[i] is outside the sector. */
+HSV_API int hsv_sector_positions(hsv_sector s, const uint64_t* keys, int64_t n, int64_t* pos);
+/* Keys (occupation integers) of reference positions (CiBasis.states[pos]). */
+HSV_API int hsv_sector_keys(hsv_sector s, const int64_t* pos, int64_t n, uint64_t* keys);
+
+/* ---- operator: replaces assemble_subspace_hamiltonian (svengine.py:115-171) */
+/* xs/zs: symplectic masks, coeffs: real weights (PauliSum arrays, pauli.py:87-107).
+ * Raises NONREAL for an odd-Y word, LEAK for a group whose net amplitude
+ * escapes the sector by more than 1e-10 (first offending x in ascending order). */
+HSV_API int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* zs,
+                  const double* coeffs, int64_t n_terms, hsv_op* out);
+HSV_API int hsv_op_destroy(hsv_op op);
+/* n_terms, n_groups (distinct x incl. diagonal), number of in-sector nonzero
+ * matrix elements is not stored (matrix-free). */
+HSV_API int hsv_op_info(hsv_op op, int64_t* n_terms, int64_t* n_groups, int64_t* n_active_groups);
+/* Number of structurally nonzero matrix elements (== reference CSR nnz). */
+HSV_API int hsv_op_count_nnz(hsv_op op, int64_t* nnz);
+/* Materialize the CSR (reference positions, ascending columns per row) for
+ * small sectors: row_offsets[dim+1], cols[nnz], vals[nnz] (host buffers). */
+HSV_API int hsv_op_to_csr(hsv_op op, int64_t* row_offsets, int64_t* cols, double* vals, int64_t nnz_cap);
+
+/* ---- states (SparseVector / SvState, sparse.py:20-70, svengine.py:89-109) */
+HSV_API int hsv_state_create(hsv_sector s, hsv_state* out);              /* all zero */
+HSV_API int hsv_state_destroy(hsv_state st);
+HSV_API int hsv_state_copy(hsv_state dst, hsv_state src);
+HSV_API int hsv_state_zero(hsv_state st);
+/* Basis state |key> (SvState.from_configuration, svengine.py:96-101). */
+HSV_API int hsv_state_set_basis(hsv_state st, uint64_t key, double re, double im);
+/* Replace contents from (ascending) reference positions; amps interleaved
+ * (re, im) pairs, amps_im may be NULL for real input. */
+HSV_API int hsv_state_set_sparse(hsv_state st, const int64_t* pos, const double* amps_re,
+                         const double* amps_im, int64_t n);
+HSV_API int hsv_state_set_keys(hsv_state st, const uint64_t* keys, const double* amps_re,
+                       const double* amps_im, int64_t n);
+HSV_API int hsv_state_nnz(hsv_state st, int64_t* nnz);
+/* Support in ascending reference position order (drops exact zeros, or
+ * |v| < prune when prune > 0). cap = capacity of the output buffers. */
+HSV_API int hsv_state_get_sparse(hsv_state st, double prune, int64_t* pos, double* amps_re,
+                         double* amps_im, int64_t cap, int64_t* n_out);
+/* <a|b> (dot, sparse.py:210-219). */
+HSV_API int hsv_state_dot(hsv_state a, hsv_state b, double* re, double* im);
+HSV_API int hsv_state_norm(hsv_state st, double* norm);
+/* y <- a*x + y, then exact zeros drop (axpy, sparse.py:222-228). */
+HSV_API int hsv_state_axpy(double a_re, double a_im, hsv_state x, hsv_state y);
+HSV_API int hsv_state_scale(hsv_state st, double a_re, double a_im);
+
+/* ---- hot path --------------------------------------------------------- */
+/* out <- H|in> over all rows (spmspv, sparse.py:177-201); |y| < prune -> 0.
+ * out must not alias in. */
+HSV_API int hsv_apply_h(hsv_op op, hsv_state in, hsv_state out, double prune);
+/* <psi|H|psi> (expectation, svengine.py:174-176). */
+HSV_API int hsv_expect_h(hsv_op op, hsv_state psi, double* e_re, double* e_im);
+/* exp(theta T)|in> for the QEB generator with occ/virt qubit masks, given
+ * c = cos(theta), s = sin(theta) computed by the caller (svengine.py:209-237).
+ * out may alias in. Raises NORM_DRIFT like svengine.py:234-236. */
+HSV_API int hsv_apply_qeb(hsv_state in, hsv_state out, uint64_t occ_mask, uint64_t virt_mask,
+                  double c, double s);
+/* T|in> (apply_generator, svengine.py:187-206). out must not alias in. */
+HSV_API int hsv_apply_generator(hsv_state in, hsv_state out, uint64_t occ_mask, uint64_t virt_mask);
+/* Pool gradients g_k = 2 Re <H psi | T_k psi> for M operators plus the
+ * energy <psi|H|psi> (SvAdaptEngine.energy + .screen, adapt.py:205-214). */
+HSV_API int hsv_energy_screen(hsv_op op, hsv_state psi, const uint64_t* occ_masks,
+                      const uint64_t* virt_masks, int64_t n_ops, double* energy,
+                      double* grads);
+/* Adjoint energy + analytic gradient of exp(t_{k-1}T_{k-1})...exp(t_0 T_0)|hf>
+ * (ansatz_energy_gradient, svengine.py:260-281); cs[i], sn[i] = cos/sin(theta_i). */
+HSV_API int hsv_energy_gradient(hsv_op op, uint64_t hf_key, const uint64_t* occ_masks,
+                        const uint64_t* virt_masks, const double* cs, const double* sn,
+                        int64_t k, double* energy, double* grads);
+/* Owner-computes shard variants for multi-GPU (rows = alpha-strings
+ * [a_lo, a_hi)).  Write, without synchronizing, to DEVICE memory:
+ *   d_out[0..1] = partial <psi|H|psi> (re, im), d_out[2..2+n_ops) = partial
+ *   gradients (already multiplied by 2).  psi must be replicated. */
+HSV_API int hsv_energy_screen_partial_async(hsv_op op, hsv_state psi, const uint64_t* occ_masks,
+                                    const uint64_t* virt_masks, int64_t n_ops,
+                                    int64_t a_lo, int64_t a_hi, double* d_out);
+/* Device pointer to the amplitude array (alpha-major, complex128) and its
+ * element count, for collectives issued by the host (e.g. NCCL all-gather). */
+HSV_API int hsv_state_device_ptr(hsv_state st, void** ptr, int64_t* n);
+/* out rows [a_lo, a_hi) <- (H in) rows; other rows untouched. */
+HSV_API int hsv_apply_h_rows_async(hsv_op op, hsv_state in, hsv_state out, int64_t a_lo,
+                           int64_t a_hi, double prune);
+
+/* ---- generic CSR x sparse vector (K1b; spmspv on arbitrary CsrMatrix) ---- */
+/* y = M x with M in CSR (int64 offsets/cols, f64 values), x dense-scattered
+ * from (x_idx, x_val, x_nnz); output is the compacted support (y != 0, or
+ * |y| >= prune) in ascending row order.  Host buffers; y buffers sized n_rows. */
+HSV_API int hsv_csr_spmspv(int64_t n_rows, int64_t n_cols, const int64_t* row_offsets,
+                   const int64_t* cols, const double* vals, int64_t nnz,
+                   const int64_t* x_idx, const double* x_val, int64_t x_nnz, double prune,
+                   int64_t* y_idx, double* y_val, int64_t* y_nnz);
+
+/* ---- generic sparse vectors (host arrays; SparseVector, sparse.py:20-245) ---- */
+/* sum over shared indices of u_val*v_val; u_idx ascending (dot, sparse.py:210-219). */
+HSV_API int hsv_vec_dot(const int64_t* u_idx, const double* u_val, int64_t nu, const int64_t* v_idx,
+                const double* v_val, int64_t nv, double* out);
+/* a*x + y merged in ascending index order, exact zeros (or |v| < prune) dropped
+ * (axpy, sparse.py:222-228); out buffers sized nx + ny. */
+HSV_API int hsv_vec_axpy(int64_t dim, double a, const int64_t* x_idx, const double* x_val, int64_t nx,
+                 const int64_t* y_idx, const double* y_val, int64_t ny, double prune,
+                 int64_t* out_idx, double* out_val, int64_t* n_out);
+/* y = a*x (divide=0, scale sparse.py:231-234) or y = x/a (divide=1, normalize :242-245). */
+HSV_API int hsv_vec_scale(const double* x, int64_t n, double a, int divide, double* y);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HSV_H_ */

@@ -1,0 +1,188 @@
+// Shared internals of libhsv: context, error plumbing, object layouts and
+// small device helpers.  See DESIGN.md for the data layout rationale.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/hsv.h"
+
+namespace hsv {
+
+constexpr int kMaxNorb = 20;          // dense alpha-major layout limit (C(20,10)^2 ~ 3.4e10 rows)
+constexpr int kBinomN = 64;
+constexpr double kSectorLeakTol = 1e-10;   // svengine.py:112
+constexpr double kNormDriftTol = 1e-9;     // svengine.py:27
+
+// ---------------------------------------------------------------- errors
+void set_error(int code, const char* fmt, ...);
+int last_code();
+
+#define HSV_TRY_CUDA(call)                                                              \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) {                                                            \
+      if (e_ == cudaErrorMemoryAllocation) {                                            \
+        cudaGetLastError();                                                             \
+        ::hsv::set_error(HSV_ERR_OOM, "device allocation failed (%s) at %s:%d",         \
+                         cudaGetErrorString(e_), __FILE__, __LINE__);                   \
+        return HSV_ERR_OOM;                                                             \
+      }                                                                                 \
+      ::hsv::set_error(HSV_ERR_CUDA, "CUDA error '%s' in %s at %s:%d",                  \
+                       cudaGetErrorString(e_), #call, __FILE__, __LINE__);              \
+      return HSV_ERR_CUDA;                                                              \
+    }                                                                                   \
+  } while (0)
+
+#define HSV_CHECK_LAUNCH() HSV_TRY_CUDA(cudaGetLastError())
+
+#define HSV_TRY(expr)             \
+  do {                            \
+    int rc_ = (expr);             \
+    if (rc_ != HSV_OK) return rc_; \
+  } while (0)
+
+#define HSV_REQUIRE(cond, code, ...)              \
+  do {                                            \
+    if (!(cond)) {                                \
+      ::hsv::set_error((code), __VA_ARGS__);      \
+      return (code);                              \
+    }                                             \
+  } while (0)
+
+// --------------------------------------------------------------- context
+struct Context {
+  int device = -1;
+  cudaStream_t stream = nullptr;   // stream all work goes to
+  cudaStream_t own = nullptr;      // library-owned stream
+  int num_sms = 148;
+  int64_t launches = 0;
+};
+Context& ctx();
+int ensure_init();
+inline cudaStream_t stream() { return ctx().stream; }
+inline void count_launch(int n = 1) { ctx().launches += n; }
+
+// stream-ordered allocation from the device pool
+template <typename T>
+int dalloc(T** p, size_t n) {
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), n * sizeof(T), stream());
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error(HSV_ERR_OOM, "device allocation of %zu bytes failed: %s", n * sizeof(T),
+              cudaGetErrorString(e));
+    return HSV_ERR_OOM;
+  }
+  return HSV_OK;
+}
+template <typename T>
+void dfree(T* p) {
+  if (p) cudaFreeAsync(p, stream());
+}
+int stream_sync();   // stream sync + error mapping
+
+// ------------------------------------------------------------- binomials
+struct BinomTable {
+  int64_t c[kBinomN][kBinomN];
+};
+const BinomTable& binom_host();
+__device__ __forceinline__ int64_t dbinom(const int64_t* tab, int n, int k);
+
+}  // namespace hsv
+
+// ---------------------------------------------------------------- objects
+// Sector: (n_alpha, n_beta) strings of norb spatial orbitals.  Compressed
+// strings (bit p = spatial orbital p of that spin) are ranked in ascending
+// order; the internal row index of (sa, sb) is Ra[sa] * Nb + Rb[sb].
+struct hsv_sector_s {
+  int n_qubits = 0, norb = 0, n_alpha = 0, n_beta = 0, ordering = 0;
+  int64_t Na = 0, Nb = 0, dim = 0;
+  int wide = 0;                     // 0: 32-bit packed words (norb<=16), 1: 64-bit
+  int qa[32] = {0}, qb[32] = {0};   // qubit carrying alpha/beta orbital p
+  std::vector<uint32_t> Sa, Sb;     // host: compressed string of each rank
+  std::vector<uint32_t> Ra, Rb;     // host: rank of each compressed string (or ~0u)
+  uint32_t *d_Sa = nullptr, *d_Sb = nullptr, *d_Ra = nullptr, *d_Rb = nullptr;
+  int64_t* d_perm = nullptr;        // internal row -> reference position
+  int64_t* d_iperm = nullptr;       // reference position -> internal row
+  int64_t* d_binom = nullptr;       // kBinomN x kBinomN
+  int8_t* d_spin = nullptr;         // spin of each qubit (0 alpha, 1 beta)
+  int32_t *d_aslot = nullptr, *d_bslot = nullptr;  // alpha/beta qubits below q
+  uint32_t compress_a(uint64_t key) const {
+    uint32_t s = 0;
+    for (int p = 0; p < norb; ++p) s |= (uint32_t)((key >> qa[p]) & 1ull) << p;
+    return s;
+  }
+  uint32_t compress_b(uint64_t key) const {
+    uint32_t s = 0;
+    for (int p = 0; p < norb; ++p) s |= (uint32_t)((key >> qb[p]) & 1ull) << p;
+    return s;
+  }
+  uint64_t expand(uint32_t sa, uint32_t sb) const {
+    uint64_t k = 0;
+    for (int p = 0; p < norb; ++p) {
+      k |= (uint64_t)((sa >> p) & 1u) << qa[p];
+      k |= (uint64_t)((sb >> p) & 1u) << qb[p];
+    }
+    return k;
+  }
+};
+
+// Matrix-free operator.  Off-diagonal x-groups that can map the sector into
+// itself are bucketed by their alpha flip part; the diagonal group (x = 0) is
+// pre-evaluated into a dense per-row table.
+struct Term {          // 16 B: one pre-signed coefficient and its packed z mask
+  double c;            // coeff * (-1)^(nY/2)   (svengine.py:140-144)
+  uint64_t z;          // packed z: za | zb << SH
+};
+struct hsv_op_s {
+  hsv_sector sec = nullptr;
+  int64_t n_terms = 0, n_groups = 0, n_active = 0, n_buckets = 0;
+  int4* d_buckets = nullptr;   // {xa, xa_pop/2, g0, g1}
+  int4* d_groups = nullptr;    // {xb, xb_pop/2, t0, t1}
+  Term* d_terms = nullptr;
+  double* d_diag = nullptr;    // per internal row; nullptr if no diagonal terms
+  // host copies of the active group table (for CSR materialization)
+  std::vector<int4> buckets, groups;
+  std::vector<Term> terms;
+};
+
+struct hsv_state_s {
+  hsv_sector sec = nullptr;
+  double2* d_amp = nullptr;    // dim complex128, alpha-major internal order
+  double* d_norm2 = nullptr;   // cached <psi|psi> (device scalar)
+  bool norm2_valid = false;
+};
+
+namespace hsv {
+// Device helpers --------------------------------------------------------
+__device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ int popc(uint32_t v) { return __popc(v); }
+__device__ __forceinline__ int popc(uint64_t v) { return __popcll(v); }
+
+__device__ __forceinline__ int64_t dbinom(const int64_t* tab, int n, int k) {
+  return (k < 0 || n < 0 || k > n) ? 0 : tab[n * kBinomN + k];
+}
+
+// Deterministic block reductions (fixed shuffle tree + fixed smem order).
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Launch helpers
+int reduce_sum_f64(const double* d_in, int64_t n, int64_t stride, int64_t count,
+                   double* d_out);   // d_out[j] = sum_i d_in[i*stride + j], j<count
+int state_norm2_async(hsv_state st);
+int state_fill_zero_async(hsv_state st);
+}  // namespace hsv

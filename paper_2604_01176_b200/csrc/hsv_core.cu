@@ -1,0 +1,329 @@
+// libhsv core: context/errors, sectors (CiBasis replacement), states
+// (SparseVector replacement) and deterministic reductions.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+
+#include "hsv_common.cuh"
+
+namespace hsv {
+
+// ---------------------------------------------------------------- errors
+static thread_local std::string g_err;
+static thread_local int g_code = HSV_OK;
+
+void set_error(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  g_code = code;
+}
+int last_code() { return g_code; }
+
+// --------------------------------------------------------------- context
+static Context g_ctx;
+Context& ctx() { return g_ctx; }
+
+int ensure_init() {
+  if (g_ctx.device >= 0) return HSV_OK;
+  int dev = 0;
+  HSV_TRY_CUDA(cudaGetDevice(&dev));
+  return hsv_init(dev);
+}
+
+int stream_sync() {
+  cudaError_t e = cudaStreamSynchronize(stream());
+  if (e != cudaSuccess) {
+    set_error(HSV_ERR_CUDA, "CUDA error during stream synchronize: %s", cudaGetErrorString(e));
+    return HSV_ERR_CUDA;
+  }
+  return HSV_OK;
+}
+
+const BinomTable& binom_host() {
+  static BinomTable t;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    memset(&t, 0, sizeof(t));
+    for (int n = 0; n < kBinomN; ++n) {
+      t.c[n][0] = 1;
+      for (int k = 1; k <= n; ++k) t.c[n][k] = t.c[n - 1][k - 1] + (k <= n - 1 ? t.c[n - 1][k] : 0);
+    }
+  });
+  return t;
+}
+
+// ------------------------------------------------------------ reductions
+// Column sums of a row-major [n x stride] array, fixed summation order.
+// Coalesced variant: one thread per column, sequential over a chunk of rows.
+__global__ void k_colsum_seq(const double* __restrict__ in, int64_t n, int64_t stride,
+                             int64_t count, int64_t chunk, double* __restrict__ out) {
+  int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t c = blockIdx.y;
+  if (j >= count) return;
+  int64_t i0 = c * chunk, i1 = min(n, i0 + chunk);
+  double acc = 0.0;
+  for (int64_t i = i0; i < i1; ++i) acc += in[i * stride + j];
+  out[c * count + j] = acc;
+}
+// Tree variant for few columns: a block reduces `chunk` rows of one column.
+__global__ void k_colsum_tree(const double* __restrict__ in, int64_t n, int64_t stride,
+                              int64_t count, int64_t chunk, double* __restrict__ out) {
+  __shared__ double sh[32];
+  int64_t j = blockIdx.x;
+  int64_t c = blockIdx.y;
+  int64_t i0 = c * chunk, i1 = min(n, i0 + chunk);
+  double acc = 0.0;
+  for (int64_t i = i0 + threadIdx.x; i < i1; i += blockDim.x) acc += in[i * stride + j];
+  acc = warp_sum(acc);
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = acc;
+  __syncthreads();
+  if (w == 0) {
+    double v = (l < (int)(blockDim.x >> 5)) ? sh[l] : 0.0;
+    v = warp_sum(v);
+    if (l == 0) out[c * count + j] = v;
+  }
+}
+
+int reduce_sum_f64(const double* d_in, int64_t n, int64_t stride, int64_t count, double* d_out) {
+  if (count <= 0) return HSV_OK;
+  if (n <= 0) {
+    HSV_TRY_CUDA(cudaMemsetAsync(d_out, 0, count * sizeof(double), stream()));
+    return HSV_OK;
+  }
+  const bool seq = count >= 64;
+  const int64_t chunk = seq ? 256 : 8192;
+  const double* src = d_in;
+  int64_t src_n = n, src_stride = stride;
+  double* tmp[2] = {nullptr, nullptr};
+  int ping = 0;
+  while (true) {
+    int64_t nch = (src_n + chunk - 1) / chunk;
+    double* dst;
+    if (nch == 1) {
+      dst = d_out;
+    } else {
+      if (!tmp[ping]) HSV_TRY(dalloc(&tmp[ping], (size_t)nch * count));
+      dst = tmp[ping];
+    }
+    if (seq) {
+      dim3 grid((unsigned)((count + 127) / 128), (unsigned)nch);
+      k_colsum_seq<<<grid, 128, 0, stream()>>>(src, src_n, src_stride, count, chunk, dst);
+    } else {
+      dim3 grid((unsigned)count, (unsigned)nch);
+      k_colsum_tree<<<grid, 256, 0, stream()>>>(src, src_n, src_stride, count, chunk, dst);
+    }
+    count_launch();
+    HSV_CHECK_LAUNCH();
+    if (nch == 1) break;
+    src = dst;
+    src_n = nch;
+    src_stride = count;
+    ping ^= 1;
+  }
+  dfree(tmp[0]);
+  dfree(tmp[1]);
+  return HSV_OK;
+}
+
+// ---------------------------------------------------------------- sector
+// Reference position of every internal row: the closed-form rank of its key
+// among the ascending sector keys (equals CiBasis position, cibasis.py:126-146).
+__global__ void k_sector_perm(const uint32_t* __restrict__ Sa, const uint32_t* __restrict__ Sb,
+                              int64_t Na, int64_t Nb, int n_qubits, int n_alpha, int n_beta,
+                              const int32_t* __restrict__ qa, const int32_t* __restrict__ qb,
+                              int norb, const int8_t* __restrict__ spin,
+                              const int32_t* __restrict__ aslot, const int32_t* __restrict__ bslot,
+                              const int64_t* __restrict__ binom, int64_t* __restrict__ perm,
+                              int64_t* __restrict__ iperm) {
+  int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (idx >= Na * Nb) return;
+  int64_t ra = idx / Nb, rb = idx - ra * Nb;
+  uint32_t sa = Sa[ra], sb = Sb[rb];
+  uint64_t key = 0;
+  for (int p = 0; p < norb; ++p) {
+    key |= (uint64_t)((sa >> p) & 1u) << qa[p];
+    key |= (uint64_t)((sb >> p) & 1u) << qb[p];
+  }
+  int al = n_alpha, bl = n_beta;
+  int64_t pos = 0;
+  for (int q = n_qubits - 1; q >= 0; --q) {
+    if ((key >> q) & 1ull) {
+      pos += dbinom(binom, aslot[q], al) * dbinom(binom, bslot[q], bl);
+      if (spin[q] == 0) --al; else --bl;
+    }
+  }
+  perm[idx] = pos;
+  iperm[pos] = idx;
+}
+
+}  // namespace hsv
+
+using namespace hsv;
+
+extern "C" {
+
+int hsv_abi_version(void) { return HSV_ABI_VERSION; }
+
+int hsv_last_error(char* buf, size_t n) {
+  if (buf && n) {
+    size_t m = std::min(n - 1, g_err.size());
+    memcpy(buf, g_err.data(), m);
+    buf[m] = 0;
+  }
+  return g_code;
+}
+
+int hsv_init(int device) {
+  if (g_ctx.device == device && g_ctx.stream) return HSV_OK;
+  HSV_TRY_CUDA(cudaSetDevice(device));
+  HSV_TRY_CUDA(cudaFree(0));
+  cudaDeviceProp prop;
+  HSV_TRY_CUDA(cudaGetDeviceProperties(&prop, device));
+  HSV_REQUIRE(prop.major >= 10, HSV_ERR_UNSUPPORTED,
+              "libhsv is built for sm_100a (B200); device %d is sm_%d%d", device, prop.major,
+              prop.minor);
+  g_ctx.num_sms = prop.multiProcessorCount;
+  if (!g_ctx.own) HSV_TRY_CUDA(cudaStreamCreateWithFlags(&g_ctx.own, cudaStreamNonBlocking));
+  g_ctx.stream = g_ctx.own;
+  g_ctx.device = device;
+  cudaMemPool_t pool;
+  HSV_TRY_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = UINT64_MAX;
+  HSV_TRY_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  return HSV_OK;
+}
+
+int hsv_set_stream(void* s) {
+  HSV_TRY(ensure_init());
+  g_ctx.stream = s ? reinterpret_cast<cudaStream_t>(s) : g_ctx.own;
+  return HSV_OK;
+}
+void* hsv_get_stream(void) {
+  if (ensure_init() != HSV_OK) return nullptr;
+  return reinterpret_cast<void*>(g_ctx.stream);
+}
+int64_t hsv_launch_count(int reset) {
+  int64_t n = g_ctx.launches;
+  if (reset) g_ctx.launches = 0;
+  return n;
+}
+int hsv_synchronize(void) {
+  HSV_TRY(ensure_init());
+  return stream_sync();
+}
+
+// ---------------------------------------------------------------- sector
+int hsv_sector_create(int n_qubits, int n_alpha, int n_beta, int ordering, hsv_sector* out) {
+  HSV_TRY(ensure_init());
+  HSV_REQUIRE(out, HSV_ERR_INVALID, "null output handle");
+  HSV_REQUIRE(ordering == HSV_INTERLEAVED || ordering == HSV_BLOCKED, HSV_ERR_INVALID,
+              "unknown ordering %d; expected interleaved (0) or blocked (1)", ordering);
+  HSV_REQUIRE(n_qubits > 0 && n_qubits % 2 == 0, HSV_ERR_INVALID,
+              "n_qubits must be even (spin orbital pairs)");
+  const int norb = n_qubits / 2;
+  HSV_REQUIRE(0 <= n_alpha && n_alpha <= norb && 0 <= n_beta && n_beta <= norb, HSV_ERR_INVALID,
+              "per-spin occupation exceeds the orbital count");
+  HSV_REQUIRE(norb <= kMaxNorb, HSV_ERR_UNSUPPORTED,
+              "n_qubits=%d exceeds the dense device layout limit (%d spatial orbitals)", n_qubits,
+              kMaxNorb);
+  auto* s = new hsv_sector_s();
+  s->n_qubits = n_qubits;
+  s->norb = norb;
+  s->n_alpha = n_alpha;
+  s->n_beta = n_beta;
+  s->ordering = ordering;
+  s->wide = norb > 16 ? 1 : 0;
+  for (int p = 0; p < norb; ++p) {
+    // cibasis.py:37-41 qubit_index
+    s->qa[p] = ordering == HSV_INTERLEAVED ? 2 * p : p;
+    s->qb[p] = ordering == HSV_INTERLEAVED ? 2 * p + 1 : p + norb;
+  }
+  const uint32_t nv = 1u << norb;
+  s->Ra.assign(nv, ~0u);
+  s->Rb.assign(nv, ~0u);
+  for (uint32_t v = 0; v < nv; ++v) {
+    int pc = __builtin_popcount(v);
+    if (pc == n_alpha) { s->Ra[v] = (uint32_t)s->Sa.size(); s->Sa.push_back(v); }
+    if (pc == n_beta) { s->Rb[v] = (uint32_t)s->Sb.size(); s->Sb.push_back(v); }
+  }
+  s->Na = (int64_t)s->Sa.size();
+  s->Nb = (int64_t)s->Sb.size();
+  s->dim = s->Na * s->Nb;
+
+  int rc = HSV_OK;
+  auto fail = [&](int code) { hsv_sector_destroy(s); return code; };
+  if ((rc = dalloc(&s->d_Sa, s->Na)) || (rc = dalloc(&s->d_Sb, s->Nb)) ||
+      (rc = dalloc(&s->d_Ra, nv)) || (rc = dalloc(&s->d_Rb, nv)) ||
+      (rc = dalloc(&s->d_perm, s->dim)) || (rc = dalloc(&s->d_iperm, s->dim)) ||
+      (rc = dalloc(&s->d_binom, kBinomN * kBinomN)) || (rc = dalloc(&s->d_spin, 64)) ||
+      (rc = dalloc(&s->d_aslot, 64)) || (rc = dalloc(&s->d_bslot, 64)))
+    return fail(rc);
+  std::vector<int8_t> spin(64, 0);
+  std::vector<int32_t> aslot(64, 0), bslot(64, 0), qa(32), qb(32);
+  for (int q = 0; q < n_qubits; ++q)
+    spin[q] = ordering == HSV_INTERLEAVED ? (q & 1) : (q < norb ? 0 : 1);
+  int na = 0, nb = 0;
+  for (int q = 0; q < n_qubits; ++q) {
+    aslot[q] = na;
+    bslot[q] = nb;
+    if (spin[q] == 0) ++na; else ++nb;
+  }
+  for (int p = 0; p < 32; ++p) { qa[p] = s->qa[p]; qb[p] = s->qb[p]; }
+  int32_t *d_qa = nullptr, *d_qb = nullptr;
+  if ((rc = dalloc(&d_qa, 32)) || (rc = dalloc(&d_qb, 32))) return fail(rc);
+  cudaStream_t st = stream();
+  cudaError_t e = cudaSuccess;
+  e = e ? e : cudaMemcpyAsync(s->d_Sa, s->Sa.data(), s->Na * 4, cudaMemcpyHostToDevice, st);
+  e = e ? e : cudaMemcpyAsync(s->d_Sb, s->Sb.data(), s->Nb * 4, cudaMemcpyHostToDevice, st);
+  e = e ? e : cudaMemcpyAsync(s->d_Ra, s->Ra.data(), nv * 4ull, cudaMemcpyHostToDevice, st);
+  e = e ? e : cudaMemcpyAsync(s->d_Rb, s->Rb.data(), nv * 4ull, cudaMemcpyHostToDevice, st);
+  e = e ? e : cudaMemcpyAsync(s->d_binom, binom_host().c, sizeof(BinomTable), cudaMemcpyHostToDevice, st);
+  e = e ? e : cudaMemcpyAsync(s->d_spin, spin.data(), 64, cudaMemcpyHostToDevice, st);
+  e = e ? e : cudaMemcpyAsync(s->d_aslot, aslot.data(), 64 * 4, cudaMemcpyHostToDevice, st);
+  e = e ? e : cudaMemcpyAsync(s->d_bslot, bslot.data(), 64 * 4, cudaMemcpyHostToDevice, st);
+  e = e ? e : cudaMemcpyAsync(d_qa, qa.data(), 32 * 4, cudaMemcpyHostToDevice, st);
+  e = e ? e : cudaMemcpyAsync(d_qb, qb.data(), 32 * 4, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) {
+    set_error(HSV_ERR_CUDA, "sector upload failed: %s", cudaGetErrorString(e));
+    return fail(HSV_ERR_CUDA);
+  }
+  if (s->dim > 0) {
+    int64_t nblk = (s->dim + 255) / 256;
+    k_sector_perm<<<(unsigned)nblk, 256, 0, st>>>(s->d_Sa, s->d_Sb, s->Na, s->Nb, n_qubits,
+                                                  n_alpha, n_beta, d_qa, d_qb, norb, s->d_spin,
+                                                  s->d_aslot, s->d_bslot, s->d_binom,
+                                                  s->d_perm, s->d_iperm);
+    count_launch();
+  }
+  dfree(d_qa);
+  dfree(d_qb);
+  if ((rc = stream_sync())) return fail(rc);
+  *out = s;
+  return HSV_OK;
+}
+
+int hsv_sector_destroy(hsv_sector s) {
+  if (!s) return HSV_OK;
+  dfree(s->d_Sa); dfree(s->d_Sb); dfree(s->d_Ra); dfree(s->d_Rb);
+  dfree(s->d_perm); dfree(s->d_iperm); dfree(s->d_binom); dfree(s->d_spin);
+  dfree(s->d_aslot); dfree(s->d_bslot);
+  delete s;
+  return HSV_OK;
+}
+
+int64_t hsv_sector_dim(hsv_sector s) { return s ? s->dim : -1; }
+
+int hsv_sector_shape(hsv_sector s, int64_t* na, int64_t* nb) {
+  HSV_REQUIRE(s, HSV_ERR_INVALID, "null sector");
+  if (na) *na = s->Na;
+  if (nb) *nb = s->Nb;
+  return HSV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,53 @@
+// Kernel argument blocks and cross-file launch helpers.
+#pragma once
+#include "hsv_common.cuh"
+
+namespace hsv {
+
+constexpr int kApplyR = 2;   // rows per lane in the K1 apply kernel
+
+struct ApplyArgs {
+  const uint32_t* Sa;
+  const uint32_t* Sb;
+  const uint32_t* Ra;
+  const uint32_t* Rb;
+  const int4* buckets;
+  int n_buckets;
+  const int4* groups;
+  const Term* terms;
+  const double* diag;
+  const double2* psi;
+  double2* out;      // nullptr: energy only
+  double* epart;     // [warps][2] energy partials or nullptr
+  int64_t Nb;
+  int64_t a_lo, a_hi;
+  int64_t units;
+  int upr;
+  double prune;
+  int energy_only;
+};
+
+int grid_for(int64_t n, int block);
+int apply_warps(const hsv_op_s* op);
+int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* epart,
+                 int64_t a_lo, int64_t a_hi, double prune, int energy_only, int64_t* n_warps);
+
+// Compressed QEB masks of one excitation operator.
+struct OpMasks {
+  uint32_t oa, va, ob, vb;
+};
+OpMasks compress_op(const hsv_sector_s* s, uint64_t occ, uint64_t virt);
+int64_t src_count(int norb, int n, uint32_t occ, uint32_t virt);
+
+// Device scratch for pair lists (src rank, partner rank) of one operator.
+struct PairLists {
+  int2* la = nullptr;
+  int2* lb = nullptr;
+  int64_t ca = 0, cb = 0;
+};
+int build_pair_lists_async(const hsv_sector_s* s, const OpMasks& m, PairLists& pl);
+
+int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w, const int4* d_ops,
+                  int n_ops, int64_t row_lo, int64_t row_hi, double* d_grads);
+
+}  // namespace hsv

@@ -1,0 +1,408 @@
+// K3 / K5: qubit-excitation (QEB) rotations, generator application and the
+// fused adjoint energy+gradient sweep (svengine.py:179-281).
+//
+// A QEB generator T with occupied set O and virtual set V couples a source
+// row b (O set, V clear) with its partner p = b ^ (O|V) (V set, O clear):
+//   T|b> = +|p>,  T|p> = -|b>;  exp(theta T) is a Givens rotation per pair.
+// Source rows are enumerated without scanning the sector: the alpha and beta
+// halves of a source row are independent, so the pair set is the product of
+// an alpha list (ranks of matching alpha strings and their partners) and a
+// beta list.  One thread handles one pair and touches only 2 rows.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+
+#include "hsv_common.cuh"
+#include "hsv_kernels.cuh"
+
+namespace hsv {
+
+OpMasks compress_op(const hsv_sector_s* s, uint64_t occ, uint64_t virt) {
+  return OpMasks{s->compress_a(occ), s->compress_a(virt), s->compress_b(occ),
+                 s->compress_b(virt)};
+}
+
+int64_t src_count(int norb, int n, uint32_t occ, uint32_t virt) {
+  const int po = __builtin_popcount(occ), pv = __builtin_popcount(virt);
+  const int free_pos = norb - po - pv, ones = n - po;
+  if (free_pos < 0 || ones < 0 || ones > free_pos) return 0;
+  return binom_host().c[free_pos][ones];
+}
+
+// One block per spin: deterministic (rank-ascending) compaction of the
+// strings in source pattern, paired with their partner ranks.
+__global__ void __launch_bounds__(1024) k_pair_list(const uint32_t* __restrict__ Sa,
+                                                    const uint32_t* __restrict__ Sb,
+                                                    const uint32_t* __restrict__ Ra,
+                                                    const uint32_t* __restrict__ Rb, int64_t Na,
+                                                    int64_t Nb, OpMasks m, int2* __restrict__ la,
+                                                    int2* __restrict__ lb) {
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int base_sh;
+  const bool alpha = blockIdx.x == 0;
+  const uint32_t* S = alpha ? Sa : Sb;
+  const uint32_t* R = alpha ? Ra : Rb;
+  const int64_t N = alpha ? Na : Nb;
+  const uint32_t occ = alpha ? m.oa : m.ob, virt = alpha ? m.va : m.vb;
+  const uint32_t flip = occ | virt;
+  int2* out = alpha ? la : lb;
+  int base = 0;
+  for (int64_t c0 = 0; c0 < N; c0 += 1024) {
+    const int64_t i = c0 + threadIdx.x;
+    uint32_t s = 0;
+    int f = 0;
+    if (i < N) {
+      s = S[i];
+      f = ((s & occ) == occ && (s & virt) == 0) ? 1 : 0;
+    }
+    int off, tot;
+    Scan(tmp).ExclusiveSum(f, off, tot);
+    if (f) out[base + off] = make_int2((int)i, (int)R[s ^ flip]);
+    base += tot;
+    __syncthreads();
+  }
+  (void)base_sh;
+}
+
+int build_pair_lists_async(const hsv_sector_s* s, const OpMasks& m, PairLists& pl) {
+  pl.ca = src_count(s->norb, s->n_alpha, m.oa, m.va);
+  pl.cb = src_count(s->norb, s->n_beta, m.ob, m.vb);
+  if (!pl.la) HSV_TRY(dalloc(&pl.la, s->Na));
+  if (!pl.lb) HSV_TRY(dalloc(&pl.lb, s->Nb));
+  if (pl.ca == 0 || pl.cb == 0) return HSV_OK;
+  k_pair_list<<<2, 1024, 0, stream()>>>(s->d_Sa, s->d_Sb, s->d_Ra, s->d_Rb, s->Na, s->Nb, m,
+                                        pl.la, pl.lb);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  return HSV_OK;
+}
+
+// ------------------------------------------------------------ pair kernels
+enum PairMode { kRotate = 0, kGenerator = 1, kAdjoint = 2 };
+
+struct PairArgs {
+  const int2* la;
+  const int2* lb;
+  int64_t cb, Nb;
+  double2* psi;          // rotated in place (kRotate / kAdjoint uncompute)
+  double2* lam;          // kAdjoint: adjoint state (rotated in place); kGenerator: output
+  const double2* src;    // kGenerator: input state
+  double c, s;           // rotation (already -theta for the adjoint sweep)
+  double* part;          // per-block partials
+  unsigned int* counter; // last-block detection (zero on entry, reset on exit)
+  double* norm2;         // kRotate: <psi|psi>; kAdjoint: <lam|lam> (in/out)
+  double* result;        // kAdjoint: gradient slot
+  int* err;              // set to 1 on norm drift
+  double* err_val;
+  int uncompute;
+};
+
+__device__ __forceinline__ void givens(double2 vb, double2 vp, double c, double s, double2& nb,
+                                       double2& np) {
+  // exact two-term sums with separate roundings, as SparseVector.from_entries
+  // merges (c*v_own) with (+-sin*v_partner) (svengine.py:219-233)
+  nb.x = __dadd_rn(__dmul_rn(c, vb.x), __dmul_rn(-s, vp.x));
+  nb.y = __dadd_rn(__dmul_rn(c, vb.y), __dmul_rn(-s, vp.y));
+  np.x = __dadd_rn(__dmul_rn(c, vp.x), __dmul_rn(s, vb.x));
+  np.y = __dadd_rn(__dmul_rn(c, vp.y), __dmul_rn(s, vb.y));
+}
+
+// Block partials then a deterministic last-block reduction (fixed order).
+template <int NV>
+__device__ bool last_block_sum(double (&v)[NV], double* __restrict__ part,
+                               unsigned int* counter, double (&tot)[NV]) {
+  __shared__ double sh[NV][32];
+  __shared__ bool amlast;
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const unsigned nblocks = gridDim.x * gridDim.y;
+  const unsigned bid = blockIdx.y * gridDim.x + blockIdx.x;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    double x = warp_sum(v[j]);
+    if (l == 0) sh[j][w] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      double x = 0.0;
+      for (int q = 0; q < nw; ++q) x += sh[j][q];
+      part[(int64_t)bid * NV + j] = x;
+    }
+    __threadfence();
+    amlast = atomicAdd(counter, 1u) == nblocks - 1;
+  }
+  __syncthreads();
+  if (!amlast) return false;
+  __threadfence();
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    double x = 0.0;
+    for (unsigned i = threadIdx.x; i < nblocks; i += blockDim.x) x += __ldcg(part + (int64_t)i * NV + j);
+    x = warp_sum(x);
+    __syncthreads();
+    if (l == 0) sh[j][w] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int q = 0; q < nw; ++q) t += sh[j][q];
+      tot[j] = t;
+    }
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+  return true;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_pairs(const PairArgs a) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int2 A = a.la[blockIdx.y];
+  double v[MODE == kAdjoint ? 3 : 2];
+#pragma unroll
+  for (int q = 0; q < (MODE == kAdjoint ? 3 : 2); ++q) v[q] = 0.0;
+  if (j < a.cb) {
+    const int2 B = a.lb[j];
+    const int64_t ib = (int64_t)A.x * a.Nb + B.x;   // source row
+    const int64_t ip = (int64_t)A.y * a.Nb + B.y;   // partner (target pattern)
+    if (MODE == kRotate) {
+      const double2 vb = a.psi[ib], vp = a.psi[ip];
+      double2 nb, np;
+      givens(vb, vp, a.c, a.s, nb, np);
+      a.psi[ib] = nb;
+      a.psi[ip] = np;
+      v[0] = vb.x * vb.x + vb.y * vb.y + vp.x * vp.x + vp.y * vp.y;
+      v[1] = nb.x * nb.x + nb.y * nb.y + np.x * np.x + np.y * np.y;
+    } else if (MODE == kGenerator) {
+      // source b -> +v_b at p; target p -> -v_p at b (svengine.py:196-203)
+      const double2 vb = a.src[ib], vp = a.src[ip];
+      a.lam[ip] = vb;
+      a.lam[ib] = make_double2(-vp.x, -vp.y);
+    } else {
+      const double2 pb = a.psi[ib], pp = a.psi[ip];
+      const double2 lb = a.lam[ib], lp = a.lam[ip];
+      // <lam| T psi>: (T psi)_b = -psi_p, (T psi)_p = +psi_b
+      v[0] = (lp.x * pb.x + lp.y * pb.y) - (lb.x * pp.x + lb.y * pp.y);
+      double2 nb, np;
+      givens(lb, lp, a.c, a.s, nb, np);
+      a.lam[ib] = nb;
+      a.lam[ip] = np;
+      v[1] = lb.x * lb.x + lb.y * lb.y + lp.x * lp.x + lp.y * lp.y;
+      v[2] = nb.x * nb.x + nb.y * nb.y + np.x * np.x + np.y * np.y;
+      if (a.uncompute) {
+        double2 qb, qp;
+        givens(pb, pp, a.c, a.s, qb, qp);
+        a.psi[ib] = qb;
+        a.psi[ip] = qp;
+      }
+    }
+  }
+  if (MODE == kGenerator) return;
+  constexpr int NV = MODE == kAdjoint ? 3 : 2;
+  double tot[NV];
+  if (last_block_sum<NV>(v, a.part, a.counter, tot) && threadIdx.x == 0) {
+    const double dold = MODE == kAdjoint ? tot[1] : tot[0];
+    const double dnew = MODE == kAdjoint ? tot[2] : tot[1];
+    const double n2 = *a.norm2;
+    const double n2new = n2 - dold + dnew;
+    const double nrm = sqrt(fmax(n2, 0.0));
+    const double drift = fabs(sqrt(fmax(n2new, 0.0)) - nrm);
+    if (drift > kNormDriftTol * fmax(1.0, nrm)) {   // svengine.py:234-236
+      if (atomicExch(a.err, 1) == 0) *a.err_val = drift;
+    }
+    *a.norm2 = n2new;
+    if (MODE == kAdjoint) *a.result = 2.0 * tot[0];
+  }
+}
+
+template <int MODE>
+static int launch_pairs(const PairLists& pl, PairArgs a, int64_t* nblocks_out = nullptr) {
+  if (pl.ca == 0 || pl.cb == 0) {
+    if (nblocks_out) *nblocks_out = 0;
+    return HSV_OK;
+  }
+  a.la = pl.la;
+  a.lb = pl.lb;
+  a.cb = pl.cb;
+  dim3 grid((unsigned)((pl.cb + 255) / 256), (unsigned)pl.ca);
+  HSV_REQUIRE(pl.ca <= 65535, HSV_ERR_UNSUPPORTED, "alpha pair list too long (%lld)",
+              (long long)pl.ca);
+  if (nblocks_out) *nblocks_out = (int64_t)grid.x * grid.y;
+  k_pairs<MODE><<<grid, 256, 0, stream()>>>(a);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  return HSV_OK;
+}
+
+static int64_t max_pair_blocks(const hsv_sector_s* s) {
+  return ((s->Nb + 255) / 256) * std::max<int64_t>(1, s->Na);
+}
+
+// Scratch shared by the pair launches of one API call.
+struct PairScratch {
+  double* part = nullptr;
+  unsigned int* counter = nullptr;
+  int* err = nullptr;
+  double* err_val = nullptr;
+  int init(const hsv_sector_s* s, int nv) {
+    HSV_TRY(dalloc(&part, max_pair_blocks(s) * nv));
+    HSV_TRY(dalloc(&counter, 1));
+    HSV_TRY(dalloc(&err, 1));
+    HSV_TRY(dalloc(&err_val, 1));
+    HSV_TRY_CUDA(cudaMemsetAsync(counter, 0, sizeof(unsigned), stream()));
+    HSV_TRY_CUDA(cudaMemsetAsync(err, 0, sizeof(int), stream()));
+    HSV_TRY_CUDA(cudaMemsetAsync(err_val, 0, sizeof(double), stream()));
+    return HSV_OK;
+  }
+  void release() { dfree(part); dfree(counter); dfree(err); dfree(err_val); }
+  int check() {
+    int h_err = 0;
+    double h_val = 0.0;
+    HSV_TRY_CUDA(cudaMemcpyAsync(&h_err, err, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    HSV_TRY_CUDA(cudaMemcpyAsync(&h_val, err_val, sizeof(double), cudaMemcpyDeviceToHost, stream()));
+    HSV_TRY(stream_sync());
+    HSV_REQUIRE(!h_err, HSV_ERR_NORM_DRIFT, "norm drift %.3e in qeb exponential", h_val);
+    return HSV_OK;
+  }
+};
+
+}  // namespace hsv
+
+using namespace hsv;
+
+extern "C" {
+
+int hsv_apply_qeb(hsv_state in, hsv_state out, uint64_t occ, uint64_t virt, double c, double s) {
+  HSV_REQUIRE(in && out && in->sec == out->sec, HSV_ERR_INVALID, "dimension mismatch");
+  HSV_REQUIRE((occ & virt) == 0 && occ && virt, HSV_ERR_INVALID, "excitation indices must be distinct");
+  if (out != in) {
+    HSV_TRY_CUDA(cudaMemcpyAsync(out->d_amp, in->d_amp, in->sec->dim * sizeof(double2),
+                                 cudaMemcpyDeviceToDevice, stream()));
+    HSV_TRY_CUDA(cudaMemcpyAsync(out->d_norm2, in->d_norm2, sizeof(double),
+                                 cudaMemcpyDeviceToDevice, stream()));
+    out->norm2_valid = in->norm2_valid;
+  }
+  if (c == 1.0 && s == 0.0) return stream_sync();   // theta == 0 returns the input (svengine.py:212)
+  if (!out->norm2_valid) HSV_TRY(state_norm2_async(out));
+  const hsv_sector_s* sec = out->sec;
+  PairLists pl;
+  PairScratch sc;
+  HSV_TRY(sc.init(sec, 2));
+  HSV_TRY(build_pair_lists_async(sec, compress_op(sec, occ, virt), pl));
+  PairArgs a{};
+  a.Nb = sec->Nb; a.psi = out->d_amp; a.c = c; a.s = s;
+  a.part = sc.part; a.counter = sc.counter; a.norm2 = out->d_norm2;
+  a.err = sc.err; a.err_val = sc.err_val;
+  HSV_TRY(launch_pairs<kRotate>(pl, a));
+  int rc = sc.check();
+  dfree(pl.la); dfree(pl.lb);
+  sc.release();
+  out->norm2_valid = true;
+  return rc;
+}
+
+int hsv_apply_generator(hsv_state in, hsv_state out, uint64_t occ, uint64_t virt) {
+  HSV_REQUIRE(in && out && in->sec == out->sec, HSV_ERR_INVALID, "dimension mismatch");
+  HSV_REQUIRE(in != out, HSV_ERR_INVALID, "hsv_apply_generator: output must not alias input");
+  HSV_REQUIRE((occ & virt) == 0 && occ && virt, HSV_ERR_INVALID, "excitation indices must be distinct");
+  const hsv_sector_s* sec = in->sec;
+  HSV_TRY(state_fill_zero_async(out));
+  PairLists pl;
+  HSV_TRY(build_pair_lists_async(sec, compress_op(sec, occ, virt), pl));
+  PairArgs a{};
+  a.Nb = sec->Nb; a.src = in->d_amp; a.lam = out->d_amp;
+  HSV_TRY(launch_pairs<kGenerator>(pl, a));
+  dfree(pl.la); dfree(pl.lb);
+  out->norm2_valid = false;
+  return stream_sync();
+}
+
+int hsv_energy_gradient(hsv_op op, uint64_t hf_key, const uint64_t* occ, const uint64_t* virt,
+                        const double* cs, const double* sn, int64_t k, double* energy,
+                        double* grads) {
+  HSV_REQUIRE(op && energy && (k == 0 || (occ && virt && cs && sn && grads)), HSV_ERR_INVALID,
+              "null argument");
+  const hsv_sector_s* sec = op->sec;
+  const int64_t dim = sec->dim;
+  // psi <- |hf>
+  uint32_t sa = sec->compress_a(hf_key), sb = sec->compress_b(hf_key);
+  HSV_REQUIRE((sec->n_qubits >= 64 || (hf_key >> sec->n_qubits) == 0) && sec->Ra[sa] != ~0u &&
+                  sec->Rb[sb] != ~0u,
+              HSV_ERR_SECTOR, "configuration %#llx is outside the basis sector",
+              (unsigned long long)hf_key);
+  for (int64_t i = 0; i < k; ++i)
+    HSV_REQUIRE((occ[i] & virt[i]) == 0 && occ[i] && virt[i], HSV_ERR_INVALID,
+                "excitation indices must be distinct");
+  double2 *psi = nullptr, *lam = nullptr;
+  double *d_n2 = nullptr, *d_ln2 = nullptr, *d_grad = nullptr, *d_e = nullptr, *epart = nullptr;
+  HSV_TRY(dalloc(&psi, dim));
+  HSV_TRY(dalloc(&lam, dim));
+  HSV_TRY(dalloc(&d_n2, 1));
+  HSV_TRY(dalloc(&d_ln2, 1));
+  HSV_TRY(dalloc(&d_grad, std::max<int64_t>(k, 1)));
+  HSV_TRY(dalloc(&d_e, 2));
+  const int nw = apply_warps(op);
+  HSV_TRY(dalloc(&epart, 2 * (int64_t)nw));
+  HSV_TRY_CUDA(cudaMemsetAsync(epart, 0, 2 * sizeof(double) * nw, stream()));
+  HSV_TRY_CUDA(cudaMemsetAsync(psi, 0, dim * sizeof(double2), stream()));
+  static thread_local double2 one;
+  static thread_local double n2one;
+  one = make_double2(1.0, 0.0);
+  n2one = 1.0;
+  const int64_t hidx = (int64_t)sec->Ra[sa] * sec->Nb + sec->Rb[sb];
+  HSV_TRY_CUDA(cudaMemcpyAsync(psi + hidx, &one, sizeof(double2), cudaMemcpyHostToDevice, stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_n2, &n2one, sizeof(double), cudaMemcpyHostToDevice, stream()));
+
+  PairScratch sc;
+  HSV_TRY(sc.init(sec, 3));
+  std::vector<PairLists> lists(k);
+  // forward sweep: psi <- exp(theta_i T_i) psi, in place
+  for (int64_t i = 0; i < k; ++i) {
+    HSV_TRY(build_pair_lists_async(sec, compress_op(sec, occ[i], virt[i]), lists[i]));
+    if (cs[i] == 1.0 && sn[i] == 0.0) continue;
+    PairArgs a{};
+    a.Nb = sec->Nb; a.psi = psi; a.c = cs[i]; a.s = sn[i];
+    a.part = sc.part; a.counter = sc.counter; a.norm2 = d_n2; a.err = sc.err; a.err_val = sc.err_val;
+    HSV_TRY(launch_pairs<kRotate>(lists[i], a));
+  }
+  // w = H psi (into lam), E = <psi|w>
+  int64_t used = 0;
+  HSV_TRY(launch_apply(op, psi, lam, epart, 0, sec->Na, 0.0, 0, &used));
+  HSV_TRY(reduce_sum_f64(epart, used, 2, 2, d_e));
+  if (k > 0) {
+    // <lam|lam> for the adjoint drift checks
+    hsv_state_s tmp;
+    tmp.sec = const_cast<hsv_sector_s*>(sec);
+    tmp.d_amp = lam;
+    tmp.d_norm2 = d_ln2;
+    HSV_TRY(state_norm2_async(&tmp));
+    tmp.d_amp = nullptr;
+    tmp.d_norm2 = nullptr;
+  }
+  // backward sweep (svengine.py:276-280), uncomputing psi instead of storing k+1 states
+  for (int64_t i = k - 1; i >= 0; --i) {
+    PairArgs a{};
+    a.Nb = sec->Nb; a.psi = psi; a.lam = lam; a.c = cs[i]; a.s = -sn[i];
+    a.part = sc.part; a.counter = sc.counter; a.norm2 = d_ln2; a.result = d_grad + i;
+    a.err = sc.err; a.err_val = sc.err_val; a.uncompute = i > 0;
+    if (lists[i].ca == 0 || lists[i].cb == 0) {
+      HSV_TRY_CUDA(cudaMemsetAsync(d_grad + i, 0, sizeof(double), stream()));
+      continue;
+    }
+    HSV_TRY(launch_pairs<kAdjoint>(lists[i], a));
+  }
+  double he[2] = {0, 0};
+  HSV_TRY_CUDA(cudaMemcpyAsync(he, d_e, 16, cudaMemcpyDeviceToHost, stream()));
+  if (k > 0)
+    HSV_TRY_CUDA(cudaMemcpyAsync(grads, d_grad, k * sizeof(double), cudaMemcpyDeviceToHost, stream()));
+  int rc = sc.check();
+  for (auto& pl : lists) { dfree(pl.la); dfree(pl.lb); }
+  sc.release();
+  dfree(psi); dfree(lam); dfree(d_n2); dfree(d_ln2); dfree(d_grad); dfree(d_e); dfree(epart);
+  HSV_TRY(stream_sync());
+  *energy = he[0];
+  return rc;
+}
+
+}  // extern "C"

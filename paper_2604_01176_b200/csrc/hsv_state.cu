@@ -1,0 +1,479 @@
+// States: dense complex128 amplitudes over a sector in alpha-major internal
+// order.  Support == exactly-nonzero amplitudes, which mirrors the reference
+// SparseVector invariant (sparse.py:33-47 drops `values == 0.0`).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "hsv_common.cuh"
+
+namespace hsv {
+
+__device__ __forceinline__ bool is_nz(double2 v) { return v.x != 0.0 || v.y != 0.0; }
+
+__global__ void k_fill_zero(double2* __restrict__ a, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) a[i] = make_double2(0.0, 0.0);
+}
+
+int grid_for(int64_t n, int block) {
+  int64_t g = (n + block - 1) / block;
+  int64_t cap = (int64_t)ctx().num_sms * 16;
+  return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+int state_fill_zero_async(hsv_state st) {
+  HSV_TRY_CUDA(cudaMemsetAsync(st->d_amp, 0, st->sec->dim * sizeof(double2), stream()));
+  HSV_TRY_CUDA(cudaMemsetAsync(st->d_norm2, 0, sizeof(double), stream()));
+  st->norm2_valid = true;
+  return HSV_OK;
+}
+
+// Per-block partial sums, fixed order; final pass in reduce_sum_f64.
+template <int NV>
+__device__ __forceinline__ void block_store(double (&v)[NV], double* __restrict__ out) {
+  __shared__ double sh[NV][32];
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    double s = warp_sum(v[j]);
+    if (l == 0) sh[j][w] = s;
+  }
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      double s = (l < (int)(blockDim.x >> 5)) ? sh[j][l] : 0.0;
+      s = warp_sum(s);
+      if (l == 0) out[blockIdx.x * (int64_t)NV + j] = s;
+    }
+  }
+}
+
+__global__ void k_norm2(const double2* __restrict__ a, int64_t n, double* __restrict__ part) {
+  double v[1] = {0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double2 x = a[i];
+    v[0] += x.x * x.x + x.y * x.y;
+  }
+  block_store<1>(v, part);
+}
+
+__global__ void k_dot(const double2* __restrict__ a, const double2* __restrict__ b, int64_t n,
+                      double* __restrict__ part) {
+  double v[2] = {0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double2 x = a[i], y = b[i];
+    v[0] += x.x * y.x + x.y * y.y;   // Re conj(x) y
+    v[1] += x.x * y.y - x.y * y.x;   // Im conj(x) y
+  }
+  block_store<2>(v, part);
+}
+
+__global__ void k_count_nz(const double2* __restrict__ a, int64_t n,
+                           unsigned long long* __restrict__ cnt) {
+  int64_t c = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    c += is_nz(a[i]) ? 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, (unsigned long long)c);
+}
+
+int state_norm2_async(hsv_state st) {
+  const int64_t n = st->sec->dim;
+  const int grid = grid_for(n, 256);
+  double* part = nullptr;
+  HSV_TRY(dalloc(&part, grid));
+  k_norm2<<<grid, 256, 0, stream()>>>(st->d_amp, n, part);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  HSV_TRY(reduce_sum_f64(part, grid, 1, 1, st->d_norm2));
+  dfree(part);
+  st->norm2_valid = true;
+  return HSV_OK;
+}
+
+// scatter (ref positions -> internal rows)
+__global__ void k_scatter_pos(const int64_t* __restrict__ pos, const double2* __restrict__ v,
+                              int64_t n, const int64_t* __restrict__ iperm,
+                              double2* __restrict__ a) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) a[iperm[pos[i]]] = v[i];
+}
+__global__ void k_scatter_idx(const int64_t* __restrict__ idx, const double2* __restrict__ v,
+                              int64_t n, double2* __restrict__ a) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) a[idx[i]] = v[i];
+}
+
+// gather into reference order + support flags
+__global__ void k_gather_ref(const double2* __restrict__ a, const int64_t* __restrict__ iperm,
+                             int64_t n, double prune, double2* __restrict__ out,
+                             int32_t* __restrict__ flag) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  double2 v = a[iperm[p]];
+  bool keep = prune > 0.0 ? (sqrt(v.x * v.x + v.y * v.y) >= prune) : is_nz(v);
+  out[p] = v;
+  flag[p] = keep ? 1 : 0;
+}
+__global__ void k_compact(const double2* __restrict__ v, const int32_t* __restrict__ flag,
+                          const int64_t* __restrict__ off, int64_t n, int64_t* __restrict__ pos,
+                          double* __restrict__ re, double* __restrict__ im) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (p >= n || !flag[p]) return;
+  int64_t o = off[p];
+  pos[o] = p;
+  re[o] = v[p].x;
+  im[o] = v[p].y;
+}
+
+__global__ void k_axpy(double ar, double ai, const double2* __restrict__ x,
+                       double2* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double2 a = x[i], b = y[i];
+    double2 r;
+    if (ai == 0.0) {   // real scale: a*x + y with separate roundings (sparse.py:226-228)
+      r.x = __dadd_rn(__dmul_rn(ar, a.x), b.x);
+      r.y = __dadd_rn(__dmul_rn(ar, a.y), b.y);
+    } else {
+      r.x = __dadd_rn(__dsub_rn(__dmul_rn(ar, a.x), __dmul_rn(ai, a.y)), b.x);
+      r.y = __dadd_rn(__dadd_rn(__dmul_rn(ar, a.y), __dmul_rn(ai, a.x)), b.y);
+    }
+    y[i] = r;
+  }
+}
+__global__ void k_scale(double ar, double ai, double2* __restrict__ y, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double2 a = y[i];
+    if (ai == 0.0) y[i] = make_double2(__dmul_rn(ar, a.x), __dmul_rn(ar, a.y));
+    else y[i] = make_double2(__dsub_rn(__dmul_rn(ar, a.x), __dmul_rn(ai, a.y)),
+                             __dadd_rn(__dmul_rn(ar, a.y), __dmul_rn(ai, a.x)));
+  }
+}
+__global__ void k_gather_i64(const int64_t* __restrict__ tab, const int64_t* __restrict__ idx,
+                             int64_t n, int64_t* __restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = idx[i] < 0 ? -1 : tab[idx[i]];
+}
+
+int upload_amps(const double* re, const double* im, int64_t n, double2** d_out) {
+  std::vector<double2> h(n);
+  for (int64_t i = 0; i < n; ++i) h[i] = make_double2(re[i], im ? im[i] : 0.0);
+  HSV_TRY(dalloc(d_out, n));
+  HSV_TRY_CUDA(cudaMemcpyAsync(*d_out, h.data(), n * sizeof(double2), cudaMemcpyHostToDevice,
+                               stream()));
+  // the host staging buffer must outlive the async copy
+  return stream_sync();
+}
+
+}  // namespace hsv
+
+using namespace hsv;
+
+extern "C" {
+
+int hsv_state_create(hsv_sector s, hsv_state* out) {
+  HSV_TRY(ensure_init());
+  HSV_REQUIRE(s && out, HSV_ERR_INVALID, "null argument");
+  auto* st = new hsv_state_s();
+  st->sec = s;
+  int rc = dalloc(&st->d_amp, s->dim);
+  if (!rc) rc = dalloc(&st->d_norm2, 1);
+  if (!rc) rc = state_fill_zero_async(st);
+  if (!rc) rc = stream_sync();
+  if (rc) { hsv_state_destroy(st); return rc; }
+  *out = st;
+  return HSV_OK;
+}
+
+int hsv_state_destroy(hsv_state st) {
+  if (!st) return HSV_OK;
+  dfree(st->d_amp);
+  dfree(st->d_norm2);
+  delete st;
+  return HSV_OK;
+}
+
+int hsv_state_copy(hsv_state dst, hsv_state src) {
+  HSV_REQUIRE(dst && src && dst->sec == src->sec, HSV_ERR_INVALID,
+              "dimension mismatch: states belong to different sectors");
+  if (dst == src) return HSV_OK;
+  HSV_TRY_CUDA(cudaMemcpyAsync(dst->d_amp, src->d_amp, src->sec->dim * sizeof(double2),
+                               cudaMemcpyDeviceToDevice, stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(dst->d_norm2, src->d_norm2, sizeof(double),
+                               cudaMemcpyDeviceToDevice, stream()));
+  dst->norm2_valid = src->norm2_valid;
+  return stream_sync();
+}
+
+int hsv_state_zero(hsv_state st) {
+  HSV_REQUIRE(st, HSV_ERR_INVALID, "null state");
+  HSV_TRY(state_fill_zero_async(st));
+  return stream_sync();
+}
+
+int hsv_state_set_basis(hsv_state st, uint64_t key, double re, double im) {
+  HSV_REQUIRE(st, HSV_ERR_INVALID, "null state");
+  hsv_sector s = st->sec;
+  uint32_t sa = s->compress_a(key), sb = s->compress_b(key);
+  bool ok = (s->n_qubits >= 64 || (key >> s->n_qubits) == 0) && s->Ra[sa] != ~0u &&
+            s->Rb[sb] != ~0u;
+  HSV_REQUIRE(ok, HSV_ERR_SECTOR, "configuration %#llx is outside the basis sector",
+              (unsigned long long)key);
+  int64_t idx = (int64_t)s->Ra[sa] * s->Nb + s->Rb[sb];
+  HSV_TRY(state_fill_zero_async(st));
+  static thread_local double2 v;
+  static thread_local double n2;
+  v = make_double2(re, im);
+  n2 = re * re + im * im;
+  HSV_TRY_CUDA(cudaMemcpyAsync(st->d_amp + idx, &v, sizeof(double2), cudaMemcpyHostToDevice,
+                               stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(st->d_norm2, &n2, sizeof(double), cudaMemcpyHostToDevice,
+                               stream()));
+  return stream_sync();
+}
+
+int hsv_state_set_sparse(hsv_state st, const int64_t* pos, const double* re, const double* im,
+                         int64_t n) {
+  HSV_REQUIRE(st && (n == 0 || (pos && re)), HSV_ERR_INVALID, "null argument");
+  for (int64_t i = 0; i < n; ++i)
+    HSV_REQUIRE(pos[i] >= 0 && pos[i] < st->sec->dim, HSV_ERR_INVALID,
+                "position %lld out of range for dimension %lld", (long long)pos[i],
+                (long long)st->sec->dim);
+  HSV_TRY(state_fill_zero_async(st));
+  if (n > 0) {
+    double2* d_v = nullptr;
+    int64_t* d_p = nullptr;
+    HSV_TRY(upload_amps(re, im, n, &d_v));
+    HSV_TRY(dalloc(&d_p, n));
+    HSV_TRY_CUDA(cudaMemcpyAsync(d_p, pos, n * 8, cudaMemcpyHostToDevice, stream()));
+    k_scatter_pos<<<(unsigned)((n + 255) / 256), 256, 0, stream()>>>(d_p, d_v, n,
+                                                                     st->sec->d_iperm, st->d_amp);
+    count_launch();
+    HSV_CHECK_LAUNCH();
+    dfree(d_v);
+    dfree(d_p);
+  }
+  HSV_TRY(state_norm2_async(st));
+  return stream_sync();
+}
+
+int hsv_state_set_keys(hsv_state st, const uint64_t* keys, const double* re, const double* im,
+                       int64_t n) {
+  HSV_REQUIRE(st && (n == 0 || (keys && re)), HSV_ERR_INVALID, "null argument");
+  hsv_sector s = st->sec;
+  std::vector<int64_t> idx(n);
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t k = keys[i];
+    uint32_t sa = s->compress_a(k), sb = s->compress_b(k);
+    bool ok = (s->n_qubits >= 64 || (k >> s->n_qubits) == 0) && s->Ra[sa] != ~0u &&
+              s->Rb[sb] != ~0u;
+    HSV_REQUIRE(ok, HSV_ERR_SECTOR, "configuration %#llx is outside the ci sector",
+                (unsigned long long)k);
+    idx[i] = (int64_t)s->Ra[sa] * s->Nb + s->Rb[sb];
+  }
+  HSV_TRY(state_fill_zero_async(st));
+  if (n > 0) {
+    double2* d_v = nullptr;
+    int64_t* d_i = nullptr;
+    HSV_TRY(upload_amps(re, im, n, &d_v));
+    HSV_TRY(dalloc(&d_i, n));
+    HSV_TRY_CUDA(cudaMemcpyAsync(d_i, idx.data(), n * 8, cudaMemcpyHostToDevice, stream()));
+    k_scatter_idx<<<(unsigned)((n + 255) / 256), 256, 0, stream()>>>(d_i, d_v, n, st->d_amp);
+    count_launch();
+    HSV_CHECK_LAUNCH();
+    HSV_TRY(stream_sync());
+    dfree(d_v);
+    dfree(d_i);
+  }
+  HSV_TRY(state_norm2_async(st));
+  return stream_sync();
+}
+
+int hsv_state_nnz(hsv_state st, int64_t* nnz) {
+  HSV_REQUIRE(st && nnz, HSV_ERR_INVALID, "null argument");
+  unsigned long long* d_c = nullptr;
+  HSV_TRY(dalloc(&d_c, 1));
+  HSV_TRY_CUDA(cudaMemsetAsync(d_c, 0, 8, stream()));
+  int grid = grid_for(st->sec->dim, 256);
+  k_count_nz<<<grid, 256, 0, stream()>>>(st->d_amp, st->sec->dim, d_c);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  unsigned long long h = 0;
+  HSV_TRY_CUDA(cudaMemcpyAsync(&h, d_c, 8, cudaMemcpyDeviceToHost, stream()));
+  HSV_TRY(stream_sync());
+  dfree(d_c);
+  *nnz = (int64_t)h;
+  return HSV_OK;
+}
+
+int hsv_state_get_sparse(hsv_state st, double prune, int64_t* pos, double* re, double* im,
+                         int64_t cap, int64_t* n_out) {
+  HSV_REQUIRE(st && n_out, HSV_ERR_INVALID, "null argument");
+  const int64_t n = st->sec->dim;
+  double2* d_ref = nullptr;
+  int32_t* d_flag = nullptr;
+  int64_t* d_off = nullptr;
+  HSV_TRY(dalloc(&d_ref, n));
+  HSV_TRY(dalloc(&d_flag, n));
+  HSV_TRY(dalloc(&d_off, n));
+  const unsigned g = (unsigned)((n + 255) / 256);
+  k_gather_ref<<<g, 256, 0, stream()>>>(st->d_amp, st->sec->d_iperm, n, prune, d_ref, d_flag);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  size_t tmp_bytes = 0;
+  HSV_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_flag, d_off, n, stream()));
+  void* d_tmp = nullptr;
+  HSV_TRY(dalloc(reinterpret_cast<char**>(&d_tmp), tmp_bytes));
+  HSV_TRY_CUDA(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_flag, d_off, n, stream()));
+  count_launch();
+  int64_t last_off = 0;
+  int32_t last_flag = 0;
+  if (n > 0) {
+    HSV_TRY_CUDA(cudaMemcpyAsync(&last_off, d_off + n - 1, 8, cudaMemcpyDeviceToHost, stream()));
+    HSV_TRY_CUDA(cudaMemcpyAsync(&last_flag, d_flag + n - 1, 4, cudaMemcpyDeviceToHost, stream()));
+  }
+  HSV_TRY(stream_sync());
+  const int64_t cnt = last_off + last_flag;
+  *n_out = cnt;
+  if (pos && cnt > 0) {
+    HSV_REQUIRE(cap >= cnt, HSV_ERR_INVALID, "output capacity %lld < support size %lld",
+                (long long)cap, (long long)cnt);
+    int64_t* d_pos = nullptr;
+    double *d_re = nullptr, *d_im = nullptr;
+    HSV_TRY(dalloc(&d_pos, cnt));
+    HSV_TRY(dalloc(&d_re, cnt));
+    HSV_TRY(dalloc(&d_im, cnt));
+    k_compact<<<g, 256, 0, stream()>>>(d_ref, d_flag, d_off, n, d_pos, d_re, d_im);
+    count_launch();
+    HSV_CHECK_LAUNCH();
+    HSV_TRY_CUDA(cudaMemcpyAsync(pos, d_pos, cnt * 8, cudaMemcpyDeviceToHost, stream()));
+    if (re) HSV_TRY_CUDA(cudaMemcpyAsync(re, d_re, cnt * 8, cudaMemcpyDeviceToHost, stream()));
+    if (im) HSV_TRY_CUDA(cudaMemcpyAsync(im, d_im, cnt * 8, cudaMemcpyDeviceToHost, stream()));
+    HSV_TRY(stream_sync());
+    dfree(d_pos); dfree(d_re); dfree(d_im);
+  }
+  dfree(d_ref); dfree(d_flag); dfree(d_off); dfree(reinterpret_cast<char*>(d_tmp));
+  return HSV_OK;
+}
+
+int hsv_state_dot(hsv_state a, hsv_state b, double* re, double* im) {
+  HSV_REQUIRE(a && b, HSV_ERR_INVALID, "null state");
+  HSV_REQUIRE(a->sec == b->sec, HSV_ERR_INVALID, "dimension mismatch in dot");
+  const int64_t n = a->sec->dim;
+  const int grid = grid_for(n, 256);
+  double *part = nullptr, *d_r = nullptr;
+  HSV_TRY(dalloc(&part, 2 * (int64_t)grid));
+  HSV_TRY(dalloc(&d_r, 2));
+  k_dot<<<grid, 256, 0, stream()>>>(a->d_amp, b->d_amp, n, part);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  HSV_TRY(reduce_sum_f64(part, grid, 2, 2, d_r));
+  double h[2];
+  HSV_TRY_CUDA(cudaMemcpyAsync(h, d_r, 16, cudaMemcpyDeviceToHost, stream()));
+  HSV_TRY(stream_sync());
+  dfree(part);
+  dfree(d_r);
+  if (re) *re = h[0];
+  if (im) *im = h[1];
+  return HSV_OK;
+}
+
+int hsv_state_norm(hsv_state st, double* norm) {
+  HSV_REQUIRE(st && norm, HSV_ERR_INVALID, "null argument");
+  HSV_TRY(state_norm2_async(st));
+  double h = 0;
+  HSV_TRY_CUDA(cudaMemcpyAsync(&h, st->d_norm2, 8, cudaMemcpyDeviceToHost, stream()));
+  HSV_TRY(stream_sync());
+  *norm = std::sqrt(h);
+  return HSV_OK;
+}
+
+int hsv_state_axpy(double ar, double ai, hsv_state x, hsv_state y) {
+  HSV_REQUIRE(x && y && x->sec == y->sec, HSV_ERR_INVALID, "dimension mismatch in axpy");
+  const int64_t n = x->sec->dim;
+  k_axpy<<<grid_for(n, 256), 256, 0, stream()>>>(ar, ai, x->d_amp, y->d_amp, n);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  y->norm2_valid = false;
+  return stream_sync();
+}
+
+int hsv_state_scale(hsv_state st, double ar, double ai) {
+  HSV_REQUIRE(st, HSV_ERR_INVALID, "null state");
+  const int64_t n = st->sec->dim;
+  k_scale<<<grid_for(n, 256), 256, 0, stream()>>>(ar, ai, st->d_amp, n);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  st->norm2_valid = false;
+  return stream_sync();
+}
+
+int hsv_state_device_ptr(hsv_state st, void** ptr, int64_t* n) {
+  HSV_REQUIRE(st, HSV_ERR_INVALID, "null state");
+  if (ptr) *ptr = st->d_amp;
+  if (n) *n = st->sec->dim;
+  st->norm2_valid = false;   // caller may write through the pointer
+  return HSV_OK;
+}
+
+int hsv_sector_positions(hsv_sector s, const uint64_t* keys, int64_t n, int64_t* pos) {
+  HSV_REQUIRE(s && (n == 0 || (keys && pos)), HSV_ERR_INVALID, "null argument");
+  if (n == 0) return HSV_OK;
+  std::vector<int64_t> internal(n);
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t k = keys[i];
+    bool ok = s->n_qubits >= 64 || (k >> s->n_qubits) == 0;
+    uint32_t sa = s->compress_a(k), sb = s->compress_b(k);
+    ok = ok && s->Ra[sa] != ~0u && s->Rb[sb] != ~0u;
+    internal[i] = ok ? (int64_t)s->Ra[sa] * s->Nb + s->Rb[sb] : -1;
+  }
+  int64_t *d_i = nullptr, *d_o = nullptr;
+  HSV_TRY(dalloc(&d_i, n));
+  HSV_TRY(dalloc(&d_o, n));
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_i, internal.data(), n * 8, cudaMemcpyHostToDevice, stream()));
+  k_gather_i64<<<(unsigned)((n + 255) / 256), 256, 0, stream()>>>(s->d_perm, d_i, n, d_o);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  HSV_TRY_CUDA(cudaMemcpyAsync(pos, d_o, n * 8, cudaMemcpyDeviceToHost, stream()));
+  HSV_TRY(stream_sync());
+  dfree(d_i);
+  dfree(d_o);
+  return HSV_OK;
+}
+
+int hsv_sector_keys(hsv_sector s, const int64_t* pos, int64_t n, uint64_t* keys) {
+  HSV_REQUIRE(s && (n == 0 || (keys && pos)), HSV_ERR_INVALID, "null argument");
+  if (n == 0) return HSV_OK;
+  for (int64_t i = 0; i < n; ++i)
+    HSV_REQUIRE(pos[i] >= 0 && pos[i] < s->dim, HSV_ERR_INVALID, "position %lld out of range",
+                (long long)pos[i]);
+  std::vector<int64_t> internal(n);
+  int64_t *d_i = nullptr, *d_o = nullptr;
+  HSV_TRY(dalloc(&d_i, n));
+  HSV_TRY(dalloc(&d_o, n));
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_i, pos, n * 8, cudaMemcpyHostToDevice, stream()));
+  k_gather_i64<<<(unsigned)((n + 255) / 256), 256, 0, stream()>>>(s->d_iperm, d_i, n, d_o);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  HSV_TRY_CUDA(cudaMemcpyAsync(internal.data(), d_o, n * 8, cudaMemcpyDeviceToHost, stream()));
+  HSV_TRY(stream_sync());
+  dfree(d_i);
+  dfree(d_o);
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t ra = internal[i] / s->Nb, rb = internal[i] % s->Nb;
+    keys[i] = s->expand(s->Sa[ra], s->Sb[rb]);
+  }
+  return HSV_OK;
+}
+
+}  // extern "C"
