@@ -1,0 +1,329 @@
+#!/usr/bin/env python3
+"""Benchmark: H12 ADAPT-VQE energy + gradient iteration on B200.
+
+One step = <psi|H|psi> plus all 1,818 QEB pool gradients of H12 (24 qubits,
+853,776 determinants) on the dense-in-sector S1 state -- the reference's
+SvAdaptEngine.energy + .screen (adapt.py:205-214), i.e. the north-star
+"energy+gradient iteration".  Metric: Pauli-term x
+amplitude updates/s = T * nnz(psi) / step time (T = 14,905 Pauli terms).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl hsv|reference]
+
+N > 1 (torchrun, one rank per GPU): owner-computes over alpha-string row
+ranges with psi replicated; per-rank partial energy + gradients are
+all-gathered (NCCL) and summed in rank order -- strong scaling of one H12
+problem.  --impl reference times the reference CPU algorithm (oracle port,
+bounded row/operator sample, extrapolated) on the host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIG = "h12"
+S1_SEED = 20240811
+METRIC = "Pauli-term x amplitude updates/s (H12 energy+gradient iteration)"
+UNIT = "updates/s"
+
+
+def s1_values(dim):
+    v = np.random.default_rng(S1_SEED).standard_normal(dim)
+    return v / float(np.linalg.norm(v))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text()), "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def cpu_reference(sysm, psi, steps=1, warmup=0):
+    """Reference CPU algorithm (oracle port) on a bounded sample; seconds/step."""
+    from oracle import cpu_baseline
+    h = sysm.hamiltonian
+    res = None
+    for _ in range(warmup + steps):
+        res = cpu_baseline.measure_step(h.xs, h.zs, h.coeffs, sysm.n_qubits, sysm.n_alpha,
+                                        sysm.n_beta, sysm.integrals.nelec, psi)
+    return res
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import paper_2604_01176_b200 as hsv
+    sysm = hsv.MolecularSystem.bundled(CONFIG)
+    dim = len(sysm.basis)
+    psi = s1_values(dim)
+    T = len(sysm.hamiltonian)
+    cpu_reference(sysm, psi, steps=1, warmup=0) if args.warmup > 0 else None
+    times, res = [], None
+    for _ in range(args.steps):
+        res = cpu_reference(sysm, psi)
+        times.append(res["t_step_s"])
+    t = statistics.mean(times)
+    val = T * dim / t
+    sample = (f"H rows [0,{res['rows']}) of {dim} ({res['sample_nnz']} CSR nnz) + "
+              f"{res['ops_sampled']} of {res['ops']} pool ops, extrapolated linearly")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic S1 state (default_rng(20240811)), bundled H12 Pauli sum",
+        "config": {"workload": "H12 STO-3G energy + 1818 QEB pool gradients, S1 dense state",
+                   "dim": dim, "n_terms": T},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": res["threads"], "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def run_hsv(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_01176_b200 as hsv
+    from paper_2604_01176_b200 import _native as N
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    N.init(local)
+    stream = torch.cuda.current_stream()
+    N.call("hsv_set_stream", N.C.c_void_p(stream.cuda_stream))
+
+    sysm = hsv.MolecularSystem.bundled(CONFIG)
+    basis = sysm.basis
+    dim = len(basis)
+    T = len(sysm.hamiltonian)
+    op = hsv.assemble_subspace_hamiltonian(sysm.hamiltonian, basis)
+    pool_ops = hsv.build_qeb_pool(sysm.n_qubits, sysm.integrals.nelec).ops
+    dpool = hsv.svengine.DevicePool(basis, pool_ops)
+    M = dpool.n
+    nnz_struct = op.nnz                       # structural nonzeros (== reference CSR nnz)
+    psi_vals = s1_values(dim)
+    pos_pinned = torch.arange(dim, dtype=torch.int64).pin_memory()
+    val_pinned = torch.from_numpy(psi_vals).pin_memory()
+    st = hsv.svengine.DeviceState(basis)
+
+    def upload():
+        N.call("hsv_state_set_sparse", st.handle,
+               N.C.cast(pos_pinned.data_ptr(), N.P_i64), N.C.cast(val_pinned.data_ptr(), N.P_dbl),
+               None, dim)
+
+    upload()
+    n_alpha_strings = basis._sector.n_alpha_strings
+    a_lo = n_alpha_strings * rank // world
+    a_hi = n_alpha_strings * (rank + 1) // world
+    d_out = torch.zeros(2 + M, dtype=torch.float64, device="cuda")
+    gathered = torch.zeros(world, 2 + M, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def step_device():
+        N.call("hsv_energy_screen_pool_async", op.handle, st.handle, dpool.handle, a_lo, a_hi,
+               N.C.c_void_p(d_out.data_ptr()))
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, d_out)
+            return gathered.sum(0)    # rank order, fixed
+        return d_out
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident throughput (value) ----
+    for _ in range(args.warmup):
+        step_device()
+    barrier()
+    N.lib().hsv_launch_count(1)
+    N.call("hsv_prof_reset")
+    N.call("hsv_prof_enable", 1)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()                     # L2 flush between timed steps (outside events)
+            ev[i][0].record()
+            out = step_device()
+            ev[i][1].record()
+        barrier()
+    N.call("hsv_prof_collect")
+    N.call("hsv_prof_enable", 0)
+    launches = int(N.lib().hsv_launch_count(1))
+    ms = [a.elapsed_time(b) for a, b in ev]
+    t_ms = float(sum(ms))
+    prof = {}
+    for k in ("apply", "screen"):
+        tot, cnt = N.dbl(), N.i64()
+        N.call("hsv_prof_get", k.encode(), N.C.byref(tot), N.C.byref(cnt))
+        prof[k] = (tot.value, cnt.value)
+    if world > 1:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    energy = float(out[0].item())
+    ms_per_step = t_ms / args.steps
+    value = T * dim / (ms_per_step * 1e-3)
+
+    # ---- end to end through the C ABI with host buffers ----
+    g_host = np.empty(M)
+    e_host = N.dbl()
+    e2e_ms = []
+    for i in range(args.warmup + args.steps):
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        upload()                               # H2D: positions + amplitudes (pinned)
+        if world > 1:
+            step_device()
+            res = gathered.sum(0).cpu().numpy()  # D2H
+            e_host.value, g_host[:] = res[0], res[2:]
+        else:
+            N.call("hsv_energy_screen_pool", op.handle, st.handle, dpool.handle,
+                   N.C.byref(e_host), N.ptr_f64(g_host))
+        b.record()
+        barrier()
+        if i >= args.warmup:
+            e2e_ms.append(a.elapsed_time(b))
+    e2e_t = sum(e2e_ms) / len(e2e_ms)
+    if world > 1:
+        tt = torch.tensor([e2e_t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_t = float(tt.item())
+    e2e_value = T * dim / (e2e_t * 1e-3)
+
+    if rank == 0:
+        pk, pk_kind = peaks()
+        hbm = float(pk.get("hbm_gbs", 6650.0))
+        rows_local = (a_hi - a_lo) * (dim // n_alpha_strings)
+        apply_ms = prof["apply"][0] / max(prof["apply"][1], 1)
+        # algorithmic bytes of one H application over the rank's rows:
+        # 16 B per nonzero matrix element (one complex128 gather) + 24 B per row
+        # (stream psi_b and write w_b ... key + amplitude) -- SURVEY.md 8(d)
+        bytes_apply = (16.0 * nnz_struct + 24.0 * dim) * rows_local / dim
+        achieved = bytes_apply / (apply_ms * 1e-3) / 1e9
+        screen_ms = prof["screen"][0] / max(prof["screen"][1], 1)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "c128 (f64)", "data": "synthetic S1 state (default_rng(20240811)), "
+                                          "bundled H12 Pauli sum from the reference builder",
+            "config": {"workload": "H12 STO-3G energy + 1818 QEB pool gradients, S1 dense state",
+                       "dim": dim, "n_terms": T, "pool": M, "csr_nnz": nnz_struct,
+                       "l2": "flushed between timed steps (256 MiB write, outside events)",
+                       "parallelism": f"owner-computes alpha rows x{world}"},
+            "energy": energy,
+            "roofline": {"bound": "hbm", "kernel": "k_apply (H|psi>, K1)",
+                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "peak_kind": pk_kind,
+                         "traffic": None, "apply_ms": apply_ms,
+                         "bytes_per_launch": bytes_apply},
+            "kernels_ms": {"apply": apply_ms, "screen": screen_ms},
+            "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_t,
+                    "h2d_bytes_per_step": dim * 16, "d2h_bytes_per_step": (2 + M) * 8},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if not args.no_cpu:
+            r = cpu_reference(sysm, psi_vals)
+            line["cpu_baseline"] = {
+                "value": T * dim / r["t_step_s"], "unit": UNIT, "cores": r["threads"],
+                "kind": "port",
+                "sample": (f"H rows [0,{r['rows']}) of {dim} ({r['sample_nnz']} CSR nnz) + "
+                           f"{r['ops_sampled']}/{r['ops']} pool ops, extrapolated"),
+                "ms_per_step": r["t_step_s"] * 1e3}
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="hsv", choices=["hsv", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "hsv":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_hsv(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -61,6 +61,7 @@ enum hsv_ordering { HSV_INTERLEAVED = 0, HSV_BLOCKED = 1 };
 typedef struct hsv_sector_s* hsv_sector;
 typedef struct hsv_op_s* hsv_op;
 typedef struct hsv_state_s* hsv_state;
+typedef struct hsv_pool_s* hsv_pool;
 
 /* ---- library / device ------------------------------------------------- */
 HSV_API int hsv_abi_version(void);
@@ -165,6 +166,26 @@ HSV_API int hsv_state_device_ptr(hsv_state st, void** ptr, int64_t* n);
 /* out rows [a_lo, a_hi) <- (H in) rows; other rows untouched. */
 HSV_API int hsv_apply_h_rows_async(hsv_op op, hsv_state in, hsv_state out, int64_t a_lo,
                            int64_t a_hi, double prune);
+
+/* ---- operator pools (build_qeb_pool, adapt.py:78-108, resident on the device) ---- */
+HSV_API int hsv_pool_create(hsv_sector s, const uint64_t* occ_masks, const uint64_t* virt_masks,
+                            int64_t n_ops, hsv_pool* out);
+HSV_API int hsv_pool_destroy(hsv_pool p);
+/* energy + all pool gradients of rows [a_lo, a_hi) into DEVICE d_out
+ * (layout as hsv_energy_screen_partial_async); no host synchronization. */
+HSV_API int hsv_energy_screen_pool_async(hsv_op op, hsv_state psi, hsv_pool pool, int64_t a_lo,
+                                         int64_t a_hi, double* d_out);
+/* synchronous full-range variant with host outputs */
+HSV_API int hsv_energy_screen_pool(hsv_op op, hsv_state psi, hsv_pool pool, double* energy,
+                                   double* grads);
+
+/* ---- live kernel timing (CUDA events on the launch stream) ---- */
+HSV_API int hsv_prof_enable(int on);
+/* synchronize, then fold recorded event pairs into per-kernel totals */
+HSV_API int hsv_prof_collect(void);
+/* kernels: "apply", "screen", "qeb", "adjoint", "generator" */
+HSV_API int hsv_prof_get(const char* kernel, double* total_ms, int64_t* count);
+HSV_API int hsv_prof_reset(void);
 
 /* ---- generic CSR x sparse vector (K1b; spmspv on arbitrary CsrMatrix) ---- */
 /* y = M x with M in CSR (int64 offsets/cols, f64 values), x dense-scattered

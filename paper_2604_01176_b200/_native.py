@@ -79,6 +79,14 @@ _SIGNATURES = {
     "hsv_vec_axpy": (C.c_int, [i64, dbl, P_i64, P_dbl, i64, P_i64, P_dbl, i64, dbl, P_i64,
                                P_dbl, P_i64]),
     "hsv_vec_scale": (C.c_int, [P_dbl, i64, dbl, C.c_int, P_dbl]),
+    "hsv_pool_create": (C.c_int, [vp, P_u64, P_u64, i64, C.POINTER(vp)]),
+    "hsv_pool_destroy": (C.c_int, [vp]),
+    "hsv_energy_screen_pool_async": (C.c_int, [vp, vp, vp, i64, i64, vp]),
+    "hsv_energy_screen_pool": (C.c_int, [vp, vp, vp, P_dbl, P_dbl]),
+    "hsv_prof_enable": (C.c_int, [C.c_int]),
+    "hsv_prof_collect": (C.c_int, []),
+    "hsv_prof_get": (C.c_int, [C.c_char_p, P_dbl, P_i64]),
+    "hsv_prof_reset": (C.c_int, []),
 }
 
 _lib = None

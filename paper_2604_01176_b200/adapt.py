@@ -22,8 +22,8 @@ import numpy as np
 import scipy.optimize
 
 from .cibasis import hartree_fock_configuration, qubit_spin
-from .svengine import (ExcitationOperator, SvState, apply_ansatz, apply_qeb_exponential,
-                       assemble_subspace_hamiltonian)
+from .svengine import (DevicePool, ExcitationOperator, SvState, apply_ansatz,
+                       apply_qeb_exponential, assemble_subspace_hamiltonian)
 
 ENGINES = ("sv", "mps", "partitioned")
 
@@ -155,6 +155,7 @@ class SvAdaptEngine:
         self.threads = config.threads
         self.run_log = TruncationLog()
         self._masks: dict = {}
+        self._dpools: dict = {}
 
     def _pool_masks(self, ops):
         key = tuple(ops)
@@ -181,13 +182,19 @@ class SvAdaptEngine:
         occ, virt = self._pool_masks(ops)
         return self.matrix.energy_gradient(self.system.hf.bits, occ, virt, thetas)
 
+    def _device_pool(self, pool):
+        ops = tuple(getattr(pool, "ops", pool))
+        dp = self._dpools.get(ops)
+        if dp is None:
+            dp = DevicePool(self.basis, ops)
+            self._dpools = {ops: dp} if len(self._dpools) > 4 else {**self._dpools, ops: dp}
+        return dp
+
     def screen(self, state, pool) -> np.ndarray:
-        occ, virt = self._pool_masks(getattr(pool, "ops", pool))
-        return self.matrix.energy_screen(state, occ, virt)[1]
+        return self.matrix.energy_screen_pool(state, self._device_pool(pool))[1]
 
     def energy_and_screen(self, state, pool):
-        occ, virt = self._pool_masks(getattr(pool, "ops", pool))
-        return self.matrix.energy_screen(state, occ, virt)
+        return self.matrix.energy_screen_pool(state, self._device_pool(pool))
 
     def state_size(self, state) -> int:
         return state.nnz

@@ -217,6 +217,7 @@ static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
   grid = std::max<int64_t>(1, std::min(grid, need));
   if (n_warps_out) *n_warps_out = grid * 8;
   if (a.units == 0) return HSV_OK;
+  ProfScope prof("apply");
   k_apply<W, SH, R><<<(unsigned)grid, 256, 0, stream()>>>(a);
   count_launch();
   HSV_CHECK_LAUNCH();

@@ -151,6 +151,13 @@ struct hsv_op_s {
   std::vector<Term> terms;
 };
 
+struct hsv_pool_s {
+  hsv_sector sec = nullptr;
+  int64_t n = 0;
+  int4* d = nullptr;          // {oa, va, ob, vb} compressed masks
+  std::vector<int4> h;
+};
+
 struct hsv_state_s {
   hsv_sector sec = nullptr;
   double2* d_amp = nullptr;    // dim complex128, alpha-major internal order
@@ -181,6 +188,17 @@ __device__ __forceinline__ double warp_max(double v) {
 }
 
 // Launch helpers
+// RAII CUDA-event pair around a launch when profiling is enabled.
+class ProfScope {
+ public:
+  explicit ProfScope(const char* name);
+  ~ProfScope();
+ private:
+  const char* name_;
+  cudaEvent_t a_ = nullptr;
+  bool active_ = false;
+};
+
 int reduce_sum_f64(const double* d_in, int64_t n, int64_t stride, int64_t count,
                    double* d_out);   // d_out[j] = sum_i d_in[i*stride + j], j<count
 int state_norm2_async(hsv_state st);

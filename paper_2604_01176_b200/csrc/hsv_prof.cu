@@ -1,0 +1,119 @@
+// Live per-kernel timing (CUDA events on the launching stream) and the
+// persistent device operator pool used by the screen kernel.
+#include <map>
+#include <string>
+#include <vector>
+
+#include "hsv_common.cuh"
+#include "hsv_kernels.cuh"
+
+namespace hsv {
+
+struct ProfPair {
+  const char* name;
+  cudaEvent_t a, b;
+};
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> free_ev;
+  std::vector<ProfPair> pending;
+  std::map<std::string, std::pair<double, int64_t>> acc;
+};
+static Prof g_prof;
+
+static cudaEvent_t take_event() {
+  if (g_prof.free_ev.empty()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+  cudaEvent_t e = g_prof.free_ev.back();
+  g_prof.free_ev.pop_back();
+  return e;
+}
+
+ProfScope::ProfScope(const char* name) : name_(name) {
+  if (!g_prof.on) return;
+  a_ = take_event();
+  cudaEventRecord(a_, stream());
+  active_ = true;
+}
+ProfScope::~ProfScope() {
+  if (!active_) return;
+  cudaEvent_t b = take_event();
+  cudaEventRecord(b, stream());
+  g_prof.pending.push_back(ProfPair{name_, a_, b});
+}
+
+}  // namespace hsv
+
+using namespace hsv;
+
+extern "C" {
+
+int hsv_prof_enable(int on) {
+  g_prof.on = on != 0;
+  return HSV_OK;
+}
+
+int hsv_prof_collect(void) {
+  HSV_TRY(stream_sync());
+  for (auto& p : g_prof.pending) {
+    float ms = 0.f;
+    HSV_TRY_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+    auto& slot = g_prof.acc[p.name];
+    slot.first += ms;
+    slot.second += 1;
+    g_prof.free_ev.push_back(p.a);
+    g_prof.free_ev.push_back(p.b);
+  }
+  g_prof.pending.clear();
+  return HSV_OK;
+}
+
+int hsv_prof_get(const char* name, double* total_ms, int64_t* count) {
+  auto it = g_prof.acc.find(name);
+  if (total_ms) *total_ms = it == g_prof.acc.end() ? 0.0 : it->second.first;
+  if (count) *count = it == g_prof.acc.end() ? 0 : it->second.second;
+  return HSV_OK;
+}
+
+int hsv_prof_reset(void) {
+  g_prof.acc.clear();
+  return HSV_OK;
+}
+
+// ---- operator pool (compressed QEB masks resident on the device) ----
+int hsv_pool_create(hsv_sector s, const uint64_t* occ, const uint64_t* virt, int64_t n,
+                    hsv_pool* out) {
+  HSV_TRY(ensure_init());
+  HSV_REQUIRE(s && out && (n == 0 || (occ && virt)), HSV_ERR_INVALID, "null argument");
+  auto* p = new hsv_pool_s();
+  p->sec = s;
+  p->n = n;
+  p->h.resize(n);
+  for (int64_t i = 0; i < n; ++i) {
+    if ((occ[i] & virt[i]) || !occ[i] || !virt[i]) {
+      delete p;
+      set_error(HSV_ERR_INVALID, "excitation indices must be distinct");
+      return HSV_ERR_INVALID;
+    }
+    OpMasks m = compress_op(s, occ[i], virt[i]);
+    p->h[i] = make_int4((int)m.oa, (int)m.va, (int)m.ob, (int)m.vb);
+  }
+  int rc = dalloc(&p->d, n);
+  if (rc) { delete p; return rc; }
+  if (n) HSV_TRY_CUDA(cudaMemcpyAsync(p->d, p->h.data(), n * sizeof(int4), cudaMemcpyHostToDevice, stream()));
+  HSV_TRY(stream_sync());
+  *out = p;
+  return HSV_OK;
+}
+
+int hsv_pool_destroy(hsv_pool p) {
+  if (!p) return HSV_OK;
+  dfree(p->d);
+  delete p;
+  return HSV_OK;
+}
+
+}  // extern "C"

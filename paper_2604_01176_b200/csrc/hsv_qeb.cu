@@ -229,6 +229,7 @@ static int launch_pairs(const PairLists& pl, PairArgs a, int64_t* nblocks_out = 
   HSV_REQUIRE(pl.ca <= 65535, HSV_ERR_UNSUPPORTED, "alpha pair list too long (%lld)",
               (long long)pl.ca);
   if (nblocks_out) *nblocks_out = (int64_t)grid.x * grid.y;
+  ProfScope prof(MODE == kRotate ? "qeb" : MODE == kAdjoint ? "adjoint" : "generator");
   k_pairs<MODE><<<grid, 256, 0, stream()>>>(a);
   count_launch();
   HSV_CHECK_LAUNCH();

@@ -113,7 +113,10 @@ int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w, cons
   a.ops = d_ops; a.n_ops = n_ops; a.psi = psi; a.w = w; a.Nb = s->Nb;
   a.row_lo = row_lo; a.row_hi = row_hi; a.part = part;
   if (nrows > 0) {
-    k_screen<<<(unsigned)grid, kScreenBlock, smem, stream()>>>(a);
+    {
+      ProfScope prof("screen");
+      k_screen<<<(unsigned)grid, kScreenBlock, smem, stream()>>>(a);
+    }
     count_launch();
     HSV_CHECK_LAUNCH();
     HSV_TRY(reduce_sum_f64(part, grid, n_ops, n_ops, d_grads));
@@ -144,15 +147,9 @@ using namespace hsv;
 
 extern "C" {
 
-int hsv_energy_screen_partial_async(hsv_op op, hsv_state psi, const uint64_t* occ,
-                                    const uint64_t* virt, int64_t n_ops, int64_t a_lo,
-                                    int64_t a_hi, double* d_out) {
-  HSV_REQUIRE(op && psi && d_out && (n_ops == 0 || (occ && virt)), HSV_ERR_INVALID, "null argument");
-  HSV_REQUIRE(psi->sec == op->sec, HSV_ERR_INVALID, "dimension mismatch");
+static int energy_screen_dev(hsv_op op, hsv_state psi, const int4* d_ops, int64_t n_ops,
+                             int64_t a_lo, int64_t a_hi, double* d_out) {
   const hsv_sector_s* s = op->sec;
-  HSV_REQUIRE(0 <= a_lo && a_lo <= a_hi && a_hi <= s->Na, HSV_ERR_INVALID, "bad alpha-row range");
-  int4* d_ops = nullptr;
-  HSV_TRY(upload_ops(s, occ, virt, n_ops, &d_ops));
   double2* w = nullptr;
   HSV_TRY(dalloc(&w, s->dim));
   const int nw = apply_warps(op);
@@ -165,7 +162,49 @@ int hsv_energy_screen_partial_async(hsv_op op, hsv_state psi, const uint64_t* oc
   HSV_TRY(launch_screen(op, psi->d_amp, w, d_ops, (int)n_ops, a_lo * s->Nb, a_hi * s->Nb, d_out + 2));
   dfree(w);
   dfree(epart);
+  return HSV_OK;
+}
+
+static int check_es_args(hsv_op op, hsv_state psi, int64_t a_lo, int64_t a_hi) {
+  HSV_REQUIRE(op && psi, HSV_ERR_INVALID, "null argument");
+  HSV_REQUIRE(psi->sec == op->sec, HSV_ERR_INVALID, "dimension mismatch");
+  HSV_REQUIRE(0 <= a_lo && a_lo <= a_hi && a_hi <= op->sec->Na, HSV_ERR_INVALID,
+              "bad alpha-row range");
+  return HSV_OK;
+}
+
+int hsv_energy_screen_partial_async(hsv_op op, hsv_state psi, const uint64_t* occ,
+                                    const uint64_t* virt, int64_t n_ops, int64_t a_lo,
+                                    int64_t a_hi, double* d_out) {
+  HSV_TRY(check_es_args(op, psi, a_lo, a_hi));
+  HSV_REQUIRE(d_out && (n_ops == 0 || (occ && virt)), HSV_ERR_INVALID, "null argument");
+  int4* d_ops = nullptr;
+  HSV_TRY(upload_ops(op->sec, occ, virt, n_ops, &d_ops));
+  HSV_TRY(energy_screen_dev(op, psi, d_ops, n_ops, a_lo, a_hi, d_out));
   dfree(d_ops);
+  return HSV_OK;
+}
+
+int hsv_energy_screen_pool_async(hsv_op op, hsv_state psi, hsv_pool pool, int64_t a_lo,
+                                 int64_t a_hi, double* d_out) {
+  HSV_TRY(check_es_args(op, psi, a_lo, a_hi));
+  HSV_REQUIRE(pool && d_out && pool->sec == op->sec, HSV_ERR_INVALID, "bad pool argument");
+  return energy_screen_dev(op, psi, pool->d, pool->n, a_lo, a_hi, d_out);
+}
+
+int hsv_energy_screen_pool(hsv_op op, hsv_state psi, hsv_pool pool, double* energy, double* grads) {
+  HSV_REQUIRE(op && pool && (pool->n == 0 || grads), HSV_ERR_INVALID, "null argument");
+  const int64_t n_ops = pool->n;
+  double* d_out = nullptr;
+  HSV_TRY(dalloc(&d_out, 2 + n_ops));
+  HSV_TRY(hsv_energy_screen_pool_async(op, psi, pool, 0, op->sec->Na, d_out));
+  static thread_local std::vector<double> h;
+  h.resize(2 + n_ops);
+  HSV_TRY_CUDA(cudaMemcpyAsync(h.data(), d_out, (2 + n_ops) * sizeof(double), cudaMemcpyDeviceToHost, stream()));
+  HSV_TRY(stream_sync());
+  dfree(d_out);
+  if (energy) *energy = h[0];
+  for (int64_t i = 0; i < n_ops; ++i) grads[i] = h[2 + i];
   return HSV_OK;
 }
 

@@ -100,11 +100,15 @@ int state_norm2_async(hsv_state st) {
 }
 
 // scatter (ref positions -> internal rows)
-__global__ void k_scatter_pos(const int64_t* __restrict__ pos, const double2* __restrict__ v,
-                              int64_t n, const int64_t* __restrict__ iperm,
-                              double2* __restrict__ a) {
+__global__ void k_scatter_pos(const int64_t* __restrict__ pos, const double* __restrict__ re,
+                              const double* __restrict__ im, int64_t n, int64_t dim,
+                              const int64_t* __restrict__ iperm, double2* __restrict__ a,
+                              int* __restrict__ bad) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) a[iperm[pos[i]]] = v[i];
+  if (i >= n) return;
+  const int64_t p = pos[i];
+  if (p < 0 || p >= dim) { *bad = 1; return; }
+  a[iperm[p]] = make_double2(re[i], im ? im[i] : 0.0);
 }
 __global__ void k_scatter_idx(const int64_t* __restrict__ idx, const double2* __restrict__ v,
                               int64_t n, double2* __restrict__ a) {
@@ -245,26 +249,37 @@ int hsv_state_set_basis(hsv_state st, uint64_t key, double re, double im) {
 int hsv_state_set_sparse(hsv_state st, const int64_t* pos, const double* re, const double* im,
                          int64_t n) {
   HSV_REQUIRE(st && (n == 0 || (pos && re)), HSV_ERR_INVALID, "null argument");
-  for (int64_t i = 0; i < n; ++i)
-    HSV_REQUIRE(pos[i] >= 0 && pos[i] < st->sec->dim, HSV_ERR_INVALID,
-                "position %lld out of range for dimension %lld", (long long)pos[i],
-                (long long)st->sec->dim);
+  // Host buffers go straight to the device (pinned buffers copy asynchronously);
+  // positions are range-checked by the scatter kernel.
   HSV_TRY(state_fill_zero_async(st));
+  int h_bad = 0;
   if (n > 0) {
-    double2* d_v = nullptr;
+    double *d_re = nullptr, *d_im = nullptr;
     int64_t* d_p = nullptr;
-    HSV_TRY(upload_amps(re, im, n, &d_v));
+    int* d_bad = nullptr;
     HSV_TRY(dalloc(&d_p, n));
+    HSV_TRY(dalloc(&d_re, n));
+    if (im) HSV_TRY(dalloc(&d_im, n));
+    HSV_TRY(dalloc(&d_bad, 1));
+    HSV_TRY_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), stream()));
     HSV_TRY_CUDA(cudaMemcpyAsync(d_p, pos, n * 8, cudaMemcpyHostToDevice, stream()));
-    k_scatter_pos<<<(unsigned)((n + 255) / 256), 256, 0, stream()>>>(d_p, d_v, n,
-                                                                     st->sec->d_iperm, st->d_amp);
+    HSV_TRY_CUDA(cudaMemcpyAsync(d_re, re, n * 8, cudaMemcpyHostToDevice, stream()));
+    if (im) HSV_TRY_CUDA(cudaMemcpyAsync(d_im, im, n * 8, cudaMemcpyHostToDevice, stream()));
+    k_scatter_pos<<<(unsigned)((n + 255) / 256), 256, 0, stream()>>>(
+        d_p, d_re, d_im, n, st->sec->dim, st->sec->d_iperm, st->d_amp, d_bad);
     count_launch();
     HSV_CHECK_LAUNCH();
-    dfree(d_v);
+    HSV_TRY_CUDA(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+    dfree(d_re);
+    dfree(d_im);
     dfree(d_p);
+    dfree(d_bad);
   }
   HSV_TRY(state_norm2_async(st));
-  return stream_sync();
+  HSV_TRY(stream_sync());
+  HSV_REQUIRE(!h_bad, HSV_ERR_INVALID, "position out of range for dimension %lld",
+              (long long)st->sec->dim);
+  return HSV_OK;
 }
 
 int hsv_state_set_keys(hsv_state st, const uint64_t* keys, const double* re, const double* im,

@@ -196,6 +196,32 @@ class SvState:
         return f"SvState(dim={len(self.basis)}, nnz={self.nnz})"
 
 
+class DevicePool:
+    """Operator pool resident on the device (compressed occ/virt masks)."""
+
+    __slots__ = ("basis", "handle", "n", "ops", "_sector_ref")
+
+    def __init__(self, basis: CiBasis, ops):
+        self.ops = tuple(ops)
+        self.basis = basis
+        self._sector_ref = None
+        occ = np.array([o.occ_mask for o in self.ops], dtype=np.uint64)
+        virt = np.array([o.virt_mask for o in self.ops], dtype=np.uint64)
+        sec = basis.sector
+        self._sector_ref = basis._sector
+        h = N.C.c_void_p()
+        N.call("hsv_pool_create", sec, N.ptr_u64(occ), N.ptr_u64(virt), occ.size, N.C.byref(h))
+        self.handle = h
+        self.n = occ.size
+
+    def __del__(self):
+        try:
+            if self.handle:
+                N.lib().hsv_pool_destroy(self.handle)
+        except Exception:
+            pass
+
+
 # --------------------------------------------------------------- operator
 class PauliOperator(CsrMatrix):
     """Matrix-free subspace Hamiltonian <b_i|H|b_j> (device x-grouped tables).
@@ -282,6 +308,13 @@ class PauliOperator(CsrMatrix):
         e = N.dbl()
         N.call("hsv_energy_screen", self.handle, s.device.handle, N.ptr_u64(occ),
                N.ptr_u64(virt), occ.size, N.C.byref(e), N.ptr_f64(g))
+        return float(e.value), g
+
+    def energy_screen_pool(self, s: "SvState", pool: "DevicePool") -> tuple[float, np.ndarray]:
+        g = np.empty(pool.n)
+        e = N.dbl()
+        N.call("hsv_energy_screen_pool", self.handle, s.device.handle, pool.handle,
+               N.C.byref(e), N.ptr_f64(g))
         return float(e.value), g
 
     def energy_gradient(self, hf_bits: int, occ_masks, virt_masks, thetas):
