@@ -157,7 +157,9 @@ def run_hsv(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     N.init(local)
-    stream = torch.cuda.current_stream()
+    # a real (non-legacy) stream shared by torch events, NCCL and libhsv launches
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     N.call("hsv_set_stream", N.C.c_void_p(stream.cuda_stream))
 
     sysm = hsv.MolecularSystem.bundled(CONFIG)

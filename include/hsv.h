@@ -179,6 +179,9 @@ HSV_API int hsv_energy_screen_pool_async(hsv_op op, hsv_state psi, hsv_pool pool
 HSV_API int hsv_energy_screen_pool(hsv_op op, hsv_state psi, hsv_pool pool, double* energy,
                                    double* grads);
 
+/* ---- tuning knobs: "apply_r" (rows per lane, 1/2/4), "screen_rows" ---- */
+HSV_API int hsv_set_tuning(const char* key, int64_t value);
+
 /* ---- live kernel timing (CUDA events on the launch stream) ---- */
 HSV_API int hsv_prof_enable(int on);
 /* synchronize, then fold recorded event pairs into per-kernel totals */

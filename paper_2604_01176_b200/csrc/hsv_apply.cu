@@ -111,9 +111,36 @@ __global__ void k_csr_rows(const uint32_t* __restrict__ Sa, const uint32_t* __re
 }
 
 // --------------------------------------------------------------- K1 apply
+// Packed per-group record of an x-local group, loaded with one or two 16-byte
+// uniform loads: meta = hb | shift << 8.
+template <typename W> struct Rec;
+template <> struct __align__(16) Rec<uint32_t> {
+  uint32_t xb, meta, xm, z0, mul, tab, pad0, pad1;
+};
+template <> struct __align__(16) Rec<uint64_t> {
+  uint32_t xb, meta, tab, pad0;
+  uint64_t xm, z0, mul, pad1;
+};
+template <typename W>
+__device__ __forceinline__ Rec<W> ldrec(const Rec<W>* p) {
+  Rec<W> r;
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  uint4* d = reinterpret_cast<uint4*>(&r);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Rec<W>) / 16); ++i) d[i] = __ldg(q + i);
+  return r;
+}
+
 // Warp-granular static schedule: a unit is 32*R consecutive beta rows of one
 // alpha row, so the alpha half of every sector test is warp-uniform and whole
 // buckets are skipped without divergence.  Each lane owns R rows.
+//
+// Matrix element of an x-local group (every z_t ^ z_0 inside the flip mask x):
+//   amp(b) = (-1)^popcount(b & z_0) * A_g[h(b & x)],
+// A_g precomputed on the host in the reference's sequential term order (exact:
+// IEEE rounding is symmetric under negation) and h a per-group perfect
+// multiply-shift hash of the in-sector patterns of b on x.  Other groups
+// (singles carrying number-operator Z's) run the sequential term loop.
 template <typename W, int SH, int R>
 __global__ void __launch_bounds__(256) k_apply(const ApplyArgs a) {
   const int lane = threadIdx.x & 31;
@@ -123,30 +150,63 @@ __global__ void __launch_bounds__(256) k_apply(const ApplyArgs a) {
   double er = 0.0, ei = 0.0;
   for (int64_t u = u0; u < u1; ++u) {
     const int64_t ra = a.a_lo + u / a.upr;
-    const int64_t ch = u % a.upr;
+    const int64_t rb0 = (u % a.upr) * (32 * R) + lane;
     const uint32_t sa = __ldg(a.Sa + ra);
     const int64_t rowbase = ra * a.Nb;
     W s[R];
     uint32_t sb[R];
-    int64_t idx[R];
-    bool live[R], inr[R];
-    double2 acc[R], pv[R];
-    bool anyl = false;
+    double2 acc[R];
+    unsigned live = 0u;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      const int64_t rb = ch * (32 * R) + k * 32 + lane;
-      inr[k] = rb < a.Nb;
-      sb[k] = inr[k] ? __ldg(a.Sb + rb) : 0u;
+      const int64_t rb = rb0 + k * 32;
+      const bool inr = rb < a.Nb;
+      sb[k] = inr ? __ldg(a.Sb + rb) : 0u;
       s[k] = (W)sa | ((W)sb[k] << SH);
-      idx[k] = rowbase + rb;
-      pv[k] = inr[k] ? a.psi[idx[k]] : make_double2(0.0, 0.0);
-      live[k] = inr[k] && (!a.energy_only || pv[k].x != 0.0 || pv[k].y != 0.0);
-      const double d = (a.diag && live[k]) ? a.diag[idx[k]] : 0.0;
-      acc[k] = make_double2(d * pv[k].x, d * pv[k].y);
-      anyl |= live[k];
+      const double2 pv = inr ? a.psi[rowbase + rb] : make_double2(0.0, 0.0);
+      const bool lv = inr && (!a.energy_only || pv.x != 0.0 || pv.y != 0.0);
+      const double d = (a.diag && lv) ? a.diag[rowbase + rb] : 0.0;
+      acc[k] = make_double2(d * pv.x, d * pv.y);
+      live |= lv ? (1u << k) : 0u;
     }
-    if (__any_sync(0xffffffffu, anyl)) {
-      for (int bk = 0; bk < a.n_buckets; ++bk) {
+    if (__any_sync(0xffffffffu, live != 0u)) {
+      // pass 1: x-local groups, amp = sign * table[hash(pattern)]
+      for (int bk = 0; bk < a.n_buckets_h; ++bk) {
+        const int4 B = __ldg(a.buckets + bk);
+        if (__popc(sa & (uint32_t)B.x) != B.y) continue;
+        const double2* __restrict__ prow =
+            a.psi + (int64_t)__ldg(a.Ra + (sa ^ (uint32_t)B.x)) * a.Nb;
+        const Rec<W>* __restrict__ rp = reinterpret_cast<const Rec<W>*>(a.recs);
+        Rec<W> cur = ldrec(rp + B.z);
+        for (int g = B.z; g < B.w; ++g) {
+          const Rec<W> nxt = ldrec(rp + (g + 1 < B.w ? g + 1 : g));   // prefetch
+          const uint32_t xb = cur.xb;
+          const int hb = (int)(cur.meta & 0xffu);
+          unsigned v = 0u;
+#pragma unroll
+          for (int k = 0; k < R; ++k)
+            v |= ((live >> k) & 1u) && __popc(sb[k] & xb) == hb ? (1u << k) : 0u;
+          if (__any_sync(0xffffffffu, v != 0u)) {
+            const int shift = (int)((cur.meta >> 8) & 0xffu);
+            const double* __restrict__ tab = a.tabs + cur.tab;
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+              const unsigned h = (unsigned)((W)((s[k] & cur.xm) * cur.mul) >> shift);
+              const double A = __ldg(tab + h);
+              const int sgn = popc(s[k] & cur.z0) << 31;
+              const double amp = __hiloint2double(__double2hiint(A) ^ sgn, __double2loint(A));
+              if ((v >> k) & 1u) {
+                const double2 p = prow[__ldg(a.Rb + (sb[k] ^ xb))];
+                acc[k].x = fma(amp, p.x, acc[k].x);
+                acc[k].y = fma(amp, p.y, acc[k].y);
+              }
+            }
+          }
+          cur = nxt;
+        }
+      }
+      // pass 2: remaining groups, sequential term loop in reference order
+      for (int bk = a.n_buckets_h; bk < a.n_buckets; ++bk) {
         const int4 B = __ldg(a.buckets + bk);
         if (__popc(sa & (uint32_t)B.x) != B.y) continue;
         const double2* __restrict__ prow =
@@ -154,14 +214,11 @@ __global__ void __launch_bounds__(256) k_apply(const ApplyArgs a) {
         for (int g = B.z; g < B.w; ++g) {
           const int4 G = __ldg(a.groups + g);
           const uint32_t xb = (uint32_t)G.x;
-          bool v[R];
-          bool anyv = false;
+          unsigned v = 0u;
 #pragma unroll
-          for (int k = 0; k < R; ++k) {
-            v[k] = live[k] && __popc(sb[k] & xb) == G.y;
-            anyv |= v[k];
-          }
-          if (!__any_sync(0xffffffffu, anyv)) continue;
+          for (int k = 0; k < R; ++k)
+            v |= ((live >> k) & 1u) && __popc(sb[k] & xb) == G.y ? (1u << k) : 0u;
+          if (!__any_sync(0xffffffffu, v != 0u)) continue;
           double amp[R];
 #pragma unroll
           for (int k = 0; k < R; ++k) amp[k] = 0.0;
@@ -173,7 +230,7 @@ __global__ void __launch_bounds__(256) k_apply(const ApplyArgs a) {
           }
 #pragma unroll
           for (int k = 0; k < R; ++k) {
-            if (v[k]) {
+            if ((v >> k) & 1u) {
               const double2 p = prow[__ldg(a.Rb + (sb[k] ^ xb))];
               acc[k].x = fma(amp[k], p.x, acc[k].x);
               acc[k].y = fma(amp[k], p.y, acc[k].y);
@@ -184,14 +241,18 @@ __global__ void __launch_bounds__(256) k_apply(const ApplyArgs a) {
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      if (!inr[k]) continue;
+      const int64_t rb = rb0 + k * 32;
+      if (rb >= a.Nb) continue;
       if (a.out) {
         double2 y = acc[k];
         if (a.prune > 0.0 && sqrt(y.x * y.x + y.y * y.y) < a.prune) y = make_double2(0.0, 0.0);
-        a.out[idx[k]] = y;
+        a.out[rowbase + rb] = y;
       }
-      er += pv[k].x * acc[k].x + pv[k].y * acc[k].y;
-      ei += pv[k].x * acc[k].y - pv[k].y * acc[k].x;
+      if (a.epart && ((live >> k) & 1u)) {
+        const double2 pv = a.psi[rowbase + rb];
+        er += pv.x * acc[k].x + pv.y * acc[k].y;
+        ei += pv.x * acc[k].y - pv.y * acc[k].x;
+      }
     }
   }
   if (a.epart) {
@@ -225,13 +286,10 @@ static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
 }
 
 int apply_warps(const hsv_op_s* op) {
-  // number of warps the apply kernel will use (for energy-partial sizing)
-  int occ = 0;
-  if (op->sec->wide)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<uint64_t, 32, kApplyR>, 256, 0);
-  else
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<uint32_t, 16, kApplyR>, 256, 0);
-  return ctx().num_sms * std::max(occ, 1) * 8;
+  // upper bound on the warps the apply kernel uses (energy-partial sizing):
+  // 256-thread blocks, at most 8 resident per SM
+  (void)op;
+  return ctx().num_sms * 64;
 }
 
 int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* epart,
@@ -241,10 +299,89 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   a.Sa = s->d_Sa; a.Sb = s->d_Sb; a.Ra = s->d_Ra; a.Rb = s->d_Rb;
   a.buckets = op->d_buckets; a.n_buckets = (int)op->n_buckets;
   a.groups = op->d_groups; a.terms = op->d_terms; a.diag = op->d_diag;
+  a.tabs = op->d_tabs; a.recs = op->d_recs; a.n_buckets_h = (int)op->n_buckets_h;
   a.psi = psi; a.out = out; a.epart = epart;
   a.Nb = s->Nb; a.a_lo = a_lo; a.a_hi = a_hi; a.prune = prune; a.energy_only = energy_only;
-  if (s->wide) return launch_apply_t<uint64_t, 32, kApplyR>(a, n_warps);
-  return launch_apply_t<uint32_t, 16, kApplyR>(a, n_warps);
+  const int R = tuning().apply_r;
+  if (s->wide) {
+    if (R == 1) return launch_apply_t<uint64_t, 32, 1>(a, n_warps);
+    if (R == 4) return launch_apply_t<uint64_t, 32, 4>(a, n_warps);
+    return launch_apply_t<uint64_t, 32, 2>(a, n_warps);
+  }
+  if (R == 1) return launch_apply_t<uint32_t, 16, 1>(a, n_warps);
+  if (R == 4) return launch_apply_t<uint32_t, 16, 4>(a, n_warps);
+  return launch_apply_t<uint32_t, 16, 2>(a, n_warps);
+}
+
+// Host: does group [t0, t1) admit amp(b) = (-1)^popc(b&z0) * A[h(b & x)]?  If
+// so, fill a perfect multiply-shift hash over the in-sector patterns of b on
+// x (ha of the alpha bits, hb of the beta bits set) and append A, summed in
+// the reference's term order, to `tabs`.
+static uint64_t splitmix(uint64_t& st) {
+  uint64_t z = (st += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+bool build_group_hash(const std::vector<Term>& terms, int t0, int t1, uint64_t xp, int ha,
+                      int hb, int SH, GroupHash& gh, std::vector<double>& tabs) {
+  gh = GroupHash{0, 0, 0, 0, -1};
+  if (t1 <= t0) return false;
+  const uint64_t z0 = terms[t0].z;
+  for (int t = t0; t < t1; ++t)
+    if ((terms[t].z ^ z0) & ~xp) return false;          // not x-local
+  std::vector<int> bits;
+  for (int q = 0; q < 64; ++q)
+    if ((xp >> q) & 1ull) bits.push_back(q);
+  if (bits.size() > 12) return false;
+  const uint64_t amask = SH == 16 ? 0xffffull : 0xffffffffull;
+  std::vector<uint64_t> pats;
+  std::vector<double> vals;
+  for (uint32_t m = 0; m < (1u << bits.size()); ++m) {
+    uint64_t t = 0;
+    for (size_t i = 0; i < bits.size(); ++i)
+      if ((m >> i) & 1u) t |= 1ull << bits[i];
+    if (__builtin_popcountll(t & amask) != ha || __builtin_popcountll(t & ~amask) != hb) continue;
+    double A = 0.0;
+    for (int q = t0; q < t1; ++q)
+      A += (__builtin_popcountll(t & (terms[q].z ^ z0)) & 1) ? -terms[q].c : terms[q].c;
+    pats.push_back(t);
+    vals.push_back(A);
+  }
+  if (pats.empty()) return false;
+  const int wbits = SH == 16 ? 32 : 64;
+  int b0 = 0;
+  while ((1u << b0) < pats.size()) ++b0;
+  uint64_t seed = xp * 0x2545f4914f6cdd1dull + 1;
+  for (int B = std::max(b0, 1); B <= b0 + 3 && B <= 8; ++B) {
+    for (int tries = 0; tries < 20000; ++tries) {
+      const uint64_t mul = splitmix(seed) | 1ull;
+      uint64_t used[4] = {0, 0, 0, 0};
+      bool ok = true;
+      for (uint64_t t : pats) {
+        const uint64_t prod = wbits == 32 ? (uint64_t)(uint32_t)((uint32_t)t * (uint32_t)mul)
+                                          : t * mul;
+        const unsigned h = (unsigned)(prod >> (wbits - B));
+        if ((used[h >> 6] >> (h & 63)) & 1ull) { ok = false; break; }
+        used[h >> 6] |= 1ull << (h & 63);
+      }
+      if (!ok) continue;
+      gh.z0 = z0;
+      gh.xm = xp;
+      gh.mul = wbits == 32 ? (uint64_t)(uint32_t)mul : mul;
+      gh.shift = wbits - B;
+      gh.tab = (int32_t)tabs.size();
+      tabs.resize(tabs.size() + (1u << B), 0.0);
+      for (size_t i = 0; i < pats.size(); ++i) {
+        const uint64_t prod = wbits == 32 ? (uint64_t)(uint32_t)((uint32_t)pats[i] * (uint32_t)mul)
+                                          : pats[i] * mul;
+        tabs[gh.tab + (prod >> (wbits - B))] = vals[i];
+      }
+      return true;
+    }
+  }
+  return false;
 }
 
 }  // namespace hsv
@@ -423,11 +560,82 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
   }
   op->n_active = (int64_t)act.size();
   op->n_buckets = (int64_t)op->buckets.size();
+  // ---- pattern tables for x-local groups ----
+  std::vector<GroupHash> ghash(op->groups.size());
+  std::vector<double> tabs;
+  for (size_t q = 0; q < op->groups.size(); ++q) {
+    const HGroup& g = hg[act[q]];
+    const uint64_t xp = (uint64_t)g.xa | ((uint64_t)g.xb << SH);
+    if (build_group_hash(op->terms, op->groups[q].z, op->groups[q].w, xp, g.pa / 2, g.pb / 2,
+                         SH, ghash[q], tabs))
+      ++op->n_hashed;
+  }
+  // Kernel layout: hashed groups first, then term-loop groups, each bucketed by
+  // alpha flip part (the order of groups only changes the summation order of
+  // distinct matrix elements, never an element's value).
+  {
+    std::vector<int4> nb, ng;
+    std::vector<GroupHash> nh;
+    const std::vector<int4> ob = op->buckets, og = op->groups;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (const int4& B : ob) {
+        bool opened = false;
+        for (int q = B.z; q < B.w; ++q) {
+          const bool hashed = ghash[q].tab >= 0;
+          if (hashed != (pass == 0)) continue;
+          if (!opened) {
+            nb.push_back(make_int4(B.x, B.y, (int)ng.size(), (int)ng.size()));
+            opened = true;
+          }
+          ng.push_back(og[q]);
+          nh.push_back(ghash[q]);
+          nb.back().w = (int)ng.size();
+        }
+      }
+      if (pass == 0) op->n_buckets_h = (int64_t)nb.size();
+    }
+    op->buckets = nb;
+    op->groups = ng;
+    ghash = nh;
+    op->n_buckets = (int64_t)nb.size();
+  }
+  std::vector<unsigned char> recs;
+  if (SH == 16) {
+    recs.resize(ghash.size() * 32);
+    for (size_t q = 0; q < ghash.size(); ++q) {
+      const GroupHash& h = ghash[q];
+      uint32_t r[8] = {(uint32_t)op->groups[q].x,
+                       (uint32_t)op->groups[q].y | ((uint32_t)h.shift << 8), (uint32_t)h.xm,
+                       (uint32_t)h.z0, (uint32_t)h.mul, (uint32_t)std::max(h.tab, 0), 0u, 0u};
+      memcpy(&recs[q * 32], r, 32);
+    }
+  } else {
+    recs.resize(ghash.size() * 48);
+    for (size_t q = 0; q < ghash.size(); ++q) {
+      const GroupHash& h = ghash[q];
+      uint32_t r[4] = {(uint32_t)op->groups[q].x,
+                       (uint32_t)op->groups[q].y | ((uint32_t)h.shift << 8),
+                       (uint32_t)std::max(h.tab, 0), 0u};
+      uint64_t r2[4] = {h.xm, h.z0, h.mul, 0ull};
+      memcpy(&recs[q * 48], r, 16);
+      memcpy(&recs[q * 48 + 16], r2, 32);
+    }
+  }
   if ((rc = dalloc(&op->d_buckets, op->buckets.size())) ||
       (rc = dalloc(&op->d_groups, op->groups.size())) ||
-      (rc = dalloc(&op->d_terms, op->terms.size())))
+      (rc = dalloc(&op->d_terms, op->terms.size())) ||
+      (rc = dalloc(&op->d_ghash, ghash.size())) || (rc = dalloc(&op->d_tabs, tabs.size())) ||
+      (rc = dalloc(reinterpret_cast<unsigned char**>(&op->d_recs), recs.size())))
     return fail(rc);
   cudaStream_t st = stream();
+  if (!recs.empty())
+    HSV_TRY_CUDA(cudaMemcpyAsync(op->d_recs, recs.data(), recs.size(), cudaMemcpyHostToDevice, st));
+  if (!ghash.empty())
+    HSV_TRY_CUDA(cudaMemcpyAsync(op->d_ghash, ghash.data(), ghash.size() * sizeof(GroupHash),
+                                 cudaMemcpyHostToDevice, st));
+  if (!tabs.empty())
+    HSV_TRY_CUDA(cudaMemcpyAsync(op->d_tabs, tabs.data(), tabs.size() * sizeof(double),
+                                 cudaMemcpyHostToDevice, st));
   if (!op->buckets.empty())
     HSV_TRY_CUDA(cudaMemcpyAsync(op->d_buckets, op->buckets.data(),
                                  op->buckets.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
@@ -449,6 +657,9 @@ int hsv_op_destroy(hsv_op op) {
   dfree(op->d_groups);
   dfree(op->d_terms);
   dfree(op->d_diag);
+  dfree(op->d_ghash);
+  dfree(op->d_tabs);
+  dfree(reinterpret_cast<unsigned char*>(op->d_recs));
   delete op;
   return HSV_OK;
 }

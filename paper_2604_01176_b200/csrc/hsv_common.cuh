@@ -139,6 +139,16 @@ struct Term {          // 16 B: one pre-signed coefficient and its packed z mask
   double c;            // coeff * (-1)^(nY/2)   (svengine.py:140-144)
   uint64_t z;          // packed z: za | zb << SH
 };
+// Per active group: sign mask, pattern mask and perfect multiply-shift hash of
+// an x-local group (tab >= 0), or tab = -1 for the sequential term loop.
+struct GroupHash {
+  uint64_t z0;
+  uint64_t xm;
+  uint64_t mul;
+  int32_t shift;
+  int32_t tab;
+};
+
 struct hsv_op_s {
   hsv_sector sec = nullptr;
   int64_t n_terms = 0, n_groups = 0, n_active = 0, n_buckets = 0;
@@ -146,6 +156,11 @@ struct hsv_op_s {
   int4* d_groups = nullptr;    // {xb, xb_pop/2, t0, t1}
   Term* d_terms = nullptr;
   double* d_diag = nullptr;    // per internal row; nullptr if no diagonal terms
+  GroupHash* d_ghash = nullptr;
+  void* d_recs = nullptr;       // packed Rec<W> per group (kernel layout)
+  int64_t n_buckets_h = 0;      // buckets [0, n_buckets_h) are x-local (hashed)
+  double* d_tabs = nullptr;
+  int64_t n_hashed = 0;
   // host copies of the active group table (for CSR materialization)
   std::vector<int4> buckets, groups;
   std::vector<Term> terms;
@@ -155,6 +170,9 @@ struct hsv_pool_s {
   hsv_sector sec = nullptr;
   int64_t n = 0;
   int4* d = nullptr;          // {oa, va, ob, vb} compressed masks
+  int* d_order = nullptr;     // operators in alpha-part order (screen kernel)
+  int2* d_opl = nullptr;      // per operator: beta list {offset, length}, length -1: empty beta half
+  int2* d_blist = nullptr;    // beta source lists {rb_src, rb_tgt}
   std::vector<int4> h;
 };
 

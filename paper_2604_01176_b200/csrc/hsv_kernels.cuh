@@ -4,7 +4,12 @@
 
 namespace hsv {
 
-constexpr int kApplyR = 2;   // rows per lane in the K1 apply kernel
+// Runtime tuning knobs (hsv_set_tuning); defaults are the measured best.
+struct Tuning {
+  int apply_r = 2;        // rows per lane in the K1 apply kernel (1, 2, 4)
+  int screen_rows = 1024; // rows staged per chunk in the screen kernel
+};
+Tuning& tuning();
 
 struct ApplyArgs {
   const uint32_t* Sa;
@@ -13,9 +18,13 @@ struct ApplyArgs {
   const uint32_t* Rb;
   const int4* buckets;
   int n_buckets;
+  int n_buckets_h;     // buckets [0, n_buckets_h) hold x-local (hashed) groups
+  const void* recs;    // Rec<W> per hashed group (same index as groups)
   const int4* groups;
   const Term* terms;
   const double* diag;
+  const GroupHash* ghash;
+  const double* tabs;
   const double2* psi;
   double2* out;      // nullptr: energy only
   double* epart;     // [warps][2] energy partials or nullptr
@@ -47,7 +56,8 @@ struct PairLists {
 };
 int build_pair_lists_async(const hsv_sector_s* s, const OpMasks& m, PairLists& pl);
 
-int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w, const int4* d_ops,
-                  int n_ops, int64_t row_lo, int64_t row_hi, double* d_grads);
+int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
+                  const hsv_pool_s* pool, int64_t a_lo, int64_t a_hi, double* d_grads);
+int pool_prepare(hsv_pool_s* p);
 
 }  // namespace hsv

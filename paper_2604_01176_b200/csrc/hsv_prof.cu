@@ -20,6 +20,8 @@ struct Prof {
   std::map<std::string, std::pair<double, int64_t>> acc;
 };
 static Prof g_prof;
+static Tuning g_tuning;
+Tuning& tuning() { return g_tuning; }
 
 static cudaEvent_t take_event() {
   if (g_prof.free_ev.empty()) {
@@ -50,6 +52,22 @@ ProfScope::~ProfScope() {
 using namespace hsv;
 
 extern "C" {
+
+int hsv_set_tuning(const char* key, int64_t value) {
+  HSV_REQUIRE(key, HSV_ERR_INVALID, "null key");
+  const std::string k(key);
+  if (k == "apply_r") {
+    HSV_REQUIRE(value == 1 || value == 2 || value == 4, HSV_ERR_INVALID, "apply_r must be 1, 2 or 4");
+    g_tuning.apply_r = (int)value;
+  } else if (k == "screen_rows") {
+    HSV_REQUIRE(value >= 64 && value <= 8192, HSV_ERR_INVALID, "screen_rows out of range");
+    g_tuning.screen_rows = (int)value;
+  } else {
+    set_error(HSV_ERR_INVALID, "unknown tuning key '%s'", key);
+    return HSV_ERR_INVALID;
+  }
+  return HSV_OK;
+}
 
 int hsv_prof_enable(int on) {
   g_prof.on = on != 0;
@@ -104,7 +122,7 @@ int hsv_pool_create(hsv_sector s, const uint64_t* occ, const uint64_t* virt, int
   int rc = dalloc(&p->d, n);
   if (rc) { delete p; return rc; }
   if (n) HSV_TRY_CUDA(cudaMemcpyAsync(p->d, p->h.data(), n * sizeof(int4), cudaMemcpyHostToDevice, stream()));
-  HSV_TRY(stream_sync());
+  if ((rc = pool_prepare(p))) { hsv_pool_destroy(p); return rc; }
   *out = p;
   return HSV_OK;
 }
@@ -112,6 +130,9 @@ int hsv_pool_create(hsv_sector s, const uint64_t* occ, const uint64_t* virt, int
 int hsv_pool_destroy(hsv_pool p) {
   if (!p) return HSV_OK;
   dfree(p->d);
+  dfree(p->d_order);
+  dfree(p->d_opl);
+  dfree(p->d_blist);
   delete p;
   return HSV_OK;
 }

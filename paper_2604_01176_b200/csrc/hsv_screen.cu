@@ -5,140 +5,198 @@
 // Row formulation (owner computes): for an owned row b,
 //   (T_k psi)_b = +psi_{b^f}  if b is in target pattern (V set, O clear),
 //               = -psi_{b^f}  if b is in source pattern (O set, V clear),
-// so only w_b = (H psi)_b of owned rows is needed and psi (replicated) is
-// gathered at the partner.  Each CTA owns a contiguous, equal share of rows,
-// stages them in shared memory in chunks, and each warp owns a fixed subset
-// of operators; per-operator sums are reduced in a fixed order.
+// so only w = H psi on owned rows is needed and psi (replicated) is gathered
+// at the partner b^f.
+//
+// A CTA owns one alpha row and a slice of the operators; a warp owns one
+// operator at a time.  If the alpha half of the row is in source (target)
+// pattern, the matching beta strings are exactly the operator's precomputed
+// beta source list (its partners), so the warp walks that list -- no per-row
+// tests, work proportional to the matches.  Operators are processed in
+// alpha-part order so the warps of a CTA share partner rows in L1.  Each
+// (alpha row, operator) partial is written once and reduced over alpha rows
+// in a fixed order: bitwise deterministic.
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cmath>
+#include <map>
 
 #include "hsv_common.cuh"
 #include "hsv_kernels.cuh"
 
 namespace hsv {
 
-constexpr int kScreenRows = 1024;
 constexpr int kScreenBlock = 256;
+constexpr int kScreenWarps = kScreenBlock / 32;
 
 struct ScreenArgs {
   const uint32_t* Sa;
-  const uint32_t* Sb;
   const uint32_t* Ra;
-  const uint32_t* Rb;
-  const int4* ops;     // {oa, va, ob, vb}
+  const int4* ops;       // {oa, va, ob, vb} (compressed)
+  const int* order;      // operator indices in alpha-part order
+  const int2* opl;       // per operator: {beta list offset, length}; length < 0: empty beta half
+  const int2* blist;     // beta source lists: {rb_src, rb_tgt}
   int n_ops;
   const double2* psi;
   const double2* w;
   int64_t Nb;
-  int64_t row_lo, row_hi;
-  double* part;        // [gridDim.x][n_ops]
+  int64_t a_lo;
+  int slices;
+  double* part;          // [alpha rows][n_ops]
 };
 
-__global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  double2* s_w = reinterpret_cast<double2*>(smem);
-  uint32_t* s_sb = reinterpret_cast<uint32_t*>(s_w + kScreenRows);
-  double* acc = reinterpret_cast<double*>(s_sb + kScreenRows);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kScreenBlock / 32;
-  const int64_t nrows = a.row_hi - a.row_lo;
-  const int64_t r0 = a.row_lo + nrows * blockIdx.x / gridDim.x;
-  const int64_t r1 = a.row_lo + nrows * (blockIdx.x + 1) / gridDim.x;
-  for (int q = threadIdx.x; q < a.n_ops; q += kScreenBlock) acc[q] = 0.0;
-  for (int64_t c0 = r0; c0 < r1; c0 += kScreenRows) {
-    const int n = (int)imin64(kScreenRows, r1 - c0);
-    __syncthreads();
-    for (int i = threadIdx.x; i < n; i += kScreenBlock) {
-      const int64_t idx = c0 + i;
-      const int64_t rb = idx % a.Nb;
-      s_sb[i] = __ldg(a.Sb + rb);
-      s_w[i] = a.w[idx];
-    }
-    __syncthreads();
-    const int64_t ra_first = c0 / a.Nb;
-    for (int op = warp; op < a.n_ops; op += nw) {
-      const int4 O = __ldg(a.ops + op);
-      const uint32_t oa = (uint32_t)O.x, va = (uint32_t)O.y, ob = (uint32_t)O.z, vb = (uint32_t)O.w;
-      const uint32_t fa = oa | va, fb = ob | vb;
-      double g = 0.0;
-      // alpha-uniform segments of the chunk
-      int lo = 0;
-      for (int64_t ra = ra_first; lo < n; ++ra) {
-        const int hi = (int)imin64(n, (ra + 1) * a.Nb - c0);
-        const uint32_t sa = __ldg(a.Sa + ra);
-        const bool as = (sa & oa) == oa && (sa & va) == 0;
-        const bool at = (sa & va) == va && (sa & oa) == 0;
-        if (as || at) {
-          const double2* __restrict__ prow = a.psi + (int64_t)__ldg(a.Ra + (sa ^ fa)) * a.Nb;
-          for (int r = lo + lane; r < hi; r += 32) {
-            const uint32_t sb = s_sb[r];
-            const bool bs = (sb & ob) == ob && (sb & vb) == 0;
-            const bool bt = (sb & vb) == vb && (sb & ob) == 0;
-            const bool tgt = at && bt, src = as && bs;
-            if (tgt || src) {
-              const double2 p = prow[__ldg(a.Rb + (sb ^ fb))];
-              const double2 wv = s_w[r];
-              const double x = wv.x * p.x + wv.y * p.y;   // Re conj(w_b) psi_{b^f}
-              g += tgt ? x : -x;
-            }
-          }
-        }
-        lo = hi;
-      }
-      g = warp_sum(g);
-      if (lane == 0) acc[op] += g;
-    }
-  }
-  __syncthreads();
-  for (int q = threadIdx.x; q < a.n_ops; q += kScreenBlock)
-    a.part[(int64_t)blockIdx.x * a.n_ops + q] = 2.0 * acc[q];
+__device__ __forceinline__ double re_conj_mul(double2 a, double2 b) {
+  return a.x * b.x + a.y * b.y;   // Re(conj(a) b)
 }
 
-int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w, const int4* d_ops,
-                  int n_ops, int64_t row_lo, int64_t row_hi, double* d_grads) {
-  const hsv_sector_s* s = op->sec;
-  if (n_ops <= 0) return HSV_OK;
-  const size_t smem = kScreenRows * (sizeof(double2) + sizeof(uint32_t)) + n_ops * sizeof(double);
-  HSV_REQUIRE(smem <= 227 * 1024, HSV_ERR_UNSUPPORTED, "operator pool too large (%d)", n_ops);
-  HSV_TRY_CUDA(cudaFuncSetAttribute(k_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = 0;
-  HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_screen, kScreenBlock, smem));
-  occ = std::max(occ, 1);
-  const int64_t nrows = row_hi - row_lo;
-  int64_t grid = (int64_t)ctx().num_sms * occ;
-  grid = std::max<int64_t>(1, std::min(grid, (nrows + 255) / 256));
-  double* part = nullptr;
-  HSV_TRY(dalloc(&part, grid * n_ops));
-  ScreenArgs a{};
-  a.Sa = s->d_Sa; a.Sb = s->d_Sb; a.Ra = s->d_Ra; a.Rb = s->d_Rb;
-  a.ops = d_ops; a.n_ops = n_ops; a.psi = psi; a.w = w; a.Nb = s->Nb;
-  a.row_lo = row_lo; a.row_hi = row_hi; a.part = part;
-  if (nrows > 0) {
-    {
-      ProfScope prof("screen");
-      k_screen<<<(unsigned)grid, kScreenBlock, smem, stream()>>>(a);
+__global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t rloc = blockIdx.y;
+  const int64_t ra = a.a_lo + rloc;
+  const uint32_t sa = __ldg(a.Sa + ra);
+  const double2* __restrict__ wrow = a.w + ra * a.Nb;
+  const int stride = a.slices * kScreenWarps;
+  for (int q = blockIdx.x * kScreenWarps + warp; q < a.n_ops; q += stride) {
+    const int op = __ldg(a.order + q);
+    const int4 O = __ldg(a.ops + op);
+    const uint32_t oa = (uint32_t)O.x, va = (uint32_t)O.y;
+    const uint32_t fa = oa | va;
+    const uint32_t ma = sa & fa;
+    const bool as = ma == oa, at = ma == va;   // both for an empty alpha half
+    double g = 0.0;
+    if (as || at) {
+      const double2* __restrict__ prow = a.psi + (int64_t)__ldg(a.Ra + (sa ^ fa)) * a.Nb;
+      const int2 L = __ldg(a.opl + op);
+      if (L.y < 0) {
+        // empty beta half: every beta string is both source and target (alpha decides)
+        for (int64_t j = lane; j < a.Nb; j += 32) g += re_conj_mul(wrow[j], prow[j]);
+        if (!at) g = -g;
+      } else {
+        const int2* __restrict__ lst = a.blist + L.x;
+        if (as)   // own rows in source pattern: (T psi)_b = -psi_p
+          for (int j = lane; j < L.y; j += 32) {
+            const int2 e = __ldg(lst + j);
+            g -= re_conj_mul(wrow[e.x], prow[e.y]);
+          }
+        if (at)   // own rows in target pattern: (T psi)_b = +psi_p
+          for (int j = lane; j < L.y; j += 32) {
+            const int2 e = __ldg(lst + j);
+            g += re_conj_mul(wrow[e.y], prow[e.x]);
+          }
+      }
     }
+    g = warp_sum(g);
+    if (lane == 0) a.part[rloc * a.n_ops + op] = 2.0 * g;
+  }
+}
+
+// One block per beta pattern: rank-ascending source strings and partners.
+__global__ void __launch_bounds__(1024) k_beta_lists(const uint32_t* __restrict__ Sb,
+                                                     const uint32_t* __restrict__ Rb, int64_t Nb,
+                                                     const int4* __restrict__ pats,
+                                                     int2* __restrict__ out) {
+  using Scan = cub::BlockScan<int, 1024>;
+  __shared__ typename Scan::TempStorage tmp;
+  const int4 P = pats[blockIdx.x];   // {ob, vb, offset, count}
+  const uint32_t ob = (uint32_t)P.x, vb = (uint32_t)P.y, fb = ob | vb;
+  int base = P.z;
+  for (int64_t c0 = 0; c0 < Nb; c0 += 1024) {
+    const int64_t i = c0 + threadIdx.x;
+    uint32_t s = 0;
+    int f = 0;
+    if (i < Nb) {
+      s = Sb[i];
+      f = (s & fb) == ob ? 1 : 0;
+    }
+    int off, tot;
+    Scan(tmp).ExclusiveSum(f, off, tot);
+    if (f) out[base + off] = make_int2((int)i, (int)Rb[s ^ fb]);
+    base += tot;
+    __syncthreads();
+  }
+}
+
+int pool_prepare(hsv_pool_s* p) {
+  const hsv_sector_s* s = p->sec;
+  const int64_t n = p->n;
+  std::map<std::pair<uint32_t, uint32_t>, int> pid;
+  std::vector<int4> pats;
+  std::vector<int2> opl(n);
+  int64_t total = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const uint32_t ob = (uint32_t)p->h[i].z, vb = (uint32_t)p->h[i].w;
+    if ((ob | vb) == 0) { opl[i] = make_int2(0, -1); continue; }
+    auto key = std::make_pair(ob, vb);
+    auto it = pid.find(key);
+    if (it == pid.end()) {
+      const int64_t cnt = src_count(s->norb, s->n_beta, ob, vb);
+      pats.push_back(make_int4((int)ob, (int)vb, (int)total, (int)cnt));
+      it = pid.emplace(key, (int)pats.size() - 1).first;
+      total += cnt;
+    }
+    opl[i] = make_int2(pats[it->second].z, pats[it->second].w);
+  }
+  HSV_REQUIRE(total < INT32_MAX, HSV_ERR_UNSUPPORTED, "beta pattern lists too large");
+  std::vector<int> order(n);
+  for (int64_t i = 0; i < n; ++i) order[i] = (int)i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+    const uint32_t fx = (uint32_t)(p->h[x].x | p->h[x].y), fy = (uint32_t)(p->h[y].x | p->h[y].y);
+    return fx != fy ? fx < fy : (uint32_t)p->h[x].x < (uint32_t)p->h[y].x;
+  });
+  HSV_TRY(dalloc(&p->d_order, n));
+  HSV_TRY(dalloc(&p->d_opl, n));
+  HSV_TRY(dalloc(&p->d_blist, total));
+  int4* d_pats = nullptr;
+  HSV_TRY(dalloc(&d_pats, pats.size()));
+  cudaStream_t st = stream();
+  if (n) {
+    HSV_TRY_CUDA(cudaMemcpyAsync(p->d_order, order.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
+    HSV_TRY_CUDA(cudaMemcpyAsync(p->d_opl, opl.data(), n * sizeof(int2), cudaMemcpyHostToDevice, st));
+  }
+  if (!pats.empty()) {
+    HSV_TRY_CUDA(cudaMemcpyAsync(d_pats, pats.data(), pats.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
+    k_beta_lists<<<(unsigned)pats.size(), 1024, 0, st>>>(s->d_Sb, s->d_Rb, s->Nb, d_pats, p->d_blist);
     count_launch();
     HSV_CHECK_LAUNCH();
-    HSV_TRY(reduce_sum_f64(part, grid, n_ops, n_ops, d_grads));
-  } else {
-    HSV_TRY_CUDA(cudaMemsetAsync(d_grads, 0, n_ops * sizeof(double), stream()));
   }
-  dfree(part);
+  HSV_TRY(stream_sync());
+  dfree(d_pats);
   return HSV_OK;
 }
 
-static int upload_ops(const hsv_sector_s* s, const uint64_t* occ, const uint64_t* virt, int64_t n,
-                      int4** d_ops) {
-  std::vector<int4> h(n);
-  for (int64_t i = 0; i < n; ++i) {
-    HSV_REQUIRE((occ[i] & virt[i]) == 0 && occ[i] && virt[i], HSV_ERR_INVALID,
-                "excitation indices must be distinct");
-    OpMasks m = compress_op(s, occ[i], virt[i]);
-    h[i] = make_int4((int)m.oa, (int)m.va, (int)m.ob, (int)m.vb);
+int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
+                  const hsv_pool_s* pool, int64_t a_lo, int64_t a_hi, double* d_grads) {
+  const hsv_sector_s* s = op->sec;
+  const int n_ops = (int)pool->n;
+  if (n_ops <= 0) return HSV_OK;
+  const int64_t rows = a_hi - a_lo;
+  if (rows <= 0) {
+    HSV_TRY_CUDA(cudaMemsetAsync(d_grads, 0, n_ops * sizeof(double), stream()));
+    return HSV_OK;
   }
-  HSV_TRY(dalloc(d_ops, n));
-  if (n) HSV_TRY_CUDA(cudaMemcpyAsync(*d_ops, h.data(), n * sizeof(int4), cudaMemcpyHostToDevice, stream()));
-  return stream_sync();
+  HSV_REQUIRE(rows <= 65535, HSV_ERR_UNSUPPORTED, "too many alpha rows for one launch");
+  // enough CTAs to fill the machine several times over
+  const int64_t want = (int64_t)ctx().num_sms * 8 * 4;
+  int slices = (int)std::min<int64_t>((want + rows - 1) / rows,
+                                      (n_ops + kScreenWarps - 1) / kScreenWarps);
+  slices = std::max(slices, 1);
+  double* part = nullptr;
+  HSV_TRY(dalloc(&part, rows * n_ops));
+  ScreenArgs a{};
+  a.Sa = s->d_Sa; a.Ra = s->d_Ra;
+  a.ops = pool->d; a.order = pool->d_order; a.opl = pool->d_opl; a.blist = pool->d_blist;
+  a.n_ops = n_ops; a.psi = psi; a.w = w; a.Nb = s->Nb; a.a_lo = a_lo; a.slices = slices;
+  a.part = part;
+  {
+    ProfScope prof("screen");
+    k_screen<<<dim3((unsigned)slices, (unsigned)rows), kScreenBlock, 0, stream()>>>(a);
+  }
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  HSV_TRY(reduce_sum_f64(part, rows, n_ops, n_ops, d_grads));
+  dfree(part);
+  return HSV_OK;
 }
 
 }  // namespace hsv
@@ -147,8 +205,8 @@ using namespace hsv;
 
 extern "C" {
 
-static int energy_screen_dev(hsv_op op, hsv_state psi, const int4* d_ops, int64_t n_ops,
-                             int64_t a_lo, int64_t a_hi, double* d_out) {
+static int energy_screen_dev(hsv_op op, hsv_state psi, const hsv_pool_s* pool, int64_t a_lo,
+                             int64_t a_hi, double* d_out) {
   const hsv_sector_s* s = op->sec;
   double2* w = nullptr;
   HSV_TRY(dalloc(&w, s->dim));
@@ -159,7 +217,7 @@ static int energy_screen_dev(hsv_op op, hsv_state psi, const int4* d_ops, int64_
   int64_t used = 0;
   HSV_TRY(launch_apply(op, psi->d_amp, w, epart, a_lo, a_hi, 0.0, 0, &used));
   HSV_TRY(reduce_sum_f64(epart, used, 2, 2, d_out));
-  HSV_TRY(launch_screen(op, psi->d_amp, w, d_ops, (int)n_ops, a_lo * s->Nb, a_hi * s->Nb, d_out + 2));
+  HSV_TRY(launch_screen(op, psi->d_amp, w, pool, a_lo, a_hi, d_out + 2));
   dfree(w);
   dfree(epart);
   return HSV_OK;
@@ -178,18 +236,18 @@ int hsv_energy_screen_partial_async(hsv_op op, hsv_state psi, const uint64_t* oc
                                     int64_t a_hi, double* d_out) {
   HSV_TRY(check_es_args(op, psi, a_lo, a_hi));
   HSV_REQUIRE(d_out && (n_ops == 0 || (occ && virt)), HSV_ERR_INVALID, "null argument");
-  int4* d_ops = nullptr;
-  HSV_TRY(upload_ops(op->sec, occ, virt, n_ops, &d_ops));
-  HSV_TRY(energy_screen_dev(op, psi, d_ops, n_ops, a_lo, a_hi, d_out));
-  dfree(d_ops);
-  return HSV_OK;
+  hsv_pool pool = nullptr;
+  HSV_TRY(hsv_pool_create(op->sec, occ, virt, n_ops, &pool));
+  const int rc = energy_screen_dev(op, psi, pool, a_lo, a_hi, d_out);
+  hsv_pool_destroy(pool);
+  return rc;
 }
 
 int hsv_energy_screen_pool_async(hsv_op op, hsv_state psi, hsv_pool pool, int64_t a_lo,
                                  int64_t a_hi, double* d_out) {
   HSV_TRY(check_es_args(op, psi, a_lo, a_hi));
   HSV_REQUIRE(pool && d_out && pool->sec == op->sec, HSV_ERR_INVALID, "bad pool argument");
-  return energy_screen_dev(op, psi, pool->d, pool->n, a_lo, a_hi, d_out);
+  return energy_screen_dev(op, psi, pool, a_lo, a_hi, d_out);
 }
 
 int hsv_energy_screen_pool(hsv_op op, hsv_state psi, hsv_pool pool, double* energy, double* grads) {
