@@ -100,6 +100,41 @@ def peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch from the committed ncu --set full capture, or None."""
+    try:
+        t = json.loads((ROOT / "profiles" / "traffic.json").read_text())
+        return t[kernel]["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
+def step_roofline(sysm, ops, nnz, dim, ms, hbm):
+    """Whole-step roofline: algorithmic bytes of <psi|H|psi> (16 P + 24 N) plus the
+    pool gradients (16 * sum_k matches_k + 24 N), SURVEY.md 8(d).  matches_k =
+    rows in source or target pattern of operator k = 2 * C_alpha * C_beta."""
+    from math import comb
+    b = sysm.basis
+    norb = sysm.n_qubits // 2
+
+    def cnt(n, occ, virt):
+        po, pv = len(occ), len(virt)
+        free, ones = norb - po - pv, n - po
+        return comb(free, ones) if 0 <= ones <= free else 0
+
+    matches = 0
+    for op in ops:
+        oa = [q for q in op.occ if q in set(range(0, sysm.n_qubits, 2))]
+        ob = [q for q in op.occ if q not in oa]
+        va = [q for q in op.virt if q in set(range(0, sysm.n_qubits, 2))]
+        vb = [q for q in op.virt if q not in va]
+        matches += 2 * cnt(b.n_alpha, oa, va) * cnt(b.n_beta, ob, vb)
+    by = 16.0 * nnz + 24.0 * dim + 16.0 * matches + 24.0 * dim
+    ach = by / (ms * 1e-3) / 1e9
+    return {"bytes": by, "matches": matches, "achieved": ach, "peak": hbm, "frac": ach / hbm,
+            "unit": "GB/s"}
+
+
 def cpu_reference(sysm, psi, steps=1, warmup=0):
     """Reference CPU algorithm (oracle port) on a bounded sample; seconds/step."""
     from oracle import cpu_baseline
@@ -149,6 +184,7 @@ def run_hsv(args):
 
     import paper_2604_01176_b200 as hsv
     from paper_2604_01176_b200 import _native as N
+    from paper_2604_01176_b200.distributed import alpha_row_range, combine_partials
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -183,8 +219,7 @@ def run_hsv(args):
 
     upload()
     n_alpha_strings = basis._sector.n_alpha_strings
-    a_lo = n_alpha_strings * rank // world
-    a_hi = n_alpha_strings * (rank + 1) // world
+    a_lo, a_hi = alpha_row_range(n_alpha_strings, rank, world)
     d_out = torch.zeros(2 + M, dtype=torch.float64, device="cuda")
     gathered = torch.zeros(world, 2 + M, dtype=torch.float64, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -194,7 +229,7 @@ def run_hsv(args):
                N.C.c_void_p(d_out.data_ptr()))
         if world > 1:
             dist.all_gather_into_tensor(gathered, d_out)
-            return gathered.sum(0)    # rank order, fixed
+            return combine_partials(gathered)    # rank order, fixed
         return d_out
 
     def barrier():
@@ -248,7 +283,7 @@ def run_hsv(args):
         upload()                               # H2D: positions + amplitudes (pinned)
         if world > 1:
             step_device()
-            res = gathered.sum(0).cpu().numpy()  # D2H
+            res = combine_partials(gathered).cpu().numpy()  # D2H
             e_host.value, g_host[:] = res[0], res[2:]
         else:
             N.call("hsv_energy_screen_pool", op.handle, st.handle, dpool.handle,
@@ -289,9 +324,13 @@ def run_hsv(args):
             "roofline": {"bound": "hbm", "kernel": "k_apply (H|psi>, K1)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "peak_kind": pk_kind,
-                         "traffic": None, "apply_ms": apply_ms,
+                         "traffic": ncu_traffic("k_apply"),
+                         "traffic_note": "ncu DRAM bytes/launch: psi (13.7 MB) is L2-resident "
+                                         "at H12, so traffic << algorithmic bytes",
+                         "apply_ms": apply_ms,
                          "bytes_per_launch": bytes_apply},
             "kernels_ms": {"apply": apply_ms, "screen": screen_ms},
+            "step_roofline": step_roofline(sysm, pool_ops, nnz_struct, dim, ms_per_step, hbm),
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_t,
                     "h2d_bytes_per_step": dim * 16, "d2h_bytes_per_step": (2 + M) * 8},
             "gpu_launches": launches,

@@ -115,6 +115,59 @@ def test_qeb_and_generator_bit_exact(hsv, name):
         assert np.array_equal(gen.values, ref[f"gen{j}_val"])
 
 
+def test_h12_bench_workload_parity(hsv):
+    """The bench workload (H12 S1 energy + 1818 pool gradients), the H12 HF
+    screen, a k=20 ADAPT-like state (bit-exact) and its adjoint energy/gradient,
+    against the oracle goldens (tests/golden/make_golden_h12.py)."""
+    ref = load_golden("ref_h12")
+    sysm = hsv.MolecularSystem.bundled("h12")
+    eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
+    pool = hsv.build_qeb_pool(sysm.n_qubits, sysm.integrals.nelec)
+    st = s1_state(hsv, sysm)
+    e, g = eng.energy_and_screen(st, pool)
+    assert abs(e - float(ref["e_s1"])) <= TOL
+    assert rel_err(g, ref["g_s1"]) <= TOL
+    w = eng.matrix.apply_state(st).to_sparse()
+    assert w.nnz == int(ref["hs1_nnz"])
+    assert rel_err(w.values[ref["hs1_rows"]], ref["hs1_rows_val"]) <= TOL
+    hf = eng.initial_state()
+    eh, gh = eng.energy_and_screen(hf, pool)
+    assert abs(eh - float(ref["e_hf"])) <= TOL * abs(float(ref["e_hf"]))
+    assert rel_err(gh, ref["g_hf"]) <= TOL
+    ops = [pool.ops[i] for i in ref["s2_ops"]]
+    s2 = eng.rebuild(ops, ref["s2_thetas"]).vec
+    assert np.array_equal(s2.indices, ref["s2_idx"]) and np.array_equal(s2.values, ref["s2_val"])
+    e2, g2 = eng.energy_and_gradient(ops, ref["s2_thetas"])
+    assert abs(e2 - float(ref["eg_s2_e"])) <= TOL * abs(float(ref["eg_s2_e"]))
+    assert rel_err(g2, ref["eg_s2_g"]) <= TOL
+
+
+def test_sharded_partials_sum_to_full(hsv):
+    """Owner-computes shards (alpha-row ranges) reproduce the full result."""
+    from paper_2604_01176_b200 import _native as N
+    import torch
+    sysm, eng, pool, ref = setup(hsv, "h10")
+    st = s1_state(hsv, sysm)
+    dp = eng._device_pool(pool)
+    na = sysm.basis._sector.n_alpha_strings
+    full = torch.zeros(2 + dp.n, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()          # libhsv runs on its own (non-blocking) stream
+    N.call("hsv_energy_screen_pool_async", eng.matrix.handle, st.device.handle, dp.handle, 0, na,
+           N.C.c_void_p(full.data_ptr()))
+    for world in (2, 3, 8):
+        parts = []
+        for r in range(world):
+            t = torch.zeros_like(full)
+            torch.cuda.synchronize()
+            N.call("hsv_energy_screen_pool_async", eng.matrix.handle, st.device.handle, dp.handle,
+                   na * r // world, na * (r + 1) // world, N.C.c_void_p(t.data_ptr()))
+            parts.append(t)
+        N.call("hsv_synchronize")
+        tot = torch.stack(parts).sum(0).cpu().numpy()
+        ref_full = full.cpu().numpy()
+        assert rel_err(tot, ref_full) <= 1e-12
+
+
 def test_determinism(hsv):
     sysm, eng, pool, ref = setup(hsv, "h8")
     st = s1_state(hsv, sysm)
