@@ -336,7 +336,7 @@ def run_hsv(args):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
-        if not args.no_cpu:
+        if not args.no_cpu and world == 1:     # cpu_baseline: rank 0 at N=1 only
             r = cpu_reference(sysm, psi_vals)
             line["cpu_baseline"] = {
                 "value": T * dim / r["t_step_s"], "unit": UNIT, "cores": r["threads"],

@@ -141,8 +141,8 @@ __device__ __forceinline__ Rec<W> ldrec(const Rec<W>* p) {
 // IEEE rounding is symmetric under negation) and h a per-group perfect
 // multiply-shift hash of the in-sector patterns of b on x.  Other groups
 // (singles carrying number-operator Z's) run the sequential term loop.
-template <typename W, int SH, int R>
-__global__ void __launch_bounds__(256) k_apply(const ApplyArgs a) {
+template <typename W, int SH, int R, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t tw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -188,15 +188,15 @@ __global__ void __launch_bounds__(256) k_apply(const ApplyArgs a) {
             v |= ((live >> k) & 1u) && __popc(sb[k] & xb) == hb ? (1u << k) : 0u;
           if (__any_sync(0xffffffffu, v != 0u)) {
             const int shift = (int)((cur.meta >> 8) & 0xffu);
-            const double* __restrict__ tab = a.tabs + cur.tab;
 #pragma unroll
             for (int k = 0; k < R; ++k) {
-              const unsigned h = (unsigned)((W)((s[k] & cur.xm) * cur.mul) >> shift);
-              const double A = __ldg(tab + h);
+              const uint32_t h = cur.tab + (uint32_t)((W)((s[k] & cur.xm) * cur.mul) >> shift);
+              const double A = __ldg(a.tabs + h);
               const int sgn = popc(s[k] & cur.z0) << 31;
               const double amp = __hiloint2double(__double2hiint(A) ^ sgn, __double2loint(A));
               if ((v >> k) & 1u) {
-                const double2 p = prow[__ldg(a.Rb + (sb[k] ^ xb))];
+                const uint32_t rk = __ldg(a.Rb + (uint32_t)(sb[k] ^ xb));
+                const double2 p = prow[rk];
                 acc[k].x = fma(amp, p.x, acc[k].x);
                 acc[k].y = fma(amp, p.y, acc[k].y);
               }
@@ -226,7 +226,10 @@ __global__ void __launch_bounds__(256) k_apply(const ApplyArgs a) {
             const double c = __ldg(&a.terms[t].c);
             const W z = (W)__ldg(&a.terms[t].z);
 #pragma unroll
-            for (int k = 0; k < R; ++k) amp[k] += (popc(s[k] & z) & 1) ? -c : c;
+            for (int k = 0; k < R; ++k) {
+              const int sgn = popc(s[k] & z) << 31;   // exact +-c: flip the sign bit
+              amp[k] += __hiloint2double(__double2hiint(c) ^ sgn, __double2loint(c));
+            }
           }
 #pragma unroll
           for (int k = 0; k < R; ++k) {
@@ -265,13 +268,13 @@ __global__ void __launch_bounds__(256) k_apply(const ApplyArgs a) {
   }
 }
 
-template <typename W, int SH, int R>
+template <typename W, int SH, int R, int MINB>
 static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
   ApplyArgs a = a0;
   a.upr = (int)((a.Nb + 32 * R - 1) / (32 * R));
   a.units = (a.a_hi - a.a_lo) * a.upr;
   int occ = 0;
-  HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<W, SH, R>, 256, 0));
+  HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<W, SH, R, MINB>, 256, 0));
   occ = std::max(occ, 1);
   int64_t grid = (int64_t)ctx().num_sms * occ;
   const int64_t need = (a.units + 7) / 8;
@@ -279,7 +282,7 @@ static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
   if (n_warps_out) *n_warps_out = grid * 8;
   if (a.units == 0) return HSV_OK;
   ProfScope prof("apply");
-  k_apply<W, SH, R><<<(unsigned)grid, 256, 0, stream()>>>(a);
+  k_apply<W, SH, R, MINB><<<(unsigned)grid, 256, 0, stream()>>>(a);
   count_launch();
   HSV_CHECK_LAUNCH();
   return HSV_OK;
@@ -302,15 +305,25 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   a.tabs = op->d_tabs; a.recs = op->d_recs; a.n_buckets_h = (int)op->n_buckets_h;
   a.psi = psi; a.out = out; a.epart = epart;
   a.Nb = s->Nb; a.a_lo = a_lo; a.a_hi = a_hi; a.prune = prune; a.energy_only = energy_only;
-  const int R = tuning().apply_r;
-  if (s->wide) {
-    if (R == 1) return launch_apply_t<uint64_t, 32, 1>(a, n_warps);
-    if (R == 4) return launch_apply_t<uint64_t, 32, 4>(a, n_warps);
-    return launch_apply_t<uint64_t, 32, 2>(a, n_warps);
+  int R = tuning().apply_r;
+  const int M = tuning().apply_minb;
+  if (R == 0) {
+    // auto: 4 rows per lane amortize group overhead better, but only if every
+    // warp still gets several units (else the tail of the static schedule wins)
+    const int64_t units4 = (a_hi - a_lo) * ((s->Nb + 127) / 128);
+    const int64_t warps4 = (int64_t)ctx().num_sms * 3 * 8;
+    R = units4 >= 6 * warps4 ? 4 : 2;
   }
-  if (R == 1) return launch_apply_t<uint32_t, 16, 1>(a, n_warps);
-  if (R == 4) return launch_apply_t<uint32_t, 16, 4>(a, n_warps);
-  return launch_apply_t<uint32_t, 16, 2>(a, n_warps);
+#define HSV_APPLY_CASES(W, SH)                                              \
+  if (R == 1) return launch_apply_t<W, SH, 1, 6>(a, n_warps);              \
+  if (R == 4 && M == 2) return launch_apply_t<W, SH, 4, 2>(a, n_warps);    \
+  if (R == 4) return launch_apply_t<W, SH, 4, 3>(a, n_warps);              \
+  if (M == 3) return launch_apply_t<W, SH, 2, 3>(a, n_warps);              \
+  if (M == 5) return launch_apply_t<W, SH, 2, 5>(a, n_warps);              \
+  return launch_apply_t<W, SH, 2, 4>(a, n_warps);
+  if (s->wide) { HSV_APPLY_CASES(uint64_t, 32) }
+  HSV_APPLY_CASES(uint32_t, 16)
+#undef HSV_APPLY_CASES
 }
 
 // Host: does group [t0, t1) admit amp(b) = (-1)^popc(b&z0) * A[h(b & x)]?  If

@@ -28,10 +28,14 @@ def prof(name):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--systems", nargs="+", default=["h12"])
-    ap.add_argument("--apply-r", nargs="+", type=int, default=[2])
+    ap.add_argument("--apply-r", nargs="+", type=int, default=[0])
+    ap.add_argument("--minb", nargs="+", type=int, default=[0])
     ap.add_argument("--screen-rows", nargs="+", type=int, default=[1024])
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--lib", default=None, help="alternative libhsv build (A/B runs)")
     args = ap.parse_args()
+    if args.lib:
+        N.load(args.lib)
     N.init(0)
     for name in args.systems:
         sysm = hsv.MolecularSystem.bundled(name)
@@ -44,9 +48,11 @@ def main():
         st = hsv.SvState(basis, hsv.SparseVector(dim, np.arange(dim, dtype=np.int64), v))
         nnz = op.nnz
         info = op.info()
-        for r in args.apply_r:
-            for sr in args.screen_rows:
+        for r, sr, mb in [(r, sr, mb) for r in args.apply_r for sr in args.screen_rows
+                          for mb in args.minb]:
+            if True:
                 N.call("hsv_set_tuning", b"apply_r", r)
+                N.call("hsv_set_tuning", b"apply_minb", mb)
                 N.call("hsv_set_tuning", b"screen_rows", sr)
                 e, g = op.energy_screen_pool(st, pool)          # warm
                 N.call("hsv_prof_reset")
@@ -59,7 +65,7 @@ def main():
                 ts, _ = prof("screen")
                 bytes_apply = 16.0 * nnz + 24.0 * dim
                 print(json.dumps({
-                    "system": name, "dim": dim, "apply_r": r, "screen_rows": sr,
+                    "system": name, "dim": dim, "apply_r": r, "minb": mb, "screen_rows": sr,
                     "apply_ms": ta, "screen_ms": ts, "apply_GBs_alg": bytes_apply / ta / 1e6,
                     "energy": e, "gmax": float(np.max(np.abs(g))), "nnz": nnz, **info}),
                     flush=True)
