@@ -174,8 +174,9 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
       for (int bk = 0; bk < a.n_buckets_h; ++bk) {
         const int4 B = __ldg(a.buckets + bk);
         if (__popc(sa & (uint32_t)B.x) != B.y) continue;
-        const double2* __restrict__ prow =
-            a.psi + (int64_t)__ldg(a.Ra + (sa ^ (uint32_t)B.x)) * a.Nb;
+        const uint32_t ra2 = __ldg(a.Ra + (sa ^ (uint32_t)B.x));
+        if (a.arow && !__ldg(a.arow + ra2)) continue;   // partner alpha row all zero
+        const double2* __restrict__ prow = a.psi + (int64_t)ra2 * a.Nb;
         const Rec<W>* __restrict__ rp = reinterpret_cast<const Rec<W>*>(a.recs);
         Rec<W> cur = ldrec(rp + B.z);
         for (int g = B.z; g < B.w; ++g) {
@@ -209,8 +210,9 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
       for (int bk = a.n_buckets_h; bk < a.n_buckets; ++bk) {
         const int4 B = __ldg(a.buckets + bk);
         if (__popc(sa & (uint32_t)B.x) != B.y) continue;
-        const double2* __restrict__ prow =
-            a.psi + (int64_t)__ldg(a.Ra + (sa ^ (uint32_t)B.x)) * a.Nb;
+        const uint32_t ra2 = __ldg(a.Ra + (sa ^ (uint32_t)B.x));
+        if (a.arow && !__ldg(a.arow + ra2)) continue;
+        const double2* __restrict__ prow = a.psi + (int64_t)ra2 * a.Nb;
         for (int g = B.z; g < B.w; ++g) {
           const int4 G = __ldg(a.groups + g);
           const uint32_t xb = (uint32_t)G.x;
@@ -296,9 +298,11 @@ int apply_warps(const hsv_op_s* op) {
 }
 
 int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* epart,
-                 int64_t a_lo, int64_t a_hi, double prune, int energy_only, int64_t* n_warps) {
+                 int64_t a_lo, int64_t a_hi, double prune, int energy_only, int64_t* n_warps,
+                 const uint32_t* arow) {
   const hsv_sector_s* s = op->sec;
   ApplyArgs a{};
+  a.arow = arow;
   a.Sa = s->d_Sa; a.Sb = s->d_Sb; a.Ra = s->d_Ra; a.Rb = s->d_Rb;
   a.buckets = op->d_buckets; a.n_buckets = (int)op->n_buckets;
   a.groups = op->d_groups; a.terms = op->d_terms; a.diag = op->d_diag;
@@ -764,8 +768,11 @@ int hsv_apply_h(hsv_op op, hsv_state in, hsv_state out, double prune) {
   HSV_REQUIRE(in->sec == op->sec && out->sec == op->sec, HSV_ERR_INVALID,
               "dimension mismatch: operator and vector belong to different sectors");
   HSV_REQUIRE(in != out, HSV_ERR_INVALID, "hsv_apply_h: output must not alias input");
-  HSV_TRY(launch_apply(op, in->d_amp, out->d_amp, nullptr, 0, op->sec->Na, prune, 0, nullptr));
+  HSV_TRY(state_arow_async(in));
+  HSV_TRY(launch_apply(op, in->d_amp, out->d_amp, nullptr, 0, op->sec->Na, prune, 0, nullptr,
+                       in->d_arow));
   out->norm2_valid = false;
+  out->arow_valid = false;
   return stream_sync();
 }
 
@@ -775,8 +782,11 @@ int hsv_apply_h_rows_async(hsv_op op, hsv_state in, hsv_state out, int64_t a_lo,
   HSV_REQUIRE(in->sec == op->sec && out->sec == op->sec, HSV_ERR_INVALID, "dimension mismatch");
   HSV_REQUIRE(0 <= a_lo && a_lo <= a_hi && a_hi <= op->sec->Na, HSV_ERR_INVALID,
               "bad alpha-row range");
-  HSV_TRY(launch_apply(op, in->d_amp, out->d_amp, nullptr, a_lo, a_hi, prune, 0, nullptr));
+  HSV_TRY(state_arow_async(in));
+  HSV_TRY(launch_apply(op, in->d_amp, out->d_amp, nullptr, a_lo, a_hi, prune, 0, nullptr,
+                       in->d_arow));
   out->norm2_valid = false;
+  out->arow_valid = false;
   return HSV_OK;
 }
 
@@ -789,7 +799,8 @@ int hsv_expect_h(hsv_op op, hsv_state psi, double* e_re, double* e_im) {
   HSV_TRY(dalloc(&d_e, 2));
   HSV_TRY_CUDA(cudaMemsetAsync(part, 0, 2 * sizeof(double) * nw, stream()));
   int64_t used = 0;
-  HSV_TRY(launch_apply(op, psi->d_amp, nullptr, part, 0, op->sec->Na, 0.0, 1, &used));
+  HSV_TRY(state_arow_async(psi));
+  HSV_TRY(launch_apply(op, psi->d_amp, nullptr, part, 0, op->sec->Na, 0.0, 1, &used, psi->d_arow));
   HSV_TRY(reduce_sum_f64(part, used, 2, 2, d_e));
   double h[2];
   HSV_TRY_CUDA(cudaMemcpyAsync(h, d_e, 16, cudaMemcpyDeviceToHost, stream()));

@@ -181,6 +181,11 @@ struct hsv_state_s {
   double2* d_amp = nullptr;    // dim complex128, alpha-major internal order
   double* d_norm2 = nullptr;   // cached <psi|psi> (device scalar)
   bool norm2_valid = false;
+  // Conservative alpha-row occupancy: d_arow[ra] != 0 if row ra may hold a
+  // nonzero.  Kernels skip work whose inputs lie in empty alpha rows, which
+  // changes no result (skipped terms are exact zeros).
+  uint32_t* d_arow = nullptr;
+  bool arow_valid = false;
 };
 
 namespace hsv {
@@ -221,4 +226,7 @@ int reduce_sum_f64(const double* d_in, int64_t n, int64_t stride, int64_t count,
                    double* d_out);   // d_out[j] = sum_i d_in[i*stride + j], j<count
 int state_norm2_async(hsv_state st);
 int state_fill_zero_async(hsv_state st);
+// alpha-row occupancy flags of a raw amplitude array / of a state (lazy)
+int arow_flags_async(const double2* amp, int64_t Na, int64_t Nb, uint32_t* flags);
+int state_arow_async(hsv_state st);
 }  // namespace hsv

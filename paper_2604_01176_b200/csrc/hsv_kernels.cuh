@@ -28,6 +28,7 @@ struct ApplyArgs {
   const GroupHash* ghash;
   const double* tabs;
   const double2* psi;
+  const uint32_t* arow;  // alpha-row occupancy of psi (skip empty partner rows) or nullptr
   double2* out;      // nullptr: energy only
   double* epart;     // [warps][2] energy partials or nullptr
   int64_t Nb;
@@ -41,7 +42,8 @@ struct ApplyArgs {
 int grid_for(int64_t n, int block);
 int apply_warps(const hsv_op_s* op);
 int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* epart,
-                 int64_t a_lo, int64_t a_hi, double prune, int energy_only, int64_t* n_warps);
+                 int64_t a_lo, int64_t a_hi, double prune, int energy_only, int64_t* n_warps,
+                 const uint32_t* arow = nullptr);
 
 // Compressed QEB masks of one excitation operator.
 struct OpMasks {
@@ -59,7 +61,8 @@ struct PairLists {
 int build_pair_lists_async(const hsv_sector_s* s, const OpMasks& m, PairLists& pl);
 
 int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
-                  const hsv_pool_s* pool, int64_t a_lo, int64_t a_hi, double* d_grads);
+                  const hsv_pool_s* pool, int64_t a_lo, int64_t a_hi, double* d_grads,
+                  const uint32_t* psi_arow = nullptr, const uint32_t* w_arow = nullptr);
 int pool_prepare(hsv_pool_s* p);
 
 }  // namespace hsv

@@ -97,6 +97,8 @@ struct PairArgs {
   int* err;              // set to 1 on norm drift
   double* err_val;
   int uncompute;
+  uint32_t* fpsi;        // alpha-row occupancy of psi (maintained), or nullptr
+  uint32_t* flam;        // alpha-row occupancy of lam (kAdjoint), or nullptr
 };
 
 __device__ __forceinline__ void givens(double2 vb, double2 vp, double c, double s, double2& nb,
@@ -162,7 +164,20 @@ __global__ void __launch_bounds__(256) k_pairs(const PairArgs a) {
   double v[MODE == kAdjoint ? 3 : 2];
 #pragma unroll
   for (int q = 0; q < (MODE == kAdjoint ? 3 : 2); ++q) v[q] = 0.0;
-  if (j < a.cb) {
+  // Skip alpha-row pairs that are entirely zero (results unchanged: all terms
+  // would be exact zeros); a nonzero row makes both rows of the pair nonzero.
+  bool active = true;
+  if (MODE != kGenerator) {
+    const bool ap = !a.fpsi || a.fpsi[A.x] || a.fpsi[A.y];
+    const bool al = MODE == kAdjoint && (!a.flam || a.flam[A.x] || a.flam[A.y]);
+    active = ap || al;
+    __syncthreads();   // every thread has read the flags before thread 0 updates them
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+      if (a.fpsi && ap && (MODE == kRotate || a.uncompute)) { a.fpsi[A.x] = 1u; a.fpsi[A.y] = 1u; }
+      if (MODE == kAdjoint && a.flam && al) { a.flam[A.x] = 1u; a.flam[A.y] = 1u; }
+    }
+  }
+  if (j < a.cb && active) {
     const int2 B = a.lb[j];
     const int64_t ib = (int64_t)A.x * a.Nb + B.x;   // source row
     const int64_t ip = (int64_t)A.y * a.Nb + B.y;   // partner (target pattern)
@@ -283,6 +298,9 @@ int hsv_apply_qeb(hsv_state in, hsv_state out, uint64_t occ, uint64_t virt, doub
     HSV_TRY_CUDA(cudaMemcpyAsync(out->d_norm2, in->d_norm2, sizeof(double),
                                  cudaMemcpyDeviceToDevice, stream()));
     out->norm2_valid = in->norm2_valid;
+    HSV_TRY_CUDA(cudaMemcpyAsync(out->d_arow, in->d_arow, in->sec->Na * sizeof(uint32_t),
+                                 cudaMemcpyDeviceToDevice, stream()));
+    out->arow_valid = in->arow_valid;
   }
   if (c == 1.0 && s == 0.0) return stream_sync();   // theta == 0 returns the input (svengine.py:212)
   if (!out->norm2_valid) HSV_TRY(state_norm2_async(out));
@@ -295,6 +313,8 @@ int hsv_apply_qeb(hsv_state in, hsv_state out, uint64_t occ, uint64_t virt, doub
   a.Nb = sec->Nb; a.psi = out->d_amp; a.c = c; a.s = s;
   a.part = sc.part; a.counter = sc.counter; a.norm2 = out->d_norm2;
   a.err = sc.err; a.err_val = sc.err_val;
+  HSV_TRY(state_arow_async(out));
+  a.fpsi = out->d_arow;                      // maintained by the kernel
   HSV_TRY(launch_pairs<kRotate>(pl, a));
   int rc = sc.check();
   dfree(pl.la); dfree(pl.lb);
@@ -316,6 +336,7 @@ int hsv_apply_generator(hsv_state in, hsv_state out, uint64_t occ, uint64_t virt
   HSV_TRY(launch_pairs<kGenerator>(pl, a));
   dfree(pl.la); dfree(pl.lb);
   out->norm2_valid = false;
+  out->arow_valid = false;
   return stream_sync();
 }
 
@@ -354,6 +375,15 @@ int hsv_energy_gradient(hsv_op op, uint64_t hf_key, const uint64_t* occ, const u
   const int64_t hidx = (int64_t)sec->Ra[sa] * sec->Nb + sec->Rb[sb];
   HSV_TRY_CUDA(cudaMemcpyAsync(psi + hidx, &one, sizeof(double2), cudaMemcpyHostToDevice, stream()));
   HSV_TRY_CUDA(cudaMemcpyAsync(d_n2, &n2one, sizeof(double), cudaMemcpyHostToDevice, stream()));
+  // alpha-row occupancy of psi (HF row only) and of lam (after H psi)
+  uint32_t *d_fpsi = nullptr, *d_flam = nullptr;
+  HSV_TRY(dalloc(&d_fpsi, std::max<int64_t>(sec->Na, 1)));
+  HSV_TRY(dalloc(&d_flam, std::max<int64_t>(sec->Na, 1)));
+  HSV_TRY_CUDA(cudaMemsetAsync(d_fpsi, 0, sec->Na * sizeof(uint32_t), stream()));
+  static thread_local uint32_t one_flag;
+  one_flag = 1u;
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_fpsi + sec->Ra[sa], &one_flag, sizeof(uint32_t),
+                               cudaMemcpyHostToDevice, stream()));
 
   PairScratch sc;
   HSV_TRY(sc.init(sec, 3));
@@ -365,12 +395,14 @@ int hsv_energy_gradient(hsv_op op, uint64_t hf_key, const uint64_t* occ, const u
     PairArgs a{};
     a.Nb = sec->Nb; a.psi = psi; a.c = cs[i]; a.s = sn[i];
     a.part = sc.part; a.counter = sc.counter; a.norm2 = d_n2; a.err = sc.err; a.err_val = sc.err_val;
+    a.fpsi = d_fpsi;
     HSV_TRY(launch_pairs<kRotate>(lists[i], a));
   }
   // w = H psi (into lam), E = <psi|w>
   int64_t used = 0;
-  HSV_TRY(launch_apply(op, psi, lam, epart, 0, sec->Na, 0.0, 0, &used));
+  HSV_TRY(launch_apply(op, psi, lam, epart, 0, sec->Na, 0.0, 0, &used, d_fpsi));
   HSV_TRY(reduce_sum_f64(epart, used, 2, 2, d_e));
+  HSV_TRY(arow_flags_async(lam, sec->Na, sec->Nb, d_flam));
   if (k > 0) {
     // <lam|lam> for the adjoint drift checks
     hsv_state_s tmp;
@@ -387,6 +419,7 @@ int hsv_energy_gradient(hsv_op op, uint64_t hf_key, const uint64_t* occ, const u
     a.Nb = sec->Nb; a.psi = psi; a.lam = lam; a.c = cs[i]; a.s = -sn[i];
     a.part = sc.part; a.counter = sc.counter; a.norm2 = d_ln2; a.result = d_grad + i;
     a.err = sc.err; a.err_val = sc.err_val; a.uncompute = i > 0;
+    a.fpsi = d_fpsi; a.flam = d_flam;
     if (lists[i].ca == 0 || lists[i].cb == 0) {
       HSV_TRY_CUDA(cudaMemsetAsync(d_grad + i, 0, sizeof(double), stream()));
       continue;
@@ -401,6 +434,7 @@ int hsv_energy_gradient(hsv_op op, uint64_t hf_key, const uint64_t* occ, const u
   for (auto& pl : lists) { dfree(pl.la); dfree(pl.lb); }
   sc.release();
   dfree(psi); dfree(lam); dfree(d_n2); dfree(d_ln2); dfree(d_grad); dfree(d_e); dfree(epart);
+  dfree(d_fpsi); dfree(d_flam);
   HSV_TRY(stream_sync());
   *energy = he[0];
   return rc;

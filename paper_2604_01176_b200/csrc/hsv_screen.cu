@@ -40,6 +40,8 @@ struct ScreenArgs {
   int n_ops;
   const double2* psi;
   const double2* w;
+  const uint32_t* psi_arow;  // alpha-row occupancy of psi (or nullptr)
+  const uint32_t* w_arow;    // alpha-row occupancy of w on owned rows (or nullptr)
   int64_t Nb;
   int64_t a_lo;
   int slices;
@@ -57,6 +59,7 @@ __global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
   const uint32_t sa = __ldg(a.Sa + ra);
   const double2* __restrict__ wrow = a.w + ra * a.Nb;
   const int stride = a.slices * kScreenWarps;
+  const bool w_zero = a.w_arow && !__ldg(a.w_arow + ra);   // own rows all zero
   for (int q = blockIdx.x * kScreenWarps + warp; q < a.n_ops; q += stride) {
     const int op = __ldg(a.order + q);
     const int4 O = __ldg(a.ops + op);
@@ -65,8 +68,9 @@ __global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
     const uint32_t ma = sa & fa;
     const bool as = ma == oa, at = ma == va;   // both for an empty alpha half
     double g = 0.0;
-    if (as || at) {
-      const double2* __restrict__ prow = a.psi + (int64_t)__ldg(a.Ra + (sa ^ fa)) * a.Nb;
+    const uint32_t ra2 = (as || at) ? __ldg(a.Ra + (sa ^ fa)) : 0u;
+    if ((as || at) && !w_zero && !(a.psi_arow && !__ldg(a.psi_arow + ra2))) {
+      const double2* __restrict__ prow = a.psi + (int64_t)ra2 * a.Nb;
       const int2 L = __ldg(a.opl + op);
       if (L.y < 0) {
         // empty beta half: every beta string is both source and target (alpha decides)
@@ -166,7 +170,8 @@ int pool_prepare(hsv_pool_s* p) {
 }
 
 int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
-                  const hsv_pool_s* pool, int64_t a_lo, int64_t a_hi, double* d_grads) {
+                  const hsv_pool_s* pool, int64_t a_lo, int64_t a_hi, double* d_grads,
+                  const uint32_t* psi_arow, const uint32_t* w_arow) {
   const hsv_sector_s* s = op->sec;
   const int n_ops = (int)pool->n;
   if (n_ops <= 0) return HSV_OK;
@@ -188,6 +193,8 @@ int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
   a.ops = pool->d; a.order = pool->d_order; a.opl = pool->d_opl; a.blist = pool->d_blist;
   a.n_ops = n_ops; a.psi = psi; a.w = w; a.Nb = s->Nb; a.a_lo = a_lo; a.slices = slices;
   a.part = part;
+  a.psi_arow = psi_arow;
+  a.w_arow = w_arow;
   {
     ProfScope prof("screen");
     k_screen<<<dim3((unsigned)slices, (unsigned)rows), kScreenBlock, 0, stream()>>>(a);
@@ -215,9 +222,15 @@ static int energy_screen_dev(hsv_op op, hsv_state psi, const hsv_pool_s* pool, i
   HSV_TRY(dalloc(&epart, 2 * (int64_t)nw));
   HSV_TRY_CUDA(cudaMemsetAsync(epart, 0, 2 * sizeof(double) * nw, stream()));
   int64_t used = 0;
-  HSV_TRY(launch_apply(op, psi->d_amp, w, epart, a_lo, a_hi, 0.0, 0, &used));
+  HSV_TRY(state_arow_async(psi));
+  HSV_TRY(launch_apply(op, psi->d_amp, w, epart, a_lo, a_hi, 0.0, 0, &used, psi->d_arow));
   HSV_TRY(reduce_sum_f64(epart, used, 2, 2, d_out));
-  HSV_TRY(launch_screen(op, psi->d_amp, w, pool, a_lo, a_hi, d_out + 2));
+  // occupancy of the owned rows of w (other rows of w are never read)
+  uint32_t* wrow = nullptr;
+  HSV_TRY(dalloc(&wrow, std::max<int64_t>(s->Na, 1)));
+  HSV_TRY(arow_flags_async(w + a_lo * s->Nb, a_hi - a_lo, s->Nb, wrow + a_lo));
+  HSV_TRY(launch_screen(op, psi->d_amp, w, pool, a_lo, a_hi, d_out + 2, psi->d_arow, wrow));
+  dfree(wrow);
   dfree(w);
   dfree(epart);
   return HSV_OK;

@@ -28,7 +28,40 @@ int grid_for(int64_t n, int block) {
 int state_fill_zero_async(hsv_state st) {
   HSV_TRY_CUDA(cudaMemsetAsync(st->d_amp, 0, st->sec->dim * sizeof(double2), stream()));
   HSV_TRY_CUDA(cudaMemsetAsync(st->d_norm2, 0, sizeof(double), stream()));
+  HSV_TRY_CUDA(cudaMemsetAsync(st->d_arow, 0, st->sec->Na * sizeof(uint32_t), stream()));
   st->norm2_valid = true;
+  st->arow_valid = true;
+  return HSV_OK;
+}
+
+// One warp per alpha row: flag = any nonzero amplitude in the row.
+__global__ void k_arow_flags(const double2* __restrict__ amp, int64_t Na, int64_t Nb,
+                             uint32_t* __restrict__ flags) {
+  const int64_t ra = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (ra >= Na) return;
+  const double2* row = amp + ra * Nb;
+  bool nz = false;
+  for (int64_t j = lane; j < Nb && !nz; j += 32) {
+    const double2 v = row[j];
+    nz = v.x != 0.0 || v.y != 0.0;
+  }
+  nz = __any_sync(0xffffffffu, nz);
+  if (lane == 0) flags[ra] = nz ? 1u : 0u;
+}
+
+int arow_flags_async(const double2* amp, int64_t Na, int64_t Nb, uint32_t* flags) {
+  if (Na == 0) return HSV_OK;
+  k_arow_flags<<<(unsigned)((Na * 32 + 255) / 256), 256, 0, stream()>>>(amp, Na, Nb, flags);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  return HSV_OK;
+}
+
+int state_arow_async(hsv_state st) {
+  if (st->arow_valid) return HSV_OK;
+  HSV_TRY(arow_flags_async(st->d_amp, st->sec->Na, st->sec->Nb, st->d_arow));
+  st->arow_valid = true;
   return HSV_OK;
 }
 
@@ -192,6 +225,7 @@ int hsv_state_create(hsv_sector s, hsv_state* out) {
   st->sec = s;
   int rc = dalloc(&st->d_amp, s->dim);
   if (!rc) rc = dalloc(&st->d_norm2, 1);
+  if (!rc) rc = dalloc(&st->d_arow, std::max<int64_t>(s->Na, 1));
   if (!rc) rc = state_fill_zero_async(st);
   if (!rc) rc = stream_sync();
   if (rc) { hsv_state_destroy(st); return rc; }
@@ -203,6 +237,7 @@ int hsv_state_destroy(hsv_state st) {
   if (!st) return HSV_OK;
   dfree(st->d_amp);
   dfree(st->d_norm2);
+  dfree(st->d_arow);
   delete st;
   return HSV_OK;
 }
@@ -215,7 +250,10 @@ int hsv_state_copy(hsv_state dst, hsv_state src) {
                                cudaMemcpyDeviceToDevice, stream()));
   HSV_TRY_CUDA(cudaMemcpyAsync(dst->d_norm2, src->d_norm2, sizeof(double),
                                cudaMemcpyDeviceToDevice, stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(dst->d_arow, src->d_arow, src->sec->Na * sizeof(uint32_t),
+                               cudaMemcpyDeviceToDevice, stream()));
   dst->norm2_valid = src->norm2_valid;
+  dst->arow_valid = src->arow_valid;
   return stream_sync();
 }
 
@@ -243,6 +281,7 @@ int hsv_state_set_basis(hsv_state st, uint64_t key, double re, double im) {
                                stream()));
   HSV_TRY_CUDA(cudaMemcpyAsync(st->d_norm2, &n2, sizeof(double), cudaMemcpyHostToDevice,
                                stream()));
+  st->arow_valid = false;
   return stream_sync();
 }
 
@@ -275,6 +314,7 @@ int hsv_state_set_sparse(hsv_state st, const int64_t* pos, const double* re, con
     dfree(d_p);
     dfree(d_bad);
   }
+  st->arow_valid = false;
   HSV_TRY(state_norm2_async(st));
   HSV_TRY(stream_sync());
   HSV_REQUIRE(!h_bad, HSV_ERR_INVALID, "position out of range for dimension %lld",
@@ -310,6 +350,7 @@ int hsv_state_set_keys(hsv_state st, const uint64_t* keys, const double* re, con
     dfree(d_v);
     dfree(d_i);
   }
+  st->arow_valid = false;
   HSV_TRY(state_norm2_async(st));
   return stream_sync();
 }
@@ -420,6 +461,7 @@ int hsv_state_axpy(double ar, double ai, hsv_state x, hsv_state y) {
   count_launch();
   HSV_CHECK_LAUNCH();
   y->norm2_valid = false;
+  y->arow_valid = false;
   return stream_sync();
 }
 
@@ -430,6 +472,7 @@ int hsv_state_scale(hsv_state st, double ar, double ai) {
   count_launch();
   HSV_CHECK_LAUNCH();
   st->norm2_valid = false;
+  st->arow_valid = false;
   return stream_sync();
 }
 
@@ -438,6 +481,7 @@ int hsv_state_device_ptr(hsv_state st, void** ptr, int64_t* n) {
   if (ptr) *ptr = st->d_amp;
   if (n) *n = st->sec->dim;
   st->norm2_valid = false;   // caller may write through the pointer
+  st->arow_valid = false;
   return HSV_OK;
 }
 
