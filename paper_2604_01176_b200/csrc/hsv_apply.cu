@@ -148,7 +148,12 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
   const int64_t tw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t u0 = gw * a.units / tw, u1 = (gw + 1) * a.units / tw;
   double er = 0.0, ei = 0.0;
-  for (int64_t u = u0; u < u1; ++u) {
+  for (int64_t uw = u0; uw < u1; ++uw) {
+    // a work unit = (row unit, bucket split); splits > 1 only when row units are scarce
+    const int64_t u = uw / a.nsplit;
+    const int sp = (int)(uw - u * a.nsplit);
+    const int bk0 = a.nsplit > 1 ? __ldg(a.split_bk + sp) : 0;
+    const int bk1 = a.nsplit > 1 ? __ldg(a.split_bk + sp + 1) : a.n_buckets;
     const int64_t ra = a.a_lo + u / a.upr;
     const int64_t rb0 = (u % a.upr) * (32 * R) + lane;
     const uint32_t sa = __ldg(a.Sa + ra);
@@ -165,13 +170,13 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
       s[k] = (W)sa | ((W)sb[k] << SH);
       const double2 pv = inr ? a.psi[rowbase + rb] : make_double2(0.0, 0.0);
       const bool lv = inr && (!a.energy_only || pv.x != 0.0 || pv.y != 0.0);
-      const double d = (a.diag && lv) ? a.diag[rowbase + rb] : 0.0;
+      const double d = (a.diag && lv && sp == 0) ? a.diag[rowbase + rb] : 0.0;
       acc[k] = make_double2(d * pv.x, d * pv.y);
       live |= lv ? (1u << k) : 0u;
     }
     if (__any_sync(0xffffffffu, live != 0u)) {
       // pass 1: x-local groups, amp = sign * table[hash(pattern)]
-      for (int bk = 0; bk < a.n_buckets_h; ++bk) {
+      for (int bk = bk0; bk < min(bk1, a.n_buckets_h); ++bk) {
         const int4 B = __ldg(a.buckets + bk);
         if (__popc(sa & (uint32_t)B.x) != B.y) continue;
         const uint32_t ra2 = __ldg(a.Ra + (sa ^ (uint32_t)B.x));
@@ -207,7 +212,7 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
         }
       }
       // pass 2: remaining groups, sequential term loop in reference order
-      for (int bk = a.n_buckets_h; bk < a.n_buckets; ++bk) {
+      for (int bk = max(bk0, a.n_buckets_h); bk < bk1; ++bk) {
         const int4 B = __ldg(a.buckets + bk);
         if (__popc(sa & (uint32_t)B.x) != B.y) continue;
         const uint32_t ra2 = __ldg(a.Ra + (sa ^ (uint32_t)B.x));
@@ -249,9 +254,13 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
       const int64_t rb = rb0 + k * 32;
       if (rb >= a.Nb) continue;
       if (a.out) {
-        double2 y = acc[k];
-        if (a.prune > 0.0 && sqrt(y.x * y.x + y.y * y.y) < a.prune) y = make_double2(0.0, 0.0);
-        a.out[rowbase + rb] = y;
+        if (a.nsplit > 1) {   // partial row, combined in split order by k_combine_splits
+          a.ypart[sp * a.part_stride + (rowbase + rb - a.a_lo * a.Nb)] = acc[k];
+        } else {
+          double2 y = acc[k];
+          if (a.prune > 0.0 && sqrt(y.x * y.x + y.y * y.y) < a.prune) y = make_double2(0.0, 0.0);
+          a.out[rowbase + rb] = y;
+        }
       }
       if (a.epart && ((live >> k) & 1u)) {
         const double2 pv = a.psi[rowbase + rb];
@@ -270,23 +279,63 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
   }
 }
 
+// Sum the per-split partial rows in split order (fixed), then the drop rule.
+__global__ void k_combine_splits(const double2* __restrict__ part, int S, int64_t rows,
+                                 double2* __restrict__ out, double prune) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  double2 y = part[i];
+  for (int s = 1; s < S; ++s) {
+    const double2 p = part[s * rows + i];
+    y.x += p.x;
+    y.y += p.y;
+  }
+  if (prune > 0.0 && sqrt(y.x * y.x + y.y * y.y) < prune) y = make_double2(0.0, 0.0);
+  out[i] = y;
+}
+
 template <typename W, int SH, int R, int MINB>
 static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
   ApplyArgs a = a0;
   a.upr = (int)((a.Nb + 32 * R - 1) / (32 * R));
-  a.units = (a.a_hi - a.a_lo) * a.upr;
+  const int64_t units1 = (a.a_hi - a.a_lo) * a.upr;
   int occ = 0;
   HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<W, SH, R, MINB>, 256, 0));
   occ = std::max(occ, 1);
-  int64_t grid = (int64_t)ctx().num_sms * occ;
+  const int64_t max_warps = (int64_t)ctx().num_sms * occ * 8;
+  // Split the bucket range of each row unit when row units alone cannot give
+  // every warp several units (small problems, or a rank's shard at N > 1).
+  int S = tuning().apply_split;
+  if (S <= 0) {
+    S = 1;
+    while (S < 8 && units1 * S < 8 * max_warps) S *= 2;
+  }
+  if (!a0.split_bk) S = 1;
+  a.nsplit = S;
+  a.split_bk = S == 1 ? nullptr : a0.split_bk + (S == 2 ? 0 : S == 4 ? 3 : 8);
+  a.units = units1 * S;
+  int64_t grid = max_warps / 8;
   const int64_t need = (a.units + 7) / 8;
   grid = std::max<int64_t>(1, std::min(grid, need));
   if (n_warps_out) *n_warps_out = grid * 8;
   if (a.units == 0) return HSV_OK;
-  ProfScope prof("apply");
-  k_apply<W, SH, R, MINB><<<(unsigned)grid, 256, 0, stream()>>>(a);
-  count_launch();
+  const int64_t rows = (a.a_hi - a.a_lo) * a.Nb;
+  double2* ypart = nullptr;
+  if (S > 1 && a.out) {
+    HSV_TRY(dalloc(&ypart, S * rows));
+    a.ypart = ypart;
+    a.part_stride = rows;
+  }
+  {
+    ProfScope prof("apply");
+    k_apply<W, SH, R, MINB><<<(unsigned)grid, 256, 0, stream()>>>(a);
+    if (ypart)
+      k_combine_splits<<<(unsigned)((rows + 255) / 256), 256, 0, stream()>>>(
+          ypart, S, rows, a.out + a.a_lo * a.Nb, a.prune);
+  }
+  count_launch(ypart ? 2 : 1);
   HSV_CHECK_LAUNCH();
+  dfree(ypart);
   return HSV_OK;
 }
 
@@ -303,6 +352,7 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   const hsv_sector_s* s = op->sec;
   ApplyArgs a{};
   a.arow = arow;
+  a.split_bk = op->d_splits;
   a.Sa = s->d_Sa; a.Sb = s->d_Sb; a.Ra = s->d_Ra; a.Rb = s->d_Rb;
   a.buckets = op->d_buckets; a.n_buckets = (int)op->n_buckets;
   a.groups = op->d_groups; a.terms = op->d_terms; a.diag = op->d_diag;
@@ -616,6 +666,30 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
     ghash = nh;
     op->n_buckets = (int64_t)nb.size();
   }
+  // bucket split boundaries (S = 2, 4, 8) balancing an estimated per-group cost
+  std::vector<int> splits;
+  {
+    std::vector<double> cum(op->buckets.size() + 1, 0.0);
+    for (size_t b = 0; b < op->buckets.size(); ++b) {
+      double c = 0.0;
+      for (int q = op->buckets[b].z; q < op->buckets[b].w; ++q)
+        c += ghash[q].tab >= 0 ? 1.0 : 1.0 + (op->groups[q].w - op->groups[q].z) / 8.0;
+      cum[b + 1] = cum[b] + c;
+    }
+    const int nb = (int)op->buckets.size();
+    for (int S : {2, 4, 8}) {
+      int prev = 0;
+      splits.push_back(0);
+      for (int k = 1; k < S; ++k) {
+        const double target = cum[nb] * k / S;
+        int b = prev;
+        while (b < nb && cum[b] < target) ++b;
+        splits.push_back(b);
+        prev = b;
+      }
+      splits.push_back(nb);
+    }
+  }
   std::vector<unsigned char> recs;
   if (SH == 16) {
     recs.resize(ghash.size() * 32);
@@ -642,9 +716,12 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
       (rc = dalloc(&op->d_groups, op->groups.size())) ||
       (rc = dalloc(&op->d_terms, op->terms.size())) ||
       (rc = dalloc(&op->d_ghash, ghash.size())) || (rc = dalloc(&op->d_tabs, tabs.size())) ||
-      (rc = dalloc(reinterpret_cast<unsigned char**>(&op->d_recs), recs.size())))
+      (rc = dalloc(reinterpret_cast<unsigned char**>(&op->d_recs), recs.size())) ||
+      (rc = dalloc(&op->d_splits, splits.size())))
     return fail(rc);
   cudaStream_t st = stream();
+  HSV_TRY_CUDA(cudaMemcpyAsync(op->d_splits, splits.data(), splits.size() * sizeof(int),
+                               cudaMemcpyHostToDevice, st));
   if (!recs.empty())
     HSV_TRY_CUDA(cudaMemcpyAsync(op->d_recs, recs.data(), recs.size(), cudaMemcpyHostToDevice, st));
   if (!ghash.empty())
@@ -677,6 +754,7 @@ int hsv_op_destroy(hsv_op op) {
   dfree(op->d_ghash);
   dfree(op->d_tabs);
   dfree(reinterpret_cast<unsigned char*>(op->d_recs));
+  dfree(op->d_splits);
   delete op;
   return HSV_OK;
 }

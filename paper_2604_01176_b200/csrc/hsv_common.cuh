@@ -159,6 +159,7 @@ struct hsv_op_s {
   GroupHash* d_ghash = nullptr;
   void* d_recs = nullptr;       // packed Rec<W> per group (kernel layout)
   int64_t n_buckets_h = 0;      // buckets [0, n_buckets_h) are x-local (hashed)
+  int* d_splits = nullptr;      // bucket boundaries for 2, 4, 8 splits: 3 + 5 + 9 ints
   double* d_tabs = nullptr;
   int64_t n_hashed = 0;
   // host copies of the active group table (for CSR materialization)

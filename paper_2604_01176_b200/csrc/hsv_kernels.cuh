@@ -10,6 +10,7 @@ struct Tuning {
   int apply_minb = 0;     // __launch_bounds__ min blocks/SM: 0 = default (R=2: 4, R=4: 3);
                           // alternatives R=2: 3 or 5, R=4: 2
   int screen_rows = 1024; // rows staged per chunk in the screen kernel
+  int apply_split = 0;    // bucket splits per row unit in K1 (0 = auto, else 1/2/4/8)
 };
 Tuning& tuning();
 
@@ -35,6 +36,10 @@ struct ApplyArgs {
   int64_t a_lo, a_hi;
   int64_t units;
   int upr;
+  int nsplit;              // bucket splits per row unit (1: none)
+  const int* split_bk;     // nsplit + 1 bucket boundaries (combined bucket index space)
+  double2* ypart;          // [nsplit][rows of a_lo..a_hi] partial rows when nsplit > 1
+  int64_t part_stride;
   double prune;
   int energy_only;
 };

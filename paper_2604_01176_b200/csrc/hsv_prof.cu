@@ -63,6 +63,10 @@ int hsv_set_tuning(const char* key, int64_t value) {
   } else if (k == "apply_minb") {
     HSV_REQUIRE(value >= 0 && value <= 6, HSV_ERR_INVALID, "apply_minb must be in [0, 6]");
     g_tuning.apply_minb = (int)value;
+  } else if (k == "apply_split") {
+    HSV_REQUIRE(value == 0 || value == 1 || value == 2 || value == 4 || value == 8,
+                HSV_ERR_INVALID, "apply_split must be 0 (auto), 1, 2, 4 or 8");
+    g_tuning.apply_split = (int)value;
   } else if (k == "screen_rows") {
     HSV_REQUIRE(value >= 64 && value <= 8192, HSV_ERR_INVALID, "screen_rows out of range");
     g_tuning.screen_rows = (int)value;

@@ -31,6 +31,9 @@ def main():
     ap.add_argument("--apply-r", nargs="+", type=int, default=[0])
     ap.add_argument("--minb", nargs="+", type=int, default=[0])
     ap.add_argument("--screen-rows", nargs="+", type=int, default=[1024])
+    ap.add_argument("--split", nargs="+", type=int, default=[0])
+    ap.add_argument("--shard", nargs="+", type=int, default=[1],
+                    help="time the rank-0 alpha-row shard of a W-way split")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--lib", default=None, help="alternative libhsv build (A/B runs)")
     args = ap.parse_args()
@@ -48,28 +51,46 @@ def main():
         st = hsv.SvState(basis, hsv.SparseVector(dim, np.arange(dim, dtype=np.int64), v))
         nnz = op.nnz
         info = op.info()
-        for r, sr, mb in [(r, sr, mb) for r in args.apply_r for sr in args.screen_rows
-                          for mb in args.minb]:
-            if True:
-                N.call("hsv_set_tuning", b"apply_r", r)
-                N.call("hsv_set_tuning", b"apply_minb", mb)
-                N.call("hsv_set_tuning", b"screen_rows", sr)
-                e, g = op.energy_screen_pool(st, pool)          # warm
-                N.call("hsv_prof_reset")
-                N.call("hsv_prof_enable", 1)
-                for _ in range(args.reps):
-                    e, g = op.energy_screen_pool(st, pool)
-                N.call("hsv_prof_collect")
-                N.call("hsv_prof_enable", 0)
-                ta, _ = prof("apply")
-                ts, _ = prof("screen")
-                bytes_apply = 16.0 * nnz + 24.0 * dim
-                print(json.dumps({
-                    "system": name, "dim": dim, "apply_r": r, "minb": mb, "screen_rows": sr,
-                    "apply_ms": ta, "screen_ms": ts, "apply_GBs_alg": bytes_apply / ta / 1e6,
-                    "energy": e, "gmax": float(np.max(np.abs(g))), "nnz": nnz, **info}),
-                    flush=True)
+        na = basis._sector.n_alpha_strings
+        d_out = None
+        for r, sr, mb, sp, sh in [(r, sr, mb, sp, sh) for r in args.apply_r
+                                  for sr in args.screen_rows for mb in args.minb
+                                  for sp in args.split for sh in args.shard]:
+            N.call("hsv_set_tuning", b"apply_r", r)
+            N.call("hsv_set_tuning", b"apply_minb", mb)
+            N.call("hsv_set_tuning", b"screen_rows", sr)
+            N.call("hsv_set_tuning", b"apply_split", sp)
+            a_hi = na // sh            # rank-0 shard of an sh-way owner-computes split
+            out = np.empty(2 + pool.n)
 
+            def step():
+                if sh == 1:
+                    return op.energy_screen_pool(st, pool)
+                N.call("hsv_energy_screen_pool_async", op.handle, st.device.handle, pool.handle,
+                       0, a_hi, N.C.c_void_p(d_dev))
+                N.call("hsv_synchronize")
+                return None, None
+            if sh > 1 and d_out is None:
+                import torch
+                d_out = torch.zeros(2 + pool.n, dtype=torch.float64, device="cuda")
+                torch.cuda.synchronize()
+            d_dev = d_out.data_ptr() if d_out is not None else 0
+            e, g = step()                    # warm
+            N.call("hsv_prof_reset")
+            N.call("hsv_prof_enable", 1)
+            for _ in range(args.reps):
+                e, g = step()
+            N.call("hsv_prof_collect")
+            N.call("hsv_prof_enable", 0)
+            ta, _ = prof("apply")
+            ts, _ = prof("screen")
+            bytes_apply = (16.0 * nnz + 24.0 * dim) * a_hi / na
+            print(json.dumps({
+                "system": name, "dim": dim, "apply_r": r, "minb": mb, "screen_rows": sr,
+                "split": sp, "shard": sh, "apply_ms": ta, "screen_ms": ts,
+                "apply_GBs_alg": bytes_apply / ta / 1e6, "energy": e,
+                "gmax": None if g is None else float(np.max(np.abs(g))), "nnz": nnz, **info}),
+                flush=True)
 
 if __name__ == "__main__":
     main()
