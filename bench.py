@@ -53,7 +53,12 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.rows = []
+        self.marks = []
         self.proc = None
+
+    def mark(self):
+        """Record the current sample count (start / end of the timed region)."""
+        self.marks.append(len(self.rows))
 
     def __enter__(self):
         try:
@@ -82,15 +87,22 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        rows = self.rows
+        scope = "timed region"
+        if len(self.marks) >= 2 and self.marks[1] > self.marks[0]:
+            rows = self.rows[self.marks[0]:self.marks[1] + 1]
+        elif len(self.marks) >= 1 and self.marks[0] > 0:
+            rows = self.rows[max(0, self.marks[0] - 2):self.marks[0] + 2]
+            scope = "around timed region (region shorter than the 100 ms sampling period)"
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+                "samples": len(rows), "scope": scope}
 
 
 def peaks():
@@ -135,15 +147,19 @@ def step_roofline(sysm, ops, nnz, dim, ms, hbm):
             "unit": "GB/s"}
 
 
-def cpu_reference(sysm, psi, steps=1, warmup=0):
-    """Reference CPU algorithm (oracle port) on a bounded sample; seconds/step."""
-    from oracle import cpu_baseline
+def cpu_reference(sysm, psi, steps, warmup):
+    """Reference CPU algorithm (oracle port) on a bounded sample: mean seconds per
+    extrapolated step over `steps` timed samples (after `warmup` untimed ones)."""
+    from oracle.cpu_baseline import ReferenceStepSampler
     h = sysm.hamiltonian
-    res = None
-    for _ in range(warmup + steps):
-        res = cpu_baseline.measure_step(h.xs, h.zs, h.coeffs, sysm.n_qubits, sysm.n_alpha,
-                                        sysm.n_beta, sysm.integrals.nelec, psi)
-    return res
+    smp = ReferenceStepSampler(h.xs, h.zs, h.coeffs, sysm.n_qubits, sysm.n_alpha,
+                               sysm.n_beta, sysm.integrals.nelec, psi)
+    for _ in range(warmup):
+        smp.step()
+    ts = [smp.step()["t_step_s"] for _ in range(steps)]
+    smp.close()
+    return {"t_step_s": statistics.mean(ts), "threads": smp.n_workers,
+            "sample": smp.describe(), "setup_s": smp.t_setup}
 
 
 def run_reference(args):
@@ -155,15 +171,9 @@ def run_reference(args):
     dim = len(sysm.basis)
     psi = s1_values(dim)
     T = len(sysm.hamiltonian)
-    cpu_reference(sysm, psi, steps=1, warmup=0) if args.warmup > 0 else None
-    times, res = [], None
-    for _ in range(args.steps):
-        res = cpu_reference(sysm, psi)
-        times.append(res["t_step_s"])
-    t = statistics.mean(times)
+    res = cpu_reference(sysm, psi, args.steps, args.warmup)
+    t = res["t_step_s"]
     val = T * dim / t
-    sample = (f"H rows [0,{res['rows']}) of {dim} ({res['sample_nnz']} CSR nnz) + "
-              f"{res['ops_sampled']} of {res['ops']} pool ops, extrapolated linearly")
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
@@ -172,7 +182,7 @@ def run_reference(args):
         "config": {"workload": "H12 STO-3G energy + 1818 QEB pool gradients, S1 dense state",
                    "dim": dim, "n_terms": T},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": res["threads"], "kind": "port",
-                         "sample": sample},
+                         "sample": res["sample"]},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -190,6 +200,8 @@ def run_hsv(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+        os.environ["NCCL_DEBUG"] = "WARN"      # keep stdout to the one JSON line
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     N.init(local)
@@ -238,15 +250,21 @@ def run_hsv(args):
         torch.cuda.synchronize()
 
     # ---- device-resident throughput (value) ----
-    for _ in range(args.warmup):
-        step_device()
-    barrier()
-    N.lib().hsv_launch_count(1)
-    N.call("hsv_prof_reset")
-    N.call("hsv_prof_enable", 1)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     with ClockSampler(local) as clk:
+        # warm-up inside the sampler so nvidia-smi is already sampling when timing starts
+        t_w = time.perf_counter()
+        while True:
+            for _ in range(args.warmup):
+                step_device()
+            barrier()
+            if time.perf_counter() - t_w > 0.5:
+                break
+        N.lib().hsv_launch_count(1)
+        N.call("hsv_prof_reset")
+        N.call("hsv_prof_enable", 1)
+        clk.mark()
         barrier()
         for i in range(args.steps):
             flush.zero_()                     # L2 flush between timed steps (outside events)
@@ -254,6 +272,7 @@ def run_hsv(args):
             out = step_device()
             ev[i][1].record()
         barrier()
+        clk.mark()
     N.call("hsv_prof_collect")
     N.call("hsv_prof_enable", 0)
     launches = int(N.lib().hsv_launch_count(1))
@@ -299,6 +318,25 @@ def run_hsv(args):
         e2e_t = float(tt.item())
     e2e_value = T * dim / (e2e_t * 1e-3)
 
+    # ---- ADAPT-VQE iteration time (second half of the BASELINE metric), N = 1 ----
+    adapt = None
+    if world == 1 and not args.no_adapt:
+        eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
+        torch.cuda.synchronize()
+        res = hsv.run_adapt(hsv.AdaptConfig(engine="sv", eps_grad=1e-6,
+                                            max_iter=args.adapt_iters), sysm, engine=eng)
+        wall = np.array([r.wall_elapsed for r in res.records])
+        evals = np.array([r.energy_evals for r in res.records])
+        it_s = np.diff(wall)
+        half = len(it_s) // 2
+        adapt = {"iterations": int(len(it_s)),
+                 "iter_ms_mean_second_half": float(np.mean(it_s[half:]) * 1e3),
+                 "iter_ms": [round(float(x) * 1e3, 2) for x in it_s],
+                 "lbfgs_evals_per_iter": np.diff(evals).tolist(),
+                 "final_energy": float(res.records[-1].energy),
+                 "final_nnz": int(res.records[-1].nnz),
+                 "mode": "free run, eps_grad=1e-6, wall clock incl. host L-BFGS"}
+
     if rank == 0:
         pk, pk_kind = peaks()
         hbm = float(pk.get("hbm_gbs", 6650.0))
@@ -334,15 +372,14 @@ def run_hsv(args):
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_t,
                     "h2d_bytes_per_step": dim * 16, "d2h_bytes_per_step": (2 + M) * 8},
             "gpu_launches": launches,
+            "adapt_iteration": adapt,
             "clocks": clk.summary(),
         }
         if not args.no_cpu and world == 1:     # cpu_baseline: rank 0 at N=1 only
-            r = cpu_reference(sysm, psi_vals)
+            r = cpu_reference(sysm, psi_vals, steps=10, warmup=1)
             line["cpu_baseline"] = {
                 "value": T * dim / r["t_step_s"], "unit": UNIT, "cores": r["threads"],
-                "kind": "port",
-                "sample": (f"H rows [0,{r['rows']}) of {dim} ({r['sample_nnz']} CSR nnz) + "
-                           f"{r['ops_sampled']}/{r['ops']} pool ops, extrapolated"),
+                "kind": "port", "sample": r["sample"] + " (10 samples)",
                 "ms_per_step": r["t_step_s"] * 1e3}
         print(json.dumps(line))
     if world > 1:
@@ -353,10 +390,12 @@ def run_hsv(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="hsv", choices=["hsv", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-adapt", action="store_true", help="skip the ADAPT iteration timing")
+    ap.add_argument("--adapt-iters", type=int, default=16)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "hsv":
         args.warmup = 3
