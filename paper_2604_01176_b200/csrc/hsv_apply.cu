@@ -146,9 +146,15 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t tw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t u0 = gw * a.units / tw, u1 = (gw + 1) * a.units / tw;
   double er = 0.0, ei = 0.0;
-  for (int64_t uw = u0; uw < u1; ++uw) {
+  // Static schedule.  Contiguous unit blocks per warp keep a warp on one alpha
+  // row (L1 reuse) and win while psi fits in L2; interleaved units keep all warps
+  // on neighbouring alpha rows so the partner rows they gather stay in L2 when
+  // psi is far larger than L2 (H14/H16).
+  const int64_t u_begin = a.interleave ? gw : gw * a.units / tw;
+  const int64_t u_end = a.interleave ? a.units : (gw + 1) * a.units / tw;
+  const int64_t u_step = a.interleave ? tw : 1;
+  for (int64_t uw = u_begin; uw < u_end; uw += u_step) {
     // a work unit = (row unit, bucket split); splits > 1 only when row units are scarce
     const int64_t u = uw / a.nsplit;
     const int sp = (int)(uw - u * a.nsplit);
@@ -313,6 +319,9 @@ static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
   if (!a0.split_bk) S = 1;
   a.nsplit = S;
   a.split_bk = S == 1 ? nullptr : a0.split_bk + (S == 2 ? 0 : S == 4 ? 3 : 8);
+  // psi well inside L2 (126 MB): contiguous; otherwise interleaved (measured)
+  const int il = tuning().apply_interleave;   // -1 auto, 0 off, 1 on
+  a.interleave = il == 1 || (il < 0 && a0.dim_bytes > ((int64_t)64 << 20));
   a.units = units1 * S;
   int64_t grid = max_warps / 8;
   const int64_t need = (a.units + 7) / 8;
@@ -353,6 +362,7 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   ApplyArgs a{};
   a.arow = arow;
   a.split_bk = op->d_splits;
+  a.dim_bytes = s->dim * (int64_t)sizeof(double2);
   a.Sa = s->d_Sa; a.Sb = s->d_Sb; a.Ra = s->d_Ra; a.Rb = s->d_Rb;
   a.buckets = op->d_buckets; a.n_buckets = (int)op->n_buckets;
   a.groups = op->d_groups; a.terms = op->d_terms; a.diag = op->d_diag;

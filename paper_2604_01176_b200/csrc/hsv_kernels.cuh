@@ -11,6 +11,7 @@ struct Tuning {
                           // alternatives R=2: 3 or 5, R=4: 2
   int screen_rows = 1024; // rows staged per chunk in the screen kernel
   int apply_split = 0;    // bucket splits per row unit in K1 (0 = auto, else 1/2/4/8)
+  int apply_interleave = -1;  // K1 unit schedule: -1 auto (psi > 64 MB), 0 contiguous, 1 interleaved
 };
 Tuning& tuning();
 
@@ -37,6 +38,8 @@ struct ApplyArgs {
   int64_t units;
   int upr;
   int nsplit;              // bucket splits per row unit (1: none)
+  int interleave;          // unit schedule: 0 contiguous blocks per warp, 1 interleaved
+  int64_t dim_bytes;       // size of psi in bytes (schedule choice)
   const int* split_bk;     // nsplit + 1 bucket boundaries (combined bucket index space)
   double2* ypart;          // [nsplit][rows of a_lo..a_hi] partial rows when nsplit > 1
   int64_t part_stride;
