@@ -85,6 +85,8 @@ def reference_outputs(name: str, system: MolecularSystem, full_hpsi: bool):
     pool = build_qeb_pool(system.n_qubits, system.integrals.nelec, system.ordering,
                           system.integrals.ms2)
     out = {"dim": len(basis), "csr_nnz": m.nnz}
+    if len(basis) <= 400:   # full reference CSR: matrix elements checked bit for bit
+        out["csr_ro"], out["csr_ci"], out["csr_v"] = m.row_offsets, m.col_indices, m.values
     # HF
     hf = engine.initial_state()
     out["e_hf"] = engine.energy(hf)

@@ -53,6 +53,15 @@ def test_csr_restatement_bitwise(name):
         assert np.array_equal(gi, ref[f"gen{j}_idx"]) and np.array_equal(gv, ref[f"gen{j}_val"])
 
 
+@pytest.mark.parametrize("name", ["h2", "h4", "h6"])
+def test_csr_arrays_equal_reference_csr(name):
+    s, h, states, ops = problem(name)
+    ref = load_golden(f"ref_{name}")
+    ro, ci, v = O.assemble_csr(h.xs, h.zs, h.coeffs, states)
+    assert np.array_equal(ro, ref["csr_ro"]) and np.array_equal(ci, ref["csr_ci"])
+    assert np.array_equal(v, ref["csr_v"])
+
+
 @pytest.mark.parametrize("name", SMALL + ["h10"])
 def test_matrix_free_restatement(name):
     s, h, states, ops = problem(name)
