@@ -123,6 +123,10 @@ HSV_API int hsv_state_nnz(hsv_state st, int64_t* nnz);
  * |v| < prune when prune > 0). cap = capacity of the output buffers. */
 HSV_API int hsv_state_get_sparse(hsv_state st, double prune, int64_t* pos, double* amps_re,
                          double* amps_im, int64_t cap, int64_t* n_out);
+/* Amplitudes at given reference positions (zero where not in the support);
+ * a cheap peek for sampled validation of very large states. */
+HSV_API int hsv_state_get_positions(hsv_state st, const int64_t* pos, int64_t n, double* amps_re,
+                                    double* amps_im);
 /* <a|b> (dot, sparse.py:210-219). */
 HSV_API int hsv_state_dot(hsv_state a, hsv_state b, double* re, double* im);
 HSV_API int hsv_state_norm(hsv_state st, double* norm);

@@ -60,6 +60,7 @@ _SIGNATURES = {
     "hsv_state_set_keys": (C.c_int, [vp, P_u64, P_dbl, P_dbl, i64]),
     "hsv_state_nnz": (C.c_int, [vp, P_i64]),
     "hsv_state_get_sparse": (C.c_int, [vp, dbl, P_i64, P_dbl, P_dbl, i64, P_i64]),
+    "hsv_state_get_positions": (C.c_int, [vp, P_i64, i64, P_dbl, P_dbl]),
     "hsv_state_dot": (C.c_int, [vp, vp, P_dbl, P_dbl]),
     "hsv_state_norm": (C.c_int, [vp, P_dbl]),
     "hsv_state_axpy": (C.c_int, [dbl, dbl, vp, vp]),

@@ -202,6 +202,12 @@ __global__ void k_gather_i64(const int64_t* __restrict__ tab, const int64_t* __r
   if (i < n) out[i] = idx[i] < 0 ? -1 : tab[idx[i]];
 }
 
+__global__ void k_gather_amp(const double2* __restrict__ a, const int64_t* __restrict__ idx,
+                             int64_t n, double2* __restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) out[i] = a[idx[i]];
+}
+
 int upload_amps(const double* re, const double* im, int64_t n, double2** d_out) {
   std::vector<double2> h(n);
   for (int64_t i = 0; i < n; ++i) h[i] = make_double2(re[i], im ? im[i] : 0.0);
@@ -419,6 +425,34 @@ int hsv_state_get_sparse(hsv_state st, double prune, int64_t* pos, double* re, d
     dfree(d_pos); dfree(d_re); dfree(d_im);
   }
   dfree(d_ref); dfree(d_flag); dfree(d_off); dfree(reinterpret_cast<char*>(d_tmp));
+  return HSV_OK;
+}
+
+int hsv_state_get_positions(hsv_state st, const int64_t* pos, int64_t n, double* re, double* im) {
+  HSV_REQUIRE(st && (n == 0 || (pos && re)), HSV_ERR_INVALID, "null argument");
+  if (n == 0) return HSV_OK;
+  for (int64_t i = 0; i < n; ++i)
+    HSV_REQUIRE(pos[i] >= 0 && pos[i] < st->sec->dim, HSV_ERR_INVALID,
+                "position %lld out of range", (long long)pos[i]);
+  int64_t *d_p = nullptr, *d_i = nullptr;
+  double2* d_v = nullptr;
+  HSV_TRY(dalloc(&d_p, n));
+  HSV_TRY(dalloc(&d_i, n));
+  HSV_TRY(dalloc(&d_v, n));
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_p, pos, n * 8, cudaMemcpyHostToDevice, stream()));
+  const unsigned g = (unsigned)((n + 255) / 256);
+  k_gather_i64<<<g, 256, 0, stream()>>>(st->sec->d_iperm, d_p, n, d_i);
+  k_gather_amp<<<g, 256, 0, stream()>>>(st->d_amp, d_i, n, d_v);
+  count_launch(2);
+  HSV_CHECK_LAUNCH();
+  std::vector<double2> h(n);
+  HSV_TRY_CUDA(cudaMemcpyAsync(h.data(), d_v, n * sizeof(double2), cudaMemcpyDeviceToHost, stream()));
+  HSV_TRY(stream_sync());
+  dfree(d_p); dfree(d_i); dfree(d_v);
+  for (int64_t i = 0; i < n; ++i) {
+    re[i] = h[i].x;
+    if (im) im[i] = h[i].y;
+  }
   return HSV_OK;
 }
 

@@ -129,6 +129,20 @@ class DeviceState:
         N.call("hsv_state_nnz", self.handle, N.C.byref(n))
         return n.value
 
+    def at_positions(self, positions) -> np.ndarray:
+        """Amplitudes at reference positions (zero outside the support)."""
+        pos = N.as_i64(positions)
+        re = np.empty(pos.size)
+        im = np.empty(pos.size)
+        N.call("hsv_state_get_positions", self.handle, N.ptr_i64(pos), pos.size, N.ptr_f64(re),
+               N.ptr_f64(im))
+        return re if not np.any(im) else re + 1j * im
+
+    def dot(self, other: "DeviceState") -> complex:
+        re, im = N.dbl(), N.dbl()
+        N.call("hsv_state_dot", self.handle, other.handle, N.C.byref(re), N.C.byref(im))
+        return complex(re.value, im.value)
+
     def to_sparse(self, prune: float = 0.0) -> SparseVector:
         n = N.i64()
         N.call("hsv_state_get_sparse", self.handle, float(prune), None, None, None, 0, N.C.byref(n))
