@@ -210,7 +210,8 @@ def run_hsv(args):
     torch.cuda.set_stream(stream)
     N.call("hsv_set_stream", N.C.c_void_p(stream.cuda_stream))
 
-    sysm = hsv.MolecularSystem.bundled(CONFIG)
+    cfg = args.config
+    sysm = hsv.MolecularSystem.bundled(cfg)
     basis = sysm.basis
     dim = len(basis)
     T = len(sysm.hamiltonian)
@@ -320,7 +321,7 @@ def run_hsv(args):
 
     # ---- ADAPT-VQE iteration time (second half of the BASELINE metric), N = 1 ----
     adapt = None
-    if world == 1 and not args.no_adapt:
+    if world == 1 and not args.no_adapt and cfg in ("h10", "h12"):
         eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
         torch.cuda.synchronize()
         res = hsv.run_adapt(hsv.AdaptConfig(engine="sv", eps_grad=1e-6,
@@ -349,12 +350,14 @@ def run_hsv(args):
         achieved = bytes_apply / (apply_ms * 1e-3) / 1e9
         screen_ms = prof["screen"][0] / max(prof["screen"][1], 1)
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": METRIC if cfg == CONFIG else METRIC.replace("H12", cfg.upper()),
+            "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "c128 (f64)", "data": "synthetic S1 state (default_rng(20240811)), "
-                                          "bundled H12 Pauli sum from the reference builder",
-            "config": {"workload": "H12 STO-3G energy + 1818 QEB pool gradients, S1 dense state",
+                                          f"bundled {cfg.upper()} Pauli sum from the reference builder",
+            "config": {"workload": f"{cfg.upper()} STO-3G energy + {M} QEB pool gradients, "
+                                   "S1 dense state",
                        "dim": dim, "n_terms": T, "pool": M, "csr_nnz": nnz_struct,
                        "l2": "flushed between timed steps (256 MiB write, outside events)",
                        "parallelism": f"owner-computes alpha rows x{world}"},
@@ -375,7 +378,7 @@ def run_hsv(args):
             "adapt_iteration": adapt,
             "clocks": clk.summary(),
         }
-        if not args.no_cpu and world == 1:     # cpu_baseline: rank 0 at N=1 only
+        if not args.no_cpu and world == 1 and cfg == CONFIG:   # rank 0 at N=1, metric config
             r = cpu_reference(sysm, psi_vals, steps=10, warmup=1)
             line["cpu_baseline"] = {
                 "value": T * dim / r["t_step_s"], "unit": UNIT, "cores": r["threads"],
@@ -396,6 +399,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-adapt", action="store_true", help="skip the ADAPT iteration timing")
     ap.add_argument("--adapt-iters", type=int, default=16)
+    ap.add_argument("--config", default=CONFIG, choices=["h8", "h10", "h12", "h14", "h16"],
+                    help="system (the BASELINE metric is quoted on h12; others for scaling runs)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "hsv":
         args.warmup = 3
