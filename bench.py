@@ -200,10 +200,20 @@ def run_hsv(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
-        os.environ["NCCL_DEBUG"] = "WARN"      # keep stdout to the one JSON line
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL prints its version banner on fd 1 when the communicator is created;
+        # route fd 1 to stderr meanwhile so stdout carries only the JSON line
+        sys.stdout.flush()
+        saved = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+            torch.cuda.synchronize()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     N.init(local)
     # a real (non-legacy) stream shared by torch events, NCCL and libhsv launches
     stream = torch.cuda.Stream()
@@ -321,9 +331,13 @@ def run_hsv(args):
 
     # ---- ADAPT-VQE iteration time (second half of the BASELINE metric), N = 1 ----
     adapt = None
-    if world == 1 and not args.no_adapt and cfg in ("h10", "h12"):
-        eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
-        torch.cuda.synchronize()
+    if not args.no_adapt and cfg in ("h10", "h12"):
+        if world > 1:
+            from paper_2604_01176_b200.distributed import DistributedSvAdaptEngine
+            eng = DistributedSvAdaptEngine(sysm, hsv.AdaptConfig())
+        else:
+            eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
+        barrier()
         res = hsv.run_adapt(hsv.AdaptConfig(engine="sv", eps_grad=1e-6,
                                             max_iter=args.adapt_iters), sysm, engine=eng)
         wall = np.array([r.wall_elapsed for r in res.records])
@@ -336,7 +350,9 @@ def run_hsv(args):
                  "lbfgs_evals_per_iter": np.diff(evals).tolist(),
                  "final_energy": float(res.records[-1].energy),
                  "final_nnz": int(res.records[-1].nnz),
-                 "mode": "free run, eps_grad=1e-6, wall clock incl. host L-BFGS"}
+                 "mode": "free run, eps_grad=1e-6, wall clock incl. host L-BFGS"
+                         + (f"; {world} ranks: H psi rows owner-computed + NCCL all-gather"
+                            if world > 1 else "")}
 
     if rank == 0:
         pk, pk_kind = peaks()

@@ -157,6 +157,18 @@ HSV_API int hsv_energy_screen(hsv_op op, hsv_state psi, const uint64_t* occ_mask
 HSV_API int hsv_energy_gradient(hsv_op op, uint64_t hf_key, const uint64_t* occ_masks,
                         const uint64_t* virt_masks, const double* cs, const double* sn,
                         int64_t k, double* energy, double* grads);
+/* The same sweep in two phases for multi-GPU (owner computes H psi rows):
+ * forward: psi <- exp(...)|hf> on all rows (replicated), w rows [a_lo, a_hi)
+ * <- (H psi) rows (returns after a stream sync, to report norm drift); the caller makes
+ * w complete on every rank (all-gather of the row blocks);
+ * backward: E = Re<psi|w> and the adjoint sweep; psi and w are consumed. */
+HSV_API int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ_masks,
+                                 const uint64_t* virt_masks, const double* cs, const double* sn,
+                                 int64_t k, int64_t a_lo, int64_t a_hi, hsv_state psi_out,
+                                 hsv_state w_out);
+HSV_API int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ_masks,
+                            const uint64_t* virt_masks, const double* cs, const double* sn,
+                            int64_t k, double* energy, double* grads);
 /* Owner-computes shard variants for multi-GPU (rows = alpha-strings
  * [a_lo, a_hi)).  Write, without synchronizing, to DEVICE memory:
  *   d_out[0..1] = partial <psi|H|psi> (re, im), d_out[2..2+n_ops) = partial

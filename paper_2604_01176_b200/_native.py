@@ -71,6 +71,9 @@ _SIGNATURES = {
     "hsv_apply_generator": (C.c_int, [vp, vp, u64, u64]),
     "hsv_energy_screen": (C.c_int, [vp, vp, P_u64, P_u64, i64, P_dbl, P_dbl]),
     "hsv_energy_gradient": (C.c_int, [vp, u64, P_u64, P_u64, P_dbl, P_dbl, i64, P_dbl, P_dbl]),
+    "hsv_eg_forward_async": (C.c_int, [vp, u64, P_u64, P_u64, P_dbl, P_dbl, i64, i64, i64, vp,
+                                       vp]),
+    "hsv_eg_backward": (C.c_int, [vp, vp, vp, P_u64, P_u64, P_dbl, P_dbl, i64, P_dbl, P_dbl]),
     "hsv_energy_screen_partial_async": (C.c_int, [vp, vp, P_u64, P_u64, i64, i64, i64, vp]),
     "hsv_state_device_ptr": (C.c_int, [vp, C.POINTER(vp), P_i64]),
     "hsv_apply_h_rows_async": (C.c_int, [vp, vp, vp, i64, i64, dbl]),

@@ -340,103 +340,126 @@ int hsv_apply_generator(hsv_state in, hsv_state out, uint64_t occ, uint64_t virt
   return stream_sync();
 }
 
-int hsv_energy_gradient(hsv_op op, uint64_t hf_key, const uint64_t* occ, const uint64_t* virt,
-                        const double* cs, const double* sn, int64_t k, double* energy,
-                        double* grads) {
-  HSV_REQUIRE(op && energy && (k == 0 || (occ && virt && cs && sn && grads)), HSV_ERR_INVALID,
-              "null argument");
+static int check_eg_args(hsv_op op, const uint64_t* occ, const uint64_t* virt, const double* cs,
+                         const double* sn, int64_t k) {
+  HSV_REQUIRE(op && (k == 0 || (occ && virt && cs && sn)), HSV_ERR_INVALID, "null argument");
+  for (int64_t i = 0; i < k; ++i)
+    HSV_REQUIRE((occ[i] & virt[i]) == 0 && occ[i] && virt[i], HSV_ERR_INVALID,
+                "excitation indices must be distinct");
+  return HSV_OK;
+}
+
+// Phase 1 of the adjoint sweep: psi <- prod_i exp(theta_i T_i)|hf> (all rows;
+// occupancy flags and norm maintained), w rows [a_lo, a_hi) <- (H psi) rows.
+int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const uint64_t* virt,
+                         const double* cs, const double* sn, int64_t k, int64_t a_lo,
+                         int64_t a_hi, hsv_state psi, hsv_state w) {
+  HSV_TRY(check_eg_args(op, occ, virt, cs, sn, k));
+  HSV_REQUIRE(psi && w && psi != w && psi->sec == op->sec && w->sec == op->sec,
+              HSV_ERR_INVALID, "bad state argument");
   const hsv_sector_s* sec = op->sec;
-  const int64_t dim = sec->dim;
-  // psi <- |hf>
-  uint32_t sa = sec->compress_a(hf_key), sb = sec->compress_b(hf_key);
+  HSV_REQUIRE(0 <= a_lo && a_lo <= a_hi && a_hi <= sec->Na, HSV_ERR_INVALID, "bad alpha-row range");
+  const uint32_t sa = sec->compress_a(hf_key), sb = sec->compress_b(hf_key);
   HSV_REQUIRE((sec->n_qubits >= 64 || (hf_key >> sec->n_qubits) == 0) && sec->Ra[sa] != ~0u &&
                   sec->Rb[sb] != ~0u,
               HSV_ERR_SECTOR, "configuration %#llx is outside the basis sector",
               (unsigned long long)hf_key);
-  for (int64_t i = 0; i < k; ++i)
-    HSV_REQUIRE((occ[i] & virt[i]) == 0 && occ[i] && virt[i], HSV_ERR_INVALID,
-                "excitation indices must be distinct");
-  double2 *psi = nullptr, *lam = nullptr;
-  double *d_n2 = nullptr, *d_ln2 = nullptr, *d_grad = nullptr, *d_e = nullptr, *epart = nullptr;
-  HSV_TRY(dalloc(&psi, dim));
-  HSV_TRY(dalloc(&lam, dim));
-  HSV_TRY(dalloc(&d_n2, 1));
-  HSV_TRY(dalloc(&d_ln2, 1));
-  HSV_TRY(dalloc(&d_grad, std::max<int64_t>(k, 1)));
-  HSV_TRY(dalloc(&d_e, 2));
-  const int nw = apply_warps(op);
-  HSV_TRY(dalloc(&epart, 2 * (int64_t)nw));
-  HSV_TRY_CUDA(cudaMemsetAsync(epart, 0, 2 * sizeof(double) * nw, stream()));
-  HSV_TRY_CUDA(cudaMemsetAsync(psi, 0, dim * sizeof(double2), stream()));
+  // psi <- |hf>, flags = HF alpha row only
+  HSV_TRY(state_fill_zero_async(psi));
   static thread_local double2 one;
   static thread_local double n2one;
+  static thread_local uint32_t one_flag;
   one = make_double2(1.0, 0.0);
   n2one = 1.0;
-  const int64_t hidx = (int64_t)sec->Ra[sa] * sec->Nb + sec->Rb[sb];
-  HSV_TRY_CUDA(cudaMemcpyAsync(psi + hidx, &one, sizeof(double2), cudaMemcpyHostToDevice, stream()));
-  HSV_TRY_CUDA(cudaMemcpyAsync(d_n2, &n2one, sizeof(double), cudaMemcpyHostToDevice, stream()));
-  // alpha-row occupancy of psi (HF row only) and of lam (after H psi)
-  uint32_t *d_fpsi = nullptr, *d_flam = nullptr;
-  HSV_TRY(dalloc(&d_fpsi, std::max<int64_t>(sec->Na, 1)));
-  HSV_TRY(dalloc(&d_flam, std::max<int64_t>(sec->Na, 1)));
-  HSV_TRY_CUDA(cudaMemsetAsync(d_fpsi, 0, sec->Na * sizeof(uint32_t), stream()));
-  static thread_local uint32_t one_flag;
   one_flag = 1u;
-  HSV_TRY_CUDA(cudaMemcpyAsync(d_fpsi + sec->Ra[sa], &one_flag, sizeof(uint32_t),
+  const int64_t hidx = (int64_t)sec->Ra[sa] * sec->Nb + sec->Rb[sb];
+  HSV_TRY_CUDA(cudaMemcpyAsync(psi->d_amp + hidx, &one, sizeof(double2), cudaMemcpyHostToDevice,
+                               stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(psi->d_norm2, &n2one, sizeof(double), cudaMemcpyHostToDevice,
+                               stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(psi->d_arow + sec->Ra[sa], &one_flag, sizeof(uint32_t),
                                cudaMemcpyHostToDevice, stream()));
+  PairScratch sc;
+  HSV_TRY(sc.init(sec, 2));
+  PairLists pl;
+  for (int64_t i = 0; i < k; ++i) {
+    if (cs[i] == 1.0 && sn[i] == 0.0) continue;
+    HSV_TRY(build_pair_lists_async(sec, compress_op(sec, occ[i], virt[i]), pl));
+    PairArgs a{};
+    a.Nb = sec->Nb; a.psi = psi->d_amp; a.c = cs[i]; a.s = sn[i];
+    a.part = sc.part; a.counter = sc.counter; a.norm2 = psi->d_norm2;
+    a.err = sc.err; a.err_val = sc.err_val; a.fpsi = psi->d_arow;
+    HSV_TRY(launch_pairs<kRotate>(pl, a));
+  }
+  psi->norm2_valid = psi->arow_valid = true;
+  int64_t used = 0;
+  HSV_TRY(launch_apply(op, psi->d_amp, w->d_amp, nullptr, a_lo, a_hi, 0.0, 0, &used, psi->d_arow));
+  w->norm2_valid = w->arow_valid = false;
+  // drift errors surface here (synchronizes)
+  const int rc = sc.check();
+  dfree(pl.la); dfree(pl.lb);
+  sc.release();
+  return rc;
+}
 
+// Phase 2: E = Re <psi|w> (w complete on every row) and the backward sweep
+// (svengine.py:276-280), uncomputing psi instead of storing k+1 states.
+// psi and w are consumed (rotated in place).
+int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
+                    const uint64_t* virt, const double* cs, const double* sn, int64_t k,
+                    double* energy, double* grads) {
+  HSV_TRY(check_eg_args(op, occ, virt, cs, sn, k));
+  HSV_REQUIRE(energy && (k == 0 || grads), HSV_ERR_INVALID, "null output");
+  HSV_REQUIRE(psi && w && psi != w && psi->sec == op->sec && w->sec == op->sec,
+              HSV_ERR_INVALID, "bad state argument");
+  const hsv_sector_s* sec = op->sec;
+  double e_re = 0.0, e_im = 0.0;
+  HSV_TRY(hsv_state_dot(psi, w, &e_re, &e_im));
+  double* d_grad = nullptr;
+  HSV_TRY(dalloc(&d_grad, std::max<int64_t>(k, 1)));
+  HSV_TRY(state_arow_async(psi));
+  HSV_TRY(state_arow_async(w));
+  if (k > 0) HSV_TRY(state_norm2_async(w));   // <lam|lam> for the drift checks
   PairScratch sc;
   HSV_TRY(sc.init(sec, 3));
-  std::vector<PairLists> lists(k);
-  // forward sweep: psi <- exp(theta_i T_i) psi, in place
-  for (int64_t i = 0; i < k; ++i) {
-    HSV_TRY(build_pair_lists_async(sec, compress_op(sec, occ[i], virt[i]), lists[i]));
-    if (cs[i] == 1.0 && sn[i] == 0.0) continue;
-    PairArgs a{};
-    a.Nb = sec->Nb; a.psi = psi; a.c = cs[i]; a.s = sn[i];
-    a.part = sc.part; a.counter = sc.counter; a.norm2 = d_n2; a.err = sc.err; a.err_val = sc.err_val;
-    a.fpsi = d_fpsi;
-    HSV_TRY(launch_pairs<kRotate>(lists[i], a));
-  }
-  // w = H psi (into lam), E = <psi|w>
-  int64_t used = 0;
-  HSV_TRY(launch_apply(op, psi, lam, epart, 0, sec->Na, 0.0, 0, &used, d_fpsi));
-  HSV_TRY(reduce_sum_f64(epart, used, 2, 2, d_e));
-  HSV_TRY(arow_flags_async(lam, sec->Na, sec->Nb, d_flam));
-  if (k > 0) {
-    // <lam|lam> for the adjoint drift checks
-    hsv_state_s tmp;
-    tmp.sec = const_cast<hsv_sector_s*>(sec);
-    tmp.d_amp = lam;
-    tmp.d_norm2 = d_ln2;
-    HSV_TRY(state_norm2_async(&tmp));
-    tmp.d_amp = nullptr;
-    tmp.d_norm2 = nullptr;
-  }
-  // backward sweep (svengine.py:276-280), uncomputing psi instead of storing k+1 states
+  PairLists pl;
   for (int64_t i = k - 1; i >= 0; --i) {
-    PairArgs a{};
-    a.Nb = sec->Nb; a.psi = psi; a.lam = lam; a.c = cs[i]; a.s = -sn[i];
-    a.part = sc.part; a.counter = sc.counter; a.norm2 = d_ln2; a.result = d_grad + i;
-    a.err = sc.err; a.err_val = sc.err_val; a.uncompute = i > 0;
-    a.fpsi = d_fpsi; a.flam = d_flam;
-    if (lists[i].ca == 0 || lists[i].cb == 0) {
+    HSV_TRY(build_pair_lists_async(sec, compress_op(sec, occ[i], virt[i]), pl));
+    if (pl.ca == 0 || pl.cb == 0) {
       HSV_TRY_CUDA(cudaMemsetAsync(d_grad + i, 0, sizeof(double), stream()));
       continue;
     }
-    HSV_TRY(launch_pairs<kAdjoint>(lists[i], a));
+    PairArgs a{};
+    a.Nb = sec->Nb; a.psi = psi->d_amp; a.lam = w->d_amp; a.c = cs[i]; a.s = -sn[i];
+    a.part = sc.part; a.counter = sc.counter; a.norm2 = w->d_norm2; a.result = d_grad + i;
+    a.err = sc.err; a.err_val = sc.err_val; a.uncompute = i > 0;
+    a.fpsi = psi->d_arow; a.flam = w->d_arow;
+    HSV_TRY(launch_pairs<kAdjoint>(pl, a));
   }
-  double he[2] = {0, 0};
-  HSV_TRY_CUDA(cudaMemcpyAsync(he, d_e, 16, cudaMemcpyDeviceToHost, stream()));
   if (k > 0)
     HSV_TRY_CUDA(cudaMemcpyAsync(grads, d_grad, k * sizeof(double), cudaMemcpyDeviceToHost, stream()));
-  int rc = sc.check();
-  for (auto& pl : lists) { dfree(pl.la); dfree(pl.lb); }
+  const int rc = sc.check();
+  dfree(pl.la); dfree(pl.lb);
   sc.release();
-  dfree(psi); dfree(lam); dfree(d_n2); dfree(d_ln2); dfree(d_grad); dfree(d_e); dfree(epart);
-  dfree(d_fpsi); dfree(d_flam);
+  dfree(d_grad);
+  psi->norm2_valid = false;
   HSV_TRY(stream_sync());
-  *energy = he[0];
+  *energy = e_re;
+  return rc;
+}
+
+int hsv_energy_gradient(hsv_op op, uint64_t hf_key, const uint64_t* occ, const uint64_t* virt,
+                        const double* cs, const double* sn, int64_t k, double* energy,
+                        double* grads) {
+  HSV_TRY(check_eg_args(op, occ, virt, cs, sn, k));
+  HSV_REQUIRE(energy && (k == 0 || grads), HSV_ERR_INVALID, "null output");
+  hsv_state psi = nullptr, w = nullptr;
+  HSV_TRY(hsv_state_create(op->sec, &psi));
+  int rc = hsv_state_create(op->sec, &w);
+  if (!rc) rc = hsv_eg_forward_async(op, hf_key, occ, virt, cs, sn, k, 0, op->sec->Na, psi, w);
+  if (!rc) rc = hsv_eg_backward(op, psi, w, occ, virt, cs, sn, k, energy, grads);
+  hsv_state_destroy(psi);
+  hsv_state_destroy(w);
   return rc;
 }
 

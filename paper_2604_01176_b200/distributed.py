@@ -16,6 +16,18 @@ import torch.distributed as dist
 from . import _native as N
 
 
+def bind_library_stream():
+    """Run libhsv kernels and torch/NCCL work on one (non-legacy) CUDA stream so
+    collectives issued by the host are ordered with the library's kernels."""
+    N.init(torch.cuda.current_device())
+    s = torch.cuda.current_stream()
+    if s.cuda_stream == 0:            # legacy default stream: switch to a real one
+        s = torch.cuda.Stream()
+        torch.cuda.set_stream(s)
+    N.call("hsv_set_stream", N.C.c_void_p(s.cuda_stream))
+    return s
+
+
 def alpha_row_range(n_alpha_strings: int, rank: int, world: int) -> tuple[int, int]:
     """Contiguous, balanced (+-1) alpha-row block of `rank` (cf. sparse.py:204-207)."""
     return n_alpha_strings * rank // world, n_alpha_strings * (rank + 1) // world
@@ -36,6 +48,104 @@ def gather_and_combine(partial: torch.Tensor, group=None) -> torch.Tensor:
     buf = torch.empty((world,) + tuple(partial.shape), dtype=partial.dtype, device=partial.device)
     dist.all_gather_into_tensor(buf, partial, group=group)
     return combine_partials(buf)
+
+
+def allgather_rows(view: torch.Tensor, n_alpha_strings: int, nb: int, group=None):
+    """Make the alpha-row blocks of a replicated [dim, 2] buffer identical on all
+    ranks: each rank contributes rows alpha_row_range(rank) (NCCL all-gather of
+    padded blocks, then placement in rank order)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    rng = [alpha_row_range(n_alpha_strings, r, world) for r in range(world)]
+    maxrows = max(hi - lo for lo, hi in rng) * nb
+    send = torch.zeros((maxrows, 2), dtype=view.dtype, device=view.device)
+    lo, hi = rng[rank]
+    send[: (hi - lo) * nb] = view[lo * nb: hi * nb]
+    recv = torch.empty((world, maxrows, 2), dtype=view.dtype, device=view.device)
+    dist.all_gather_into_tensor(recv, send, group=group)
+    for r, (lo, hi) in enumerate(rng):
+        if r != rank:
+            view[lo * nb: hi * nb] = recv[r, : (hi - lo) * nb]
+
+
+class DistributedSvAdaptEngine:
+    """SvAdaptEngine over torch.distributed ranks (one GPU each).
+
+    * screen / energy: owner-computes partials, all-gathered and summed in rank order;
+    * energy_and_gradient: forward sweep replicated, H psi rows owner-computed and
+      all-gathered (NCCL), backward adjoint sweep replicated -- every rank obtains
+      bitwise identical E and gradients, so the host L-BFGS stays in lock step.
+    """
+
+    name = "sv"
+    uses_coordinate_search = False
+
+    def __init__(self, system, config, group=None):
+        from .adapt import SvAdaptEngine
+        from .svengine import DeviceState
+        bind_library_stream()
+        self.inner = SvAdaptEngine(system, config)
+        self.system, self.basis, self.matrix = system, self.inner.basis, self.inner.matrix
+        self.run_log = self.inner.run_log
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.na = self.basis._sector.n_alpha_strings
+        self.nb = self.basis._sector.n_beta_strings
+        self.a_lo, self.a_hi = alpha_row_range(self.na, self.rank, self.world)
+        self._psi = DeviceState(self.basis)
+        self._w = DeviceState(self.basis)
+        self._screens = {}
+
+    def initial_state(self):
+        return self.inner.initial_state()
+
+    def apply(self, state, op, theta, log=None):
+        return self.inner.apply(state, op, theta)
+
+    def rebuild(self, ops, thetas):
+        return self.inner.rebuild(ops, thetas)
+
+    def state_size(self, state):
+        return state.nnz
+
+    def drain_log(self):
+        return []
+
+    def _screen(self, pool):
+        key = tuple(getattr(pool, "ops", pool))
+        if key not in self._screens:
+            self._screens[key] = ShardedEnergyScreen(self.inner, key, self.rank, self.world)
+        return self._screens[key]
+
+    def energy_and_screen(self, state, pool):
+        sc = self._screen(pool)
+        sc.launch(state)
+        tot = gather_and_combine(sc.partial, self.group)
+        host = tot.cpu().numpy()
+        return float(host[0]), host[2:].copy()
+
+    def screen(self, state, pool):
+        return self.energy_and_screen(state, pool)[1]
+
+    def energy(self, state):
+        return self.energy_and_screen(state, ())[0]     # empty pool: energy partials only
+
+    def energy_and_gradient(self, ops, thetas):
+        import numpy as np
+        occ, virt = self.inner._pool_masks(ops)
+        th = np.ascontiguousarray(thetas, dtype=np.float64)
+        cs, sn = N.as_f64(np.cos(th)), N.as_f64(np.sin(th))
+        N.call("hsv_eg_forward_async", self.matrix.handle, int(self.system.hf.bits),
+               N.ptr_u64(occ), N.ptr_u64(virt), N.ptr_f64(cs), N.ptr_f64(sn), th.size,
+               self.a_lo, self.a_hi, self._psi.handle, self._w.handle)
+        allgather_rows(self._w.torch_view(), self.na, self.nb, self.group)
+        g = np.empty(th.size)
+        e = N.dbl()
+        N.call("hsv_eg_backward", self.matrix.handle, self._psi.handle, self._w.handle,
+               N.ptr_u64(occ), N.ptr_u64(virt), N.ptr_f64(cs), N.ptr_f64(sn), th.size,
+               N.C.byref(e), N.ptr_f64(g))
+        return float(e.value), g
 
 
 class ShardedEnergyScreen:

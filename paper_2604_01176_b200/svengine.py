@@ -138,6 +138,19 @@ class DeviceState:
                N.ptr_f64(im))
         return re if not np.any(im) else re + 1j * im
 
+    @property
+    def __cuda_array_interface__(self):
+        ptr, n = N.C.c_void_p(), N.i64()
+        N.call("hsv_state_device_ptr", self.handle, N.C.byref(ptr), N.C.byref(n))
+        return {"shape": (n.value, 2), "typestr": "<f8", "data": (ptr.value or 0, False),
+                "version": 3, "strides": None}
+
+    def torch_view(self):
+        """Zero-copy torch float64 [dim, 2] view of the (alpha-major) amplitudes, for
+        collectives issued by the host; writes through it invalidate cached norms."""
+        import torch
+        return torch.as_tensor(self, device="cuda")
+
     def dot(self, other: "DeviceState") -> complex:
         re, im = N.dbl(), N.dbl()
         N.call("hsv_state_dot", self.handle, other.handle, N.C.byref(re), N.C.byref(im))
