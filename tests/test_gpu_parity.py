@@ -168,6 +168,41 @@ def test_sharded_partials_sum_to_full(hsv):
         assert rel_err(tot, ref_full) <= 1e-12
 
 
+def test_two_phase_adjoint_sweep_emulated_shards(hsv):
+    """hsv_eg_forward on 3 alpha-row blocks (as 3 ranks would), rows assembled like
+    the NCCL all-gather does, then hsv_eg_backward == the one-call adjoint sweep."""
+    import torch
+    from paper_2604_01176_b200 import _native as N
+    from paper_2604_01176_b200.distributed import alpha_row_range
+    from paper_2604_01176_b200.svengine import DeviceState
+    sysm, eng, pool, ref = setup(hsv, "h8")
+    ops = [pool.ops[i] for i in ref["s2_ops"]]
+    th = np.asarray(ref["s2_thetas"], dtype=np.float64)
+    occ, virt = eng._pool_masks(ops)
+    cs, sn = np.cos(th), np.sin(th)
+    na = sysm.basis._sector.n_alpha_strings
+    nb = sysm.basis._sector.n_beta_strings
+    psi = DeviceState(sysm.basis)
+    w_full = DeviceState(sysm.basis)
+    world = 3
+    for r in range(world):
+        lo, hi = alpha_row_range(na, r, world)
+        wr = DeviceState(sysm.basis)
+        N.call("hsv_eg_forward_async", eng.matrix.handle, int(sysm.hf.bits), N.ptr_u64(occ),
+               N.ptr_u64(virt), N.ptr_f64(cs), N.ptr_f64(sn), th.size, lo, hi, psi.handle,
+               wr.handle)
+        N.call("hsv_synchronize")
+        w_full.torch_view()[lo * nb: hi * nb] = wr.torch_view()[lo * nb: hi * nb]
+        torch.cuda.synchronize()
+    g = np.empty(th.size)
+    e = N.dbl()
+    N.call("hsv_eg_backward", eng.matrix.handle, psi.handle, w_full.handle, N.ptr_u64(occ),
+           N.ptr_u64(virt), N.ptr_f64(cs), N.ptr_f64(sn), th.size, N.C.byref(e), N.ptr_f64(g))
+    e1, g1 = eng.energy_and_gradient(ops, th)
+    assert abs(e.value - e1) <= 1e-13 and rel_err(g, g1) <= 1e-13
+    assert abs(e1 - float(ref["eg_s2_e"])) <= TOL and rel_err(g1, ref["eg_s2_g"]) <= TOL
+
+
 def test_determinism(hsv):
     sysm, eng, pool, ref = setup(hsv, "h8")
     st = s1_state(hsv, sysm)
