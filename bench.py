@@ -337,9 +337,12 @@ def run_hsv(args):
             eng = DistributedSvAdaptEngine(sysm, hsv.AdaptConfig())
         else:
             eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
+        from paper_2604_01176_b200.fci import lanczos_ground_energy
+        e_fci = lanczos_ground_energy(eng.matrix)      # device Lanczos (untimed)
         barrier()
         res = hsv.run_adapt(hsv.AdaptConfig(engine="sv", eps_grad=1e-6,
-                                            max_iter=args.adapt_iters), sysm, engine=eng)
+                                            max_iter=args.adapt_iters), sysm, engine=eng,
+                            reference_energy=e_fci)
         wall = np.array([r.wall_elapsed for r in res.records])
         evals = np.array([r.energy_evals for r in res.records])
         it_s = np.diff(wall)
@@ -349,6 +352,8 @@ def run_hsv(args):
                  "iter_ms": [round(float(x) * 1e3, 2) for x in it_s],
                  "lbfgs_evals_per_iter": np.diff(evals).tolist(),
                  "final_energy": float(res.records[-1].energy),
+                 "e_fci_device_lanczos": e_fci,
+                 "final_abs_error": float(res.records[-1].abs_error),
                  "final_nnz": int(res.records[-1].nnz),
                  "mode": "free run, eps_grad=1e-6, wall clock incl. host L-BFGS"
                          + (f"; {world} ranks: H psi rows owner-computed + NCCL all-gather"

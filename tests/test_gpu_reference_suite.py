@@ -312,6 +312,16 @@ def test_criterion_03_h6_chemical_accuracy(hsv, systems):
     assert hits and hits[0] <= 250
 
 
+@pytest.mark.parametrize("name", ["h2", "h4", "h6", "h8", "h10"])
+def test_gpu_lanczos_fci_matches_reference_eigsh(hsv, name):
+    """Device Lanczos (fci.py) vs the reference's oracle.fci_ground_energy values."""
+    from paper_2604_01176_b200.fci import lanczos_ground_energy
+    s = hsv.MolecularSystem.bundled(name)
+    m = hsv.assemble_subspace_hamiltonian(s.hamiltonian, s.basis)
+    e = lanczos_ground_energy(m)
+    assert abs(e - float(load_golden(f"ref_{name}")["e_fci"])) <= 1e-10
+
+
 # --------------------------------------------------- orderings / sectors
 def _to_blocked(x: int, n: int) -> int:
     norb = n // 2
