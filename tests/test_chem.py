@@ -1,0 +1,63 @@
+"""Host Hamiltonian build (chem.py) against the reference builder's Pauli sums.
+
+The bundled ham_h*.npz were produced by the reference (FCIDUMP -> JW,
+tests/golden/make_golden.py); here the package rebuilds them from the same
+FCIDUMP text and must give the same Pauli words with coefficients to 1e-13.
+FCIDUMP inputs are read from the reference tree when it is mounted (this CPU
+suite); the GPU box never reads it.
+"""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_2604_01176_b200 import chem
+from paper_2604_01176_b200.system import MolecularSystem
+
+DATA = Path("/root/reference/pkg/src/svmps/data")
+
+
+@pytest.mark.skipif(not DATA.exists(), reason="reference FCIDUMP fixtures not mounted")
+@pytest.mark.parametrize("name", ["h2", "h4", "h6", "h8"])
+def test_jw_matches_reference_pauli_sum(name):
+    ints = chem.load_fcidump(DATA / f"{name}.fcidump")
+    ours = chem.molecular_system(ints)
+    ref = MolecularSystem.bundled(name)
+    a, b = ours.hamiltonian, ref.hamiltonian
+    assert a.n_qubits == b.n_qubits
+    assert np.array_equal(a.xs, b.xs) and np.array_equal(a.zs, b.zs)
+    assert np.max(np.abs(a.coeffs - b.coeffs)) <= 1e-13
+    assert ours.hf.bits == ref.hf.bits
+    assert (ours.n_alpha, ours.n_beta) == (ref.n_alpha, ref.n_beta)
+
+
+def test_fcidump_roundtrip_minimal():
+    text = """ &FCI NORB=2,NELEC=2,MS2=0,
+  ORBSYM=1,1,
+  ISYM=1,
+ &END
+  0.5 1 1 1 1
+  0.25 2 1 1 1
+  0.6 2 2 2 2
+  0.3 2 2 1 1
+  -1.2 1 1 0 0
+  0.1 2 1 0 0
+  -0.4 2 2 0 0
+  0.7 0 0 0 0
+"""
+    ints = chem.parse_fcidump(text)
+    assert ints.norb == 2 and ints.nelec == 2 and ints.core_energy == 0.7
+    assert ints.one_body[0, 1] == ints.one_body[1, 0] == 0.1
+    g = ints.two_body
+    assert g[1, 0, 0, 0] == g[0, 1, 0, 0] == g[0, 0, 1, 0] == g[0, 0, 0, 1] == 0.25
+    assert g[1, 1, 0, 0] == g[0, 0, 1, 1] == 0.3
+    h = chem.molecular_system(ints).hamiltonian
+    assert h.identity_coefficient != 0.0
+    assert np.all(np.bitwise_count((h.xs & h.zs).astype(np.uint64)) % 2 == 0)   # real words
+
+
+def test_non_hermitian_rejected():
+    h = np.zeros((4, 4))
+    h[0, 2] = 1.0                     # a+_0 a_2 without its conjugate
+    with pytest.raises(ValueError, match="not Hermitian"):
+        chem.jordan_wigner(h, np.zeros((4,) * 4), 0.0, 4)
