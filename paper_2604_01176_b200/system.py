@@ -61,6 +61,17 @@ class MolecularSystem:
         return cls(integrals=info, ordering=ordering, hamiltonian=h, hf=hf)
 
     @classmethod
+    def from_fcidump(cls, path, ordering: str = "interleaved") -> "MolecularSystem":
+        """FCIDUMP -> spin orbitals -> Jordan-Wigner (system.py:43-45 semantics)."""
+        from .chem import load_fcidump, molecular_system
+        return molecular_system(load_fcidump(path), ordering)
+
+    @classmethod
+    def from_fcidump_text(cls, text: str, ordering: str = "interleaved") -> "MolecularSystem":
+        from .chem import molecular_system, parse_fcidump
+        return molecular_system(parse_fcidump(text), ordering)
+
+    @classmethod
     def bundled(cls, name: str) -> "MolecularSystem":
         with np.load(bundled_hamiltonian(name)) as z:
             n = int(z["n_qubits"])
