@@ -57,9 +57,21 @@ def main():
             print(json.dumps({"system": name, "k": k, "eval_ms": dt * 1e3,
                               "kernel_ms_per_eval": kern, "energy": e}), flush=True)
         recs = []
+        N.call("hsv_prof_reset")
+        N.call("hsv_prof_enable", 1)
+        N.lib().hsv_launch_count(1)
         t0 = time.perf_counter()
         res = hsv.run_adapt(hsv.AdaptConfig(engine="sv", eps_grad=1e-6, max_iter=args.iters),
                             sysm, engine=eng, progress=recs.append)
+        N.call("hsv_prof_collect")
+        N.call("hsv_prof_enable", 0)
+        kern = {}
+        for kn in ("apply", "screen", "qeb", "adjoint"):
+            t, c = N.dbl(), N.i64()
+            N.call("hsv_prof_get", kn.encode(), N.C.byref(t), N.C.byref(c))
+            kern[kn] = {"ms": round(t.value, 2), "launches": c.value}
+        print(json.dumps({"system": name, "adapt_kernel_totals": kern,
+                          "all_launches": int(N.lib().hsv_launch_count(1))}), flush=True)
         wall = [r.wall_elapsed for r in res.records]
         it_t = np.diff(wall)
         evals = np.diff([r.energy_evals for r in res.records])
