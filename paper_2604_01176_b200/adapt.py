@@ -156,6 +156,7 @@ class SvAdaptEngine:
         self.run_log = TruncationLog()
         self._masks: dict = {}
         self._dpools: dict = {}
+        self._dpool_last = None
 
     def _pool_masks(self, ops):
         key = tuple(ops)
@@ -183,11 +184,16 @@ class SvAdaptEngine:
         return self.matrix.energy_gradient(self.system.hf.bits, occ, virt, thetas)
 
     def _device_pool(self, pool):
-        ops = tuple(getattr(pool, "ops", pool))
+        seq = getattr(pool, "ops", pool)
+        last = self._dpool_last
+        if last is not None and last[0] is seq and isinstance(seq, tuple):
+            return last[1]                        # same immutable op tuple: skip hashing 1818 ops
+        ops = tuple(seq)
         dp = self._dpools.get(ops)
         if dp is None:
             dp = DevicePool(self.basis, ops)
             self._dpools = {ops: dp} if len(self._dpools) > 4 else {**self._dpools, ops: dp}
+        self._dpool_last = (seq, dp)
         return dp
 
     def screen(self, state, pool) -> np.ndarray:

@@ -111,26 +111,6 @@ __global__ void k_csr_rows(const uint32_t* __restrict__ Sa, const uint32_t* __re
 }
 
 // --------------------------------------------------------------- K1 apply
-// Packed per-group record of an x-local group, loaded with one or two 16-byte
-// uniform loads: meta = hb | shift << 8.
-template <typename W> struct Rec;
-template <> struct __align__(16) Rec<uint32_t> {
-  uint32_t xb, meta, xm, z0, mul, tab, pad0, pad1;
-};
-template <> struct __align__(16) Rec<uint64_t> {
-  uint32_t xb, meta, tab, pad0;
-  uint64_t xm, z0, mul, pad1;
-};
-template <typename W>
-__device__ __forceinline__ Rec<W> ldrec(const Rec<W>* p) {
-  Rec<W> r;
-  const uint4* q = reinterpret_cast<const uint4*>(p);
-  uint4* d = reinterpret_cast<uint4*>(&r);
-#pragma unroll
-  for (int i = 0; i < (int)(sizeof(Rec<W>) / 16); ++i) d[i] = __ldg(q + i);
-  return r;
-}
-
 // Warp-granular static schedule: a unit is 32*R consecutive beta rows of one
 // alpha row, so the alpha half of every sector test is warp-uniform and whole
 // buckets are skipped without divergence.  Each lane owns R rows.
@@ -357,7 +337,7 @@ int apply_warps(const hsv_op_s* op) {
 
 int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* epart,
                  int64_t a_lo, int64_t a_hi, double prune, int energy_only, int64_t* n_warps,
-                 const uint32_t* arow) {
+                 const uint32_t* arow, bool* dense_hint) {
   const hsv_sector_s* s = op->sec;
   ApplyArgs a{};
   a.arow = arow;
@@ -369,6 +349,11 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   a.tabs = op->d_tabs; a.recs = op->d_recs; a.n_buckets_h = (int)op->n_buckets_h;
   a.psi = psi; a.out = out; a.epart = epart;
   a.Nb = s->Nb; a.a_lo = a_lo; a.a_hi = a_hi; a.prune = prune; a.energy_only = energy_only;
+  if (tuning().push != 0) {   // sparse psi: scatter + sort-reduce (hsv_push.cu)
+    bool done = false;
+    HSV_TRY(launch_push(op, a, &done, n_warps, dense_hint));
+    if (done) return HSV_OK;
+  }
   int R = tuning().apply_r;
   const int M = tuning().apply_minb;
   if (R == 0) {
@@ -858,9 +843,10 @@ int hsv_apply_h(hsv_op op, hsv_state in, hsv_state out, double prune) {
   HSV_REQUIRE(in != out, HSV_ERR_INVALID, "hsv_apply_h: output must not alias input");
   HSV_TRY(state_arow_async(in));
   HSV_TRY(launch_apply(op, in->d_amp, out->d_amp, nullptr, 0, op->sec->Na, prune, 0, nullptr,
-                       in->d_arow));
+                       in->d_arow, &in->dense_hint));
   out->norm2_valid = false;
   out->arow_valid = false;
+  out->dense_hint = false;
   return stream_sync();
 }
 
@@ -872,9 +858,10 @@ int hsv_apply_h_rows_async(hsv_op op, hsv_state in, hsv_state out, int64_t a_lo,
               "bad alpha-row range");
   HSV_TRY(state_arow_async(in));
   HSV_TRY(launch_apply(op, in->d_amp, out->d_amp, nullptr, a_lo, a_hi, prune, 0, nullptr,
-                       in->d_arow));
+                       in->d_arow, &in->dense_hint));
   out->norm2_valid = false;
   out->arow_valid = false;
+  out->dense_hint = false;
   return HSV_OK;
 }
 
@@ -888,7 +875,8 @@ int hsv_expect_h(hsv_op op, hsv_state psi, double* e_re, double* e_im) {
   HSV_TRY_CUDA(cudaMemsetAsync(part, 0, 2 * sizeof(double) * nw, stream()));
   int64_t used = 0;
   HSV_TRY(state_arow_async(psi));
-  HSV_TRY(launch_apply(op, psi->d_amp, nullptr, part, 0, op->sec->Na, 0.0, 1, &used, psi->d_arow));
+  HSV_TRY(launch_apply(op, psi->d_amp, nullptr, part, 0, op->sec->Na, 0.0, 1, &used, psi->d_arow,
+                       &psi->dense_hint));
   HSV_TRY(reduce_sum_f64(part, used, 2, 2, d_e));
   double h[2];
   HSV_TRY_CUDA(cudaMemcpyAsync(h, d_e, 16, cudaMemcpyDeviceToHost, stream()));

@@ -187,6 +187,9 @@ struct hsv_state_s {
   // changes no result (skipped terms are exact zeros).
   uint32_t* d_arow = nullptr;
   bool arow_valid = false;
+  // Set when the K1 push path found psi too dense (skip its probe next time);
+  // cleared by every write.  Only ever disables the push path.
+  bool dense_hint = false;
 };
 
 namespace hsv {

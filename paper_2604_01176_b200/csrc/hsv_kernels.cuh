@@ -12,6 +12,8 @@ struct Tuning {
   int screen_rows = 1024; // rows staged per chunk in the screen kernel
   int apply_split = 0;    // bucket splits per row unit in K1 (0 = auto, else 1/2/4/8)
   int apply_interleave = -1;  // K1 unit schedule: -1 auto (psi > 64 MB), 0 contiguous, 1 interleaved
+  int push = -1;          // sparse-psi push path: -1 auto, 0 off, 1 whenever it fits in memory
+  int push_keys = 32;   // auto: push while nnz(psi) * (1 + groups) <= push_keys * rows - 2^20
 };
 Tuning& tuning();
 
@@ -47,11 +49,45 @@ struct ApplyArgs {
   int energy_only;
 };
 
+// Packed per-group record of an x-local group, loaded with one or two 16-byte
+// uniform loads: meta = hb | shift << 8.
+template <typename W> struct Rec;
+template <> struct __align__(16) Rec<uint32_t> {
+  uint32_t xb, meta, xm, z0, mul, tab, pad0, pad1;
+};
+template <> struct __align__(16) Rec<uint64_t> {
+  uint32_t xb, meta, tab, pad0;
+  uint64_t xm, z0, mul, pad1;
+};
+template <typename W>
+__device__ __forceinline__ Rec<W> ldrec(const Rec<W>* p) {
+  Rec<W> r;
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  uint4* d = reinterpret_cast<uint4*>(&r);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Rec<W>) / 16); ++i) d[i] = __ldg(q + i);
+  return r;
+}
+
+// Matrix element of an x-local group at row s: (-1)^popc(s & z0) * A[h(s & x)].
+template <typename W>
+__device__ __forceinline__ double rec_amp(const Rec<W>& r, W s, const double* __restrict__ tabs) {
+  const int shift = (int)((r.meta >> 8) & 0xffu);
+  const uint32_t h = r.tab + (uint32_t)((W)((s & r.xm) * r.mul) >> shift);
+  const double A = __ldg(tabs + h);
+  const int sgn = popc(s & r.z0) << 31;
+  return __hiloint2double(__double2hiint(A) ^ sgn, __double2loint(A));
+}
+
 int grid_for(int64_t n, int block);
 int apply_warps(const hsv_op_s* op);
+// Push (scatter + sort-reduce) K1 for sparse psi; *done = false: use the pull kernel.
+// dense_hint (optional, per state): skip when set, set when psi is found dense.
+int launch_push(const hsv_op_s* op, const ApplyArgs& a, bool* done, int64_t* n_warps,
+                bool* dense_hint);
 int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* epart,
                  int64_t a_lo, int64_t a_hi, double prune, int energy_only, int64_t* n_warps,
-                 const uint32_t* arow = nullptr);
+                 const uint32_t* arow = nullptr, bool* dense_hint = nullptr);
 
 // Compressed QEB masks of one excitation operator.
 struct OpMasks {

@@ -301,6 +301,7 @@ int hsv_apply_qeb(hsv_state in, hsv_state out, uint64_t occ, uint64_t virt, doub
     HSV_TRY_CUDA(cudaMemcpyAsync(out->d_arow, in->d_arow, in->sec->Na * sizeof(uint32_t),
                                  cudaMemcpyDeviceToDevice, stream()));
     out->arow_valid = in->arow_valid;
+    out->dense_hint = in->dense_hint;
   }
   if (c == 1.0 && s == 0.0) return stream_sync();   // theta == 0 returns the input (svengine.py:212)
   if (!out->norm2_valid) HSV_TRY(state_norm2_async(out));
@@ -320,6 +321,7 @@ int hsv_apply_qeb(hsv_state in, hsv_state out, uint64_t occ, uint64_t virt, doub
   dfree(pl.la); dfree(pl.lb);
   sc.release();
   out->norm2_valid = true;
+  out->dense_hint = false;
   return rc;
 }
 
@@ -337,6 +339,7 @@ int hsv_apply_generator(hsv_state in, hsv_state out, uint64_t occ, uint64_t virt
   dfree(pl.la); dfree(pl.lb);
   out->norm2_valid = false;
   out->arow_valid = false;
+  out->dense_hint = false;
   return stream_sync();
 }
 
@@ -392,9 +395,12 @@ int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const 
     HSV_TRY(launch_pairs<kRotate>(pl, a));
   }
   psi->norm2_valid = psi->arow_valid = true;
+  psi->dense_hint = false;
   int64_t used = 0;
-  HSV_TRY(launch_apply(op, psi->d_amp, w->d_amp, nullptr, a_lo, a_hi, 0.0, 0, &used, psi->d_arow));
+  HSV_TRY(launch_apply(op, psi->d_amp, w->d_amp, nullptr, a_lo, a_hi, 0.0, 0, &used, psi->d_arow,
+                       &psi->dense_hint));
   w->norm2_valid = w->arow_valid = false;
+  w->dense_hint = false;
   // drift errors surface here (synchronizes)
   const int rc = sc.check();
   dfree(pl.la); dfree(pl.lb);
@@ -443,6 +449,7 @@ int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
   sc.release();
   dfree(d_grad);
   psi->norm2_valid = false;
+  psi->dense_hint = w->dense_hint = false;
   HSV_TRY(stream_sync());
   *energy = e_re;
   return rc;

@@ -223,7 +223,8 @@ static int energy_screen_dev(hsv_op op, hsv_state psi, const hsv_pool_s* pool, i
   HSV_TRY_CUDA(cudaMemsetAsync(epart, 0, 2 * sizeof(double) * nw, stream()));
   int64_t used = 0;
   HSV_TRY(state_arow_async(psi));
-  HSV_TRY(launch_apply(op, psi->d_amp, w, epart, a_lo, a_hi, 0.0, 0, &used, psi->d_arow));
+  HSV_TRY(launch_apply(op, psi->d_amp, w, epart, a_lo, a_hi, 0.0, 0, &used, psi->d_arow,
+                       &psi->dense_hint));
   HSV_TRY(reduce_sum_f64(epart, used, 2, 2, d_out));
   // occupancy of the owned rows of w (other rows of w are never read)
   uint32_t* wrow = nullptr;

@@ -31,6 +31,7 @@ int state_fill_zero_async(hsv_state st) {
   HSV_TRY_CUDA(cudaMemsetAsync(st->d_arow, 0, st->sec->Na * sizeof(uint32_t), stream()));
   st->norm2_valid = true;
   st->arow_valid = true;
+  st->dense_hint = false;
   return HSV_OK;
 }
 
@@ -260,6 +261,7 @@ int hsv_state_copy(hsv_state dst, hsv_state src) {
                                cudaMemcpyDeviceToDevice, stream()));
   dst->norm2_valid = src->norm2_valid;
   dst->arow_valid = src->arow_valid;
+  dst->dense_hint = src->dense_hint;
   return stream_sync();
 }
 
@@ -288,6 +290,7 @@ int hsv_state_set_basis(hsv_state st, uint64_t key, double re, double im) {
   HSV_TRY_CUDA(cudaMemcpyAsync(st->d_norm2, &n2, sizeof(double), cudaMemcpyHostToDevice,
                                stream()));
   st->arow_valid = false;
+  st->dense_hint = false;
   return stream_sync();
 }
 
@@ -321,6 +324,7 @@ int hsv_state_set_sparse(hsv_state st, const int64_t* pos, const double* re, con
     dfree(d_bad);
   }
   st->arow_valid = false;
+  st->dense_hint = false;
   HSV_TRY(state_norm2_async(st));
   HSV_TRY(stream_sync());
   HSV_REQUIRE(!h_bad, HSV_ERR_INVALID, "position out of range for dimension %lld",
@@ -357,6 +361,7 @@ int hsv_state_set_keys(hsv_state st, const uint64_t* keys, const double* re, con
     dfree(d_i);
   }
   st->arow_valid = false;
+  st->dense_hint = false;
   HSV_TRY(state_norm2_async(st));
   return stream_sync();
 }
@@ -496,6 +501,7 @@ int hsv_state_axpy(double ar, double ai, hsv_state x, hsv_state y) {
   HSV_CHECK_LAUNCH();
   y->norm2_valid = false;
   y->arow_valid = false;
+  y->dense_hint = false;
   return stream_sync();
 }
 
@@ -507,6 +513,7 @@ int hsv_state_scale(hsv_state st, double ar, double ai) {
   HSV_CHECK_LAUNCH();
   st->norm2_valid = false;
   st->arow_valid = false;
+  st->dense_hint = false;
   return stream_sync();
 }
 
@@ -516,6 +523,7 @@ int hsv_state_device_ptr(hsv_state st, void** ptr, int64_t* n) {
   if (n) *n = st->sec->dim;
   st->norm2_valid = false;   // caller may write through the pointer
   st->arow_valid = false;
+  st->dense_hint = false;
   return HSV_OK;
 }
 

@@ -66,7 +66,7 @@ def main():
         N.call("hsv_prof_collect")
         N.call("hsv_prof_enable", 0)
         kern = {}
-        for kn in ("apply", "screen", "qeb", "adjoint"):
+        for kn in ("apply", "push", "push_collect", "screen", "qeb", "adjoint"):
             t, c = N.dbl(), N.i64()
             N.call("hsv_prof_get", kn.encode(), N.C.byref(t), N.C.byref(c))
             kern[kn] = {"ms": round(t.value, 2), "launches": c.value}
