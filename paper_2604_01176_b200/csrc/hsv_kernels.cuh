@@ -13,7 +13,9 @@ struct Tuning {
   int apply_split = 0;    // bucket splits per row unit in K1 (0 = auto, else 1/2/4/8)
   int apply_interleave = -1;  // K1 unit schedule: -1 auto (psi > 64 MB), 0 contiguous, 1 interleaved
   int push = -1;          // sparse-psi push path: -1 auto, 0 off, 1 whenever it fits in memory
-  int push_keys = 32;   // auto: push while nnz(psi) * (1 + groups) <= push_keys * rows - 2^20
+  int push_keys = 32;
+  int sweep = 1;          // adjoint/forward sweeps: 1 one cooperative launch, 0 launch per op
+  int sweep_grid = 0;     // sweep blocks: 0 = min(co-resident, work items)   // auto: push while nnz(psi) * (1 + groups) <= push_keys * rows - 2^20
 };
 Tuning& tuning();
 

@@ -73,6 +73,12 @@ int hsv_set_tuning(const char* key, int64_t value) {
   } else if (k == "push") {
     HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "push must be -1, 0 or 1");
     g_tuning.push = (int)value;
+  } else if (k == "sweep") {
+    HSV_REQUIRE(value == 0 || value == 1, HSV_ERR_INVALID, "sweep must be 0 or 1");
+    g_tuning.sweep = (int)value;
+  } else if (k == "sweep_grid") {
+    HSV_REQUIRE(value >= 0 && value <= (1 << 20), HSV_ERR_INVALID, "sweep_grid out of range");
+    g_tuning.sweep_grid = (int)value;
   } else if (k == "push_keys") {
     HSV_REQUIRE(value >= 0 && value <= 4096, HSV_ERR_INVALID, "push_keys out of range");
     g_tuning.push_keys = (int)value;

@@ -8,6 +8,7 @@
 // halves of a source row are independent, so the pair set is the product of
 // an alpha list (ranks of matching alpha strings and their partners) and a
 // beta list.  One thread handles one pair and touches only 2 rows.
+#include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -283,6 +284,298 @@ struct PairScratch {
   }
 };
 
+// ------------------------------------------------------------- fused sweep
+// All k rotations of a forward (kRotate) or adjoint (kAdjoint) sweep in ONE
+// cooperative launch: a persistent grid walks op after op, separated by a
+// grid barrier, instead of 2k launches (pair-list build + pair kernel per op)
+// whose host cost dominates at ADAPT sizes.
+//   phase 0: the pair lists of every op, built in parallel: the i-th source
+//            string of an op's alpha (beta) half is unranked directly
+//            (combinatorial number system over the free orbitals; ascending
+//            order = the rank order k_pair_list produces);
+//   phase 1: per op, work item = (alpha pair y, 256-wide beta chunk x) =
+//            block (x, y) of k_pairs; grid barrier between ops;
+//   phase 2: per-op totals (one op per block) and the norm chain.
+// Every reduction replays last_block_sum's order, so results are
+// bit-identical to the per-op launch path (tests/test_gpu_sweep.py).
+struct SweepOp {
+  uint32_t oa, va, ob, vb;
+  int32_t ca, cb, nx, la_off;   // la_off / lb_off: offsets of the op's lists
+  int32_t lb_off, pad;
+  double c, s;
+};
+
+struct SweepArgs {
+  const SweepOp* ops;
+  int n_ops;
+  int norb, n_alpha, n_beta;
+  int64_t Nb;
+  const uint32_t* Ra;
+  const uint32_t* Rb;
+  const int64_t* binom;
+  int2* lists;           // phase-0 pair lists {rank, partner rank}
+  double2* psi;
+  double2* lam;
+  uint32_t* fpsi;
+  uint32_t* flam;
+  double* part;          // [chunk][max_items][NV] per-op block partials
+  int64_t part_stride;   // max_items * NV
+  int chunk;             // ops per reduction chunk
+  double* red;           // [n_ops][NV] per-op totals
+  double* norm2;
+  double* grads;         // kAdjoint: gradient of op i at grads[i]
+  int* err;
+  double* err_val;
+};
+
+// Grid-wide barrier of the cooperative launch (measured 1.2 us at 2 blocks/SM,
+// 2.0 us at 6 blocks/SM; a hand-rolled atomic/spin barrier was 1.7x slower).
+__device__ __forceinline__ void grid_barrier() { cooperative_groups::this_grid().sync(); }
+
+// i-th string (ascending) with `occ` set, `virt` clear and `ones` electrons on
+// the remaining orbitals of `nmask`; binomials from a 32-bit table bt[n*32+k].
+__device__ __forceinline__ uint32_t unrank_string(int i, uint32_t occ, uint32_t virt,
+                                                  uint32_t nmask, int ones, const int* bt) {
+  uint32_t fm = nmask & ~(occ | virt);
+  uint32_t s = occ;
+  for (int p = __popc(fm) - 1; p >= 0 && ones > 0; --p) {
+    const int pos = 31 - __clz(fm);
+    fm &= ~(1u << pos);
+    const int c = ones <= p ? bt[p * 32 + ones] : 0;   // strings with this orbital empty first
+    if (i >= c) {
+      s |= 1u << pos;
+      i -= c;
+      --ones;
+    }
+  }
+  return s;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_sweep(const SweepArgs a) {
+  constexpr int NV = MODE == kAdjoint ? 3 : 2;
+  __shared__ double sh[NV][8];
+  __shared__ int bt[33 * 32];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const uint32_t nmask = a.norb >= 32 ? 0xffffffffu : ((1u << a.norb) - 1u);
+  for (int i = threadIdx.x; i < 33 * 32; i += blockDim.x) {
+    const int n = i >> 5, k = i & 31;
+    bt[i] = (int)dbinom(a.binom, n, k);
+  }
+  __syncthreads();
+  // phase 0: pair lists of all ops
+  {
+    const int tid = blockIdx.x * blockDim.x + threadIdx.x, nth = gridDim.x * blockDim.x;
+    for (int oi = 0; oi < a.n_ops; ++oi) {
+      const SweepOp o = a.ops[oi];
+      const int ones_a = a.n_alpha - __popc(o.oa), ones_b = a.n_beta - __popc(o.ob);
+      for (int e = tid; e < o.ca + o.cb; e += nth) {
+        const bool al = e < o.ca;
+        const uint32_t oc = al ? o.oa : o.ob, vi = al ? o.va : o.vb;
+        const uint32_t s = unrank_string(al ? e : e - o.ca, oc, vi, nmask, al ? ones_a : ones_b, bt);
+        const uint32_t* R = al ? a.Ra : a.Rb;
+        a.lists[(al ? o.la_off : o.lb_off - o.ca) + e] =
+            make_int2((int)__ldg(R + s), (int)__ldg(R + (s ^ (oc | vi))));
+      }
+    }
+  }
+  grid_barrier();
+  for (int c0 = 0; c0 < a.n_ops; c0 += a.chunk) {
+  const int c1 = min(a.n_ops, c0 + a.chunk);
+  for (int op = c0; op < c1; ++op) {
+    const int oi = MODE == kRotate ? op : a.n_ops - 1 - op;
+    const SweepOp o = a.ops[oi];
+    const int uncompute = MODE == kAdjoint && oi > 0;
+    double* part = a.part + (op - c0) * a.part_stride;
+    const int items = o.ca * o.nx;
+    const int2* la = a.lists + o.la_off;
+    const int2* lb = a.lists + o.lb_off;
+    for (int it = blockIdx.x; it < items; it += gridDim.x) {
+      const int y = it / o.nx;
+      const int xc = it - y * o.nx;
+      const int j = xc * 256 + threadIdx.x;
+      const int2 A = la[y];
+      const int2 B = j < o.cb ? lb[j] : make_int2(0, 0);
+      const bool ap = !a.fpsi || a.fpsi[A.x] || a.fpsi[A.y];
+      const bool al = MODE == kAdjoint && (!a.flam || a.flam[A.x] || a.flam[A.y]);
+      __syncthreads();   // flags read by every thread before thread 0 updates them
+      if (threadIdx.x == 0 && xc == 0) {
+        if (a.fpsi && ap && (MODE == kRotate || uncompute)) { a.fpsi[A.x] = 1u; a.fpsi[A.y] = 1u; }
+        if (MODE == kAdjoint && a.flam && al) { a.flam[A.x] = 1u; a.flam[A.y] = 1u; }
+      }
+      if (!(ap || al)) {   // whole item inactive: its partials are exact zeros
+        if (threadIdx.x == 0)
+          for (int q = 0; q < NV; ++q) part[(int64_t)it * NV + q] = 0.0;
+        continue;
+      }
+      double v[NV];
+#pragma unroll
+      for (int q = 0; q < NV; ++q) v[q] = 0.0;
+      if (j < o.cb) {
+        const int64_t ib = (int64_t)A.x * a.Nb + B.x;   // source row
+        const int64_t ip = (int64_t)A.y * a.Nb + B.y;   // partner
+        if (MODE == kRotate) {
+          const double2 vb = a.psi[ib], vp = a.psi[ip];
+          double2 nb, np;
+          givens(vb, vp, o.c, o.s, nb, np);
+          a.psi[ib] = nb;
+          a.psi[ip] = np;
+          v[0] = vb.x * vb.x + vb.y * vb.y + vp.x * vp.x + vp.y * vp.y;
+          v[1] = nb.x * nb.x + nb.y * nb.y + np.x * np.x + np.y * np.y;
+        } else {
+          const double2 pb = a.psi[ib], pp = a.psi[ip];
+          const double2 lb2 = a.lam[ib], lp = a.lam[ip];
+          v[0] = (lp.x * pb.x + lp.y * pb.y) - (lb2.x * pp.x + lb2.y * pp.y);
+          double2 nb, np;
+          givens(lb2, lp, o.c, -o.s, nb, np);
+          a.lam[ib] = nb;
+          a.lam[ip] = np;
+          v[1] = lb2.x * lb2.x + lb2.y * lb2.y + lp.x * lp.x + lp.y * lp.y;
+          v[NV - 1] = nb.x * nb.x + nb.y * nb.y + np.x * np.x + np.y * np.y;
+          if (uncompute) {
+            double2 qb, qp;
+            givens(pb, pp, o.c, -o.s, qb, qp);
+            a.psi[ib] = qb;
+            a.psi[ip] = qp;
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {   // block partial, last_block_sum order
+        const double x = warp_sum(v[q]);
+        if (l == 0) sh[q][w] = x;
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+          double x = 0.0;
+          for (int k = 0; k < 8; ++k) x += sh[q][k];
+          part[(int64_t)it * NV + q] = x;
+        }
+      }
+    }
+    grid_barrier();   // op i+1 reads rows and flags op i wrote
+  }
+  // phase 2: per-op totals of the chunk, one op per block (last_block_sum order)
+  for (int op = c0 + blockIdx.x; op < c1; op += gridDim.x) {
+    const int oi = MODE == kRotate ? op : a.n_ops - 1 - op;
+    const int items = a.ops[oi].ca * a.ops[oi].nx;
+    const double* part = a.part + (op - c0) * a.part_stride;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double x = 0.0;
+      for (int i = threadIdx.x; i < items; i += blockDim.x) x += __ldcg(part + (int64_t)i * NV + q);
+      x = warp_sum(x);
+      __syncthreads();
+      if (l == 0) sh[q][w] = x;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int k = 0; k < 8; ++k) t += sh[q][k];
+        a.red[(int64_t)op * NV + q] = t;
+      }
+    }
+  }
+  grid_barrier();   // totals visible; partial buffers free for the next chunk
+  if (blockIdx.x == 0 && threadIdx.x == 0) {   // norm chain in sweep order
+    double n2 = *a.norm2;
+    for (int op = c0; op < c1; ++op) {
+      const int oi = MODE == kRotate ? op : a.n_ops - 1 - op;
+      const double* tot = a.red + (int64_t)op * NV;
+      const double dold = MODE == kAdjoint ? __ldcg(tot + 1) : __ldcg(tot);
+      const double dnew = MODE == kAdjoint ? __ldcg(tot + 2) : __ldcg(tot + 1);
+      const double n2new = n2 - dold + dnew;
+      const double nrm = sqrt(fmax(n2, 0.0));
+      const double drift = fabs(sqrt(fmax(n2new, 0.0)) - nrm);
+      if (drift > kNormDriftTol * fmax(1.0, nrm)) {   // svengine.py:234-236
+        if (atomicExch(a.err, 1) == 0) *a.err_val = drift;
+      }
+      n2 = n2new;
+      if (MODE == kAdjoint)
+        a.grads[oi] = a.ops[oi].ca > 0 ? 2.0 * __ldcg(tot) : 0.0;
+    }
+    *a.norm2 = n2;
+  }
+  }
+}
+
+// Launch one fused sweep over host op descriptors (MODE kRotate: forward order,
+// kAdjoint: reverse order, gradients to d_grads).
+template <int MODE>
+static int launch_sweep(const hsv_sector_s* sec, const std::vector<SweepOp>& ops_in, double2* psi,
+                        uint32_t* fpsi, double2* lam, uint32_t* flam, double* norm2,
+                        double* d_grads, PairScratch& sc) {
+  if (ops_in.empty()) return HSV_OK;
+  constexpr int NV = MODE == kAdjoint ? 3 : 2;
+  static thread_local std::vector<SweepOp> ops;
+  ops = ops_in;
+  int64_t max_items = 1, n_list = 0;
+  for (SweepOp& o : ops) {
+    max_items = std::max<int64_t>(max_items, (int64_t)o.ca * o.nx);
+    o.la_off = (int32_t)n_list;
+    o.lb_off = (int32_t)(n_list + o.ca);
+    n_list += (int64_t)o.ca + o.cb;
+  }
+  HSV_REQUIRE(n_list < INT32_MAX && max_items < INT32_MAX, HSV_ERR_UNSUPPORTED,
+              "sweep pair lists too long");
+  int2* lists = nullptr;
+  HSV_TRY(dalloc(&lists, std::max<int64_t>(n_list, 1)));
+  // ops per reduction chunk: partials of a chunk stay within 64 MB
+  const int64_t chunk = std::max<int64_t>(
+      1, std::min<int64_t>((int64_t)ops.size(), ((int64_t)8 << 20) / (max_items * NV)));
+  SweepOp* d_ops = nullptr;
+  double *part = nullptr, *red = nullptr;
+  HSV_TRY(dalloc(&d_ops, ops.size()));
+  HSV_TRY(dalloc(&part, chunk * max_items * NV));
+  HSV_TRY(dalloc(&red, (int64_t)ops.size() * NV));
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_ops, ops.data(), ops.size() * sizeof(SweepOp),
+                               cudaMemcpyHostToDevice, stream()));
+  SweepArgs a{};
+  a.ops = d_ops; a.n_ops = (int)ops.size();
+  a.norb = sec->norb; a.n_alpha = sec->n_alpha; a.n_beta = sec->n_beta;
+  a.Nb = sec->Nb; a.Ra = sec->d_Ra; a.Rb = sec->d_Rb; a.binom = sec->d_binom; a.lists = lists;
+  a.psi = psi; a.lam = lam; a.fpsi = fpsi; a.flam = flam;
+  a.part = part; a.part_stride = max_items * NV; a.chunk = (int)chunk; a.red = red;
+  a.norm2 = norm2; a.grads = d_grads; a.err = sc.err; a.err_val = sc.err_val;
+  static int occ[3] = {0, 0, 0};
+  if (!occ[MODE]) {
+    HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[MODE], k_sweep<MODE>, 256, 0));
+    occ[MODE] = std::max(occ[MODE], 1);
+  }
+  // Full residency only when the ops carry enough rows to need the memory
+  // parallelism; small sweeps are barrier bound (cheaper with fewer blocks).
+  const int64_t resident = (int64_t)ctx().num_sms * occ[MODE];
+  const int64_t want = tuning().sweep_grid > 0 ? tuning().sweep_grid
+                       : max_items >= 8 * resident ? resident
+                                                   : std::min<int64_t>(max_items, 2 * ctx().num_sms);
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(resident, want));
+  void* params[] = {&a};
+  {
+    ProfScope prof(MODE == kRotate ? "qeb" : "adjoint");
+    HSV_TRY_CUDA(cudaLaunchCooperativeKernel((const void*)k_sweep<MODE>, dim3((unsigned)grid),
+                                             dim3(256), params, 0, stream()));
+  }
+  count_launch();
+  dfree(d_ops);
+  dfree(part);
+  dfree(red);
+  dfree(lists);
+  return HSV_OK;
+}
+
+static SweepOp sweep_op(const hsv_sector_s* sec, uint64_t occ, uint64_t virt, double c, double s) {
+  const OpMasks m = compress_op(sec, occ, virt);
+  SweepOp o{};
+  o.oa = m.oa; o.va = m.va; o.ob = m.ob; o.vb = m.vb;
+  o.ca = (int32_t)src_count(sec->norb, sec->n_alpha, m.oa, m.va);
+  o.cb = (int32_t)src_count(sec->norb, sec->n_beta, m.ob, m.vb);
+  o.nx = (int32_t)((o.cb + 255) / 256);
+  if (o.ca == 0 || o.cb == 0) o.ca = o.cb = o.nx = 0;
+  o.c = c; o.s = s;
+  return o;
+}
+
 }  // namespace hsv
 
 using namespace hsv;
@@ -385,14 +678,23 @@ int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const 
   PairScratch sc;
   HSV_TRY(sc.init(sec, 2));
   PairLists pl;
-  for (int64_t i = 0; i < k; ++i) {
-    if (cs[i] == 1.0 && sn[i] == 0.0) continue;
-    HSV_TRY(build_pair_lists_async(sec, compress_op(sec, occ[i], virt[i]), pl));
-    PairArgs a{};
-    a.Nb = sec->Nb; a.psi = psi->d_amp; a.c = cs[i]; a.s = sn[i];
-    a.part = sc.part; a.counter = sc.counter; a.norm2 = psi->d_norm2;
-    a.err = sc.err; a.err_val = sc.err_val; a.fpsi = psi->d_arow;
-    HSV_TRY(launch_pairs<kRotate>(pl, a));
+  if (tuning().sweep) {
+    static thread_local std::vector<SweepOp> ops;
+    ops.clear();
+    for (int64_t i = 0; i < k; ++i)
+      if (!(cs[i] == 1.0 && sn[i] == 0.0)) ops.push_back(sweep_op(sec, occ[i], virt[i], cs[i], sn[i]));
+    HSV_TRY(launch_sweep<kRotate>(sec, ops, psi->d_amp, psi->d_arow, nullptr, nullptr,
+                                  psi->d_norm2, nullptr, sc));
+  } else {
+    for (int64_t i = 0; i < k; ++i) {
+      if (cs[i] == 1.0 && sn[i] == 0.0) continue;
+      HSV_TRY(build_pair_lists_async(sec, compress_op(sec, occ[i], virt[i]), pl));
+      PairArgs a{};
+      a.Nb = sec->Nb; a.psi = psi->d_amp; a.c = cs[i]; a.s = sn[i];
+      a.part = sc.part; a.counter = sc.counter; a.norm2 = psi->d_norm2;
+      a.err = sc.err; a.err_val = sc.err_val; a.fpsi = psi->d_arow;
+      HSV_TRY(launch_pairs<kRotate>(pl, a));
+    }
   }
   psi->norm2_valid = psi->arow_valid = true;
   psi->dense_hint = false;
@@ -429,7 +731,14 @@ int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
   PairScratch sc;
   HSV_TRY(sc.init(sec, 3));
   PairLists pl;
-  for (int64_t i = k - 1; i >= 0; --i) {
+  if (tuning().sweep) {
+    static thread_local std::vector<SweepOp> ops;
+    ops.clear();
+    for (int64_t i = 0; i < k; ++i) ops.push_back(sweep_op(sec, occ[i], virt[i], cs[i], sn[i]));
+    HSV_TRY(launch_sweep<kAdjoint>(sec, ops, psi->d_amp, psi->d_arow, w->d_amp, w->d_arow,
+                                   w->d_norm2, d_grad, sc));
+  }
+  for (int64_t i = tuning().sweep ? -1 : k - 1; i >= 0; --i) {
     HSV_TRY(build_pair_lists_async(sec, compress_op(sec, occ[i], virt[i]), pl));
     if (pl.ca == 0 || pl.cb == 0) {
       HSV_TRY_CUDA(cudaMemsetAsync(d_grad + i, 0, sizeof(double), stream()));

@@ -94,7 +94,7 @@ def test_h14_shards_sum_to_full(hsv):
     dim = len(s.basis)
     psi = s1(hsv, s.basis, dim)
     eng = hsv.SvAdaptEngine.__new__(hsv.SvAdaptEngine)
-    eng.basis, eng.matrix, eng._dpools = s.basis, m, {}
+    eng.basis, eng.matrix, eng._dpools, eng._dpool_last = s.basis, m, {}, None
     dp = eng._device_pool(hsv.build_qeb_pool(s.n_qubits, s.integrals.nelec))
     na = s.basis._sector.n_alpha_strings
     full = torch.zeros(2 + dp.n, dtype=torch.float64, device="cuda")

@@ -1,0 +1,71 @@
+"""The fused cooperative sweep (one launch for all k rotations, hsv_qeb.cu
+k_sweep) against the per-op launch path: energies, gradients and the
+forward state bit for bit (same pairs, same reduction order)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hsv():
+    import paper_2604_01176_b200 as hsv
+    return hsv
+
+
+@pytest.fixture()
+def N():
+    from paper_2604_01176_b200 import _native as N
+    yield N
+    N.call("hsv_set_tuning", b"sweep", 1)
+
+
+def eg(N, eng, ops, th, sweep):
+    N.call("hsv_set_tuning", b"sweep", sweep)
+    return eng.energy_and_gradient(ops, th)
+
+
+@pytest.mark.parametrize("name,k", [("h2", 3), ("h4", 12), ("h6", 30), ("h8", 40),
+                                    ("h10", 25), ("h12", 20)])
+def test_sweep_bitwise_equals_per_op(hsv, N, name, k):
+    sysm = hsv.MolecularSystem.bundled(name)
+    eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
+    pool = hsv.build_qeb_pool(sysm.n_qubits, sysm.integrals.nelec)
+    rng = np.random.default_rng(3)
+    for trial in range(2):
+        idx = rng.integers(0, len(pool), size=k)
+        th = rng.uniform(-0.4, 0.4, size=k)
+        th[::5] = 0.0                               # identity rotations are skipped forward
+        ops = [pool.ops[i] for i in idx]
+        e1, g1 = eg(N, eng, ops, th, 1)
+        e0, g0 = eg(N, eng, ops, th, 0)
+        assert e1 == e0
+        assert np.array_equal(g1, g0)
+
+
+def test_sweep_forward_state_and_two_phase(hsv, N):
+    """hsv_eg_forward_async leaves the same psi / w either way."""
+    from paper_2604_01176_b200.svengine import DeviceState
+    sysm = hsv.MolecularSystem.bundled("h8")
+    eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
+    pool = hsv.build_qeb_pool(sysm.n_qubits, sysm.integrals.nelec)
+    rng = np.random.default_rng(8)
+    ops = [pool.ops[i] for i in rng.integers(0, len(pool), size=24)]
+    th = rng.uniform(-0.5, 0.5, size=24)
+    occ, virt = eng._pool_masks(ops)
+    cs, sn = np.cos(th), np.sin(th)
+    na = sysm.basis._sector.n_alpha_strings
+    out = []
+    for sweep in (1, 0):
+        N.call("hsv_set_tuning", b"sweep", sweep)
+        psi, w = DeviceState(sysm.basis), DeviceState(sysm.basis)
+        N.call("hsv_eg_forward_async", eng.matrix.handle, int(sysm.hf.bits), N.ptr_u64(occ),
+               N.ptr_u64(virt), N.ptr_f64(cs), N.ptr_f64(sn), th.size, 0, na, psi.handle,
+               w.handle)
+        N.call("hsv_synchronize")
+        out.append((psi.to_sparse(), w.to_sparse()))
+    (p1, w1), (p0, w0) = out
+    assert np.array_equal(p1.indices, p0.indices) and np.array_equal(p1.values, p0.values)
+    assert np.array_equal(w1.indices, w0.indices) and np.array_equal(w1.values, w0.values)
+    ref = hsv.apply_ansatz(sysm.basis, sysm.hf, ops, th).vec
+    assert np.array_equal(ref.indices, p1.indices) and np.array_equal(ref.values, p1.values)

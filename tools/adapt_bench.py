@@ -29,8 +29,13 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--ks", nargs="+", type=int, default=[20, 100])
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--tune", nargs="*", default=[], help="hsv_set_tuning key=value pairs")
+    ap.add_argument("--no-loop", action="store_true", help="skip the full ADAPT loop")
     args = ap.parse_args()
     N.init(0)
+    for kv in args.tune:
+        key, val = kv.split("=")
+        N.call("hsv_set_tuning", key.encode(), int(val))
     for name in args.systems:
         sysm = hsv.MolecularSystem.bundled(name)
         eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
@@ -43,19 +48,25 @@ def main():
             eng.energy_and_gradient(ops, th)
             N.call("hsv_prof_reset")
             N.call("hsv_prof_enable", 1)
-            t0 = time.perf_counter()
+            walls = []
             for _ in range(args.reps):
+                t0 = time.perf_counter()
                 e, g = eng.energy_and_gradient(ops, th)
-            dt = (time.perf_counter() - t0) / args.reps
+                walls.append(time.perf_counter() - t0)
             N.call("hsv_prof_collect")
             N.call("hsv_prof_enable", 0)
             kern = {}
-            for kn in ("apply", "qeb", "adjoint"):
+            for kn in ("apply", "push", "push_collect", "qeb", "adjoint"):
                 t, c = N.dbl(), N.i64()
                 N.call("hsv_prof_get", kn.encode(), N.C.byref(t), N.C.byref(c))
-                kern[kn] = t.value / args.reps
-            print(json.dumps({"system": name, "k": k, "eval_ms": dt * 1e3,
-                              "kernel_ms_per_eval": kern, "energy": e}), flush=True)
+                kern[kn] = round(t.value / args.reps, 4)
+            print(json.dumps({"system": name, "k": k, "eval_ms": float(np.mean(walls)) * 1e3,
+                              "eval_ms_median": float(np.median(walls)) * 1e3,
+                              "eval_ms_max": float(np.max(walls)) * 1e3,
+                              "kernel_ms_per_eval": kern, "energy": e, "tune": args.tune}),
+                  flush=True)
+        if args.no_loop:
+            continue
         recs = []
         N.call("hsv_prof_reset")
         N.call("hsv_prof_enable", 1)
