@@ -167,11 +167,13 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
         if (__popc(sa & (uint32_t)B.x) != B.y) continue;
         const uint32_t ra2 = __ldg(a.Ra + (sa ^ (uint32_t)B.x));
         if (a.arow && !__ldg(a.arow + ra2)) continue;   // partner alpha row all zero
-        const double2* __restrict__ prow = a.psi + (int64_t)ra2 * a.Nb;
+        // 32-bit row offsets (dim < 2^32, checked at launch) and no record
+        // prefetch: both free registers the compiler otherwise spends on
+        // re-deriving addresses (measured -6.6% at H12)
+        const uint32_t rowoff = ra2 * (uint32_t)a.Nb;
         const Rec<W>* __restrict__ rp = reinterpret_cast<const Rec<W>*>(a.recs);
-        Rec<W> cur = ldrec(rp + B.z);
         for (int g = B.z; g < B.w; ++g) {
-          const Rec<W> nxt = ldrec(rp + (g + 1 < B.w ? g + 1 : g));   // prefetch
+          const Rec<W> cur = ldrec(rp + g);
           const uint32_t xb = cur.xb;
           const int hb = (int)(cur.meta & 0xffu);
           unsigned v = 0u;
@@ -188,13 +190,12 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
               const double amp = __hiloint2double(__double2hiint(A) ^ sgn, __double2loint(A));
               if ((v >> k) & 1u) {
                 const uint32_t rk = __ldg(a.Rb + (uint32_t)(sb[k] ^ xb));
-                const double2 p = prow[rk];
+                const double2 p = a.psi[rowoff + rk];
                 acc[k].x = fma(amp, p.x, acc[k].x);
                 acc[k].y = fma(amp, p.y, acc[k].y);
               }
             }
           }
-          cur = nxt;
         }
       }
       // pass 2: remaining groups, sequential term loop in reference order
@@ -203,7 +204,7 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
         if (__popc(sa & (uint32_t)B.x) != B.y) continue;
         const uint32_t ra2 = __ldg(a.Ra + (sa ^ (uint32_t)B.x));
         if (a.arow && !__ldg(a.arow + ra2)) continue;
-        const double2* __restrict__ prow = a.psi + (int64_t)ra2 * a.Nb;
+        const uint32_t rowoff = ra2 * (uint32_t)a.Nb;
         for (int g = B.z; g < B.w; ++g) {
           const int4 G = __ldg(a.groups + g);
           const uint32_t xb = (uint32_t)G.x;
@@ -215,19 +216,39 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
           double amp[R];
 #pragma unroll
           for (int k = 0; k < R; ++k) amp[k] = 0.0;
-          for (int t = G.z; t < G.w; ++t) {
-            const double c = __ldg(&a.terms[t].c);
-            const W z = (W)__ldg(&a.terms[t].z);
+          const uint64_t gz = __ldg(a.gsz + g);
+          if (gz >> 63) {   // single-Z group: one shift + one LOP per term and row
+            const SzTerm* __restrict__ sz = reinterpret_cast<const SzTerm*>(a.szt);
+            for (int t = G.z; t < G.w; ++t) {
+              const uint4 q = __ldg(reinterpret_cast<const uint4*>(sz + t));
+              const int chi = (int)q.y;
 #pragma unroll
-            for (int k = 0; k < R; ++k) {
-              const int sgn = popc(s[k] & z) << 31;   // exact +-c: flip the sign bit
-              amp[k] += __hiloint2double(__double2hiint(c) ^ sgn, __double2loint(c));
+              for (int k = 0; k < R; ++k) {
+                const uint32_t sb31 = SH == 16 ? ((uint32_t)s[k] << q.z) & q.w
+                                               : ((uint32_t)(s[k] >> q.z) << 31) & q.w;
+                amp[k] += __hiloint2double(chi ^ (int)sb31, (int)q.x);
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < R; ++k) {   // common sign (-1)^popc(s & z0): exact
+              const int sgn = popc(s[k] & (W)gz) << 31;
+              amp[k] = __hiloint2double(__double2hiint(amp[k]) ^ sgn, __double2loint(amp[k]));
+            }
+          } else {
+            for (int t = G.z; t < G.w; ++t) {
+              const double c = __ldg(&a.terms[t].c);
+              const W z = (W)__ldg(&a.terms[t].z);
+#pragma unroll
+              for (int k = 0; k < R; ++k) {
+                const int sgn = popc(s[k] & z) << 31;   // exact +-c: flip the sign bit
+                amp[k] += __hiloint2double(__double2hiint(c) ^ sgn, __double2loint(c));
+              }
             }
           }
 #pragma unroll
           for (int k = 0; k < R; ++k) {
             if ((v >> k) & 1u) {
-              const double2 p = prow[__ldg(a.Rb + (sb[k] ^ xb))];
+              const double2 p = a.psi[rowoff + __ldg(a.Rb + (sb[k] ^ xb))];
               acc[k].x = fma(amp[k], p.x, acc[k].x);
               acc[k].y = fma(amp[k], p.y, acc[k].y);
             }
@@ -347,8 +368,12 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   a.buckets = op->d_buckets; a.n_buckets = (int)op->n_buckets;
   a.groups = op->d_groups; a.terms = op->d_terms; a.diag = op->d_diag;
   a.tabs = op->d_tabs; a.recs = op->d_recs; a.n_buckets_h = (int)op->n_buckets_h;
+  a.gsz = op->d_gsz; a.szt = op->d_szt;
   a.psi = psi; a.out = out; a.epart = epart;
   a.Nb = s->Nb; a.a_lo = a_lo; a.a_hi = a_hi; a.prune = prune; a.energy_only = energy_only;
+  HSV_REQUIRE(s->dim < ((int64_t)1 << 32), HSV_ERR_UNSUPPORTED,
+              "sector dimension %lld exceeds the 32-bit row index of the apply kernel",
+              (long long)s->dim);
   if (tuning().push != 0) {   // sparse psi: scatter + sort-reduce (hsv_push.cu)
     bool done = false;
     HSV_TRY(launch_push(op, a, &done, n_warps, dense_hint));
@@ -661,6 +686,43 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
     ghash = nh;
     op->n_buckets = (int64_t)nb.size();
   }
+  // single-Z form of the term-loop groups (see SzTerm)
+  std::vector<uint64_t> gsz(op->groups.size(), 0ull);
+  std::vector<SzTerm> szt(op->terms.size(), SzTerm{0.0, 0u, 0u});
+  for (const int4& B : op->buckets) {
+    for (int q = B.z; q < B.w; ++q) {
+      if (ghash[q].tab >= 0) continue;
+      const int4 G = op->groups[q];
+      const uint64_t xp = (uint64_t)(uint32_t)B.x | ((uint64_t)(uint32_t)G.x << SH);
+      const int fixed = (B.y + G.y) & 1;   // parity(s & xp) on in-sector rows
+      // reference z: a term every other term differs from by <= 1 bit off the
+      // flip mask (the term without an extra number-operator Z)
+      auto fits = [&](uint64_t zr) {
+        for (int t = G.z; t < G.w; ++t) {
+          const uint64_t d = op->terms[t].z ^ zr, dx = d & xp;
+          if (!(dx == 0 || dx == xp) || __builtin_popcountll(d & ~xp) > 1) return false;
+        }
+        return true;
+      };
+      uint64_t z0 = 0;
+      bool ok = false;
+      for (int t = G.z; !ok && t < G.w; ++t)
+        if (fits(op->terms[t].z)) { z0 = op->terms[t].z; ok = true; }
+      ok = ok && (z0 >> 63) == 0;
+      for (int t = G.z; ok && t < G.w; ++t) {
+        const uint64_t d = op->terms[t].z ^ z0, dx = d & xp, dout = d & ~xp;
+        ok = (dx == 0 || dx == xp) && __builtin_popcountll(dout) <= 1;
+        if (!ok) break;
+        const int r = dout ? __builtin_ctzll(dout) : 0;
+        const double c = (dx == xp && fixed) ? -op->terms[t].c : op->terms[t].c;
+        szt[t] = SzTerm{c, (uint32_t)(SH == 16 ? 31 - r : r), dout ? 0x80000000u : 0u};
+      }
+      if (ok) {
+        gsz[q] = (1ull << 63) | z0;
+        ++op->n_single_z;
+      }
+    }
+  }
   // bucket split boundaries (S = 2, 4, 8) balancing an estimated per-group cost
   std::vector<int> splits;
   {
@@ -712,9 +774,16 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
       (rc = dalloc(&op->d_terms, op->terms.size())) ||
       (rc = dalloc(&op->d_ghash, ghash.size())) || (rc = dalloc(&op->d_tabs, tabs.size())) ||
       (rc = dalloc(reinterpret_cast<unsigned char**>(&op->d_recs), recs.size())) ||
-      (rc = dalloc(&op->d_splits, splits.size())))
+      (rc = dalloc(&op->d_splits, splits.size())) || (rc = dalloc(&op->d_gsz, gsz.size())) ||
+      (rc = dalloc(reinterpret_cast<SzTerm**>(&op->d_szt), szt.size())))
     return fail(rc);
   cudaStream_t st = stream();
+  if (!gsz.empty())
+    HSV_TRY_CUDA(cudaMemcpyAsync(op->d_gsz, gsz.data(), gsz.size() * sizeof(uint64_t),
+                                 cudaMemcpyHostToDevice, st));
+  if (!szt.empty())
+    HSV_TRY_CUDA(cudaMemcpyAsync(op->d_szt, szt.data(), szt.size() * sizeof(SzTerm),
+                                 cudaMemcpyHostToDevice, st));
   HSV_TRY_CUDA(cudaMemcpyAsync(op->d_splits, splits.data(), splits.size() * sizeof(int),
                                cudaMemcpyHostToDevice, st));
   if (!recs.empty())
@@ -750,6 +819,8 @@ int hsv_op_destroy(hsv_op op) {
   dfree(op->d_tabs);
   dfree(reinterpret_cast<unsigned char*>(op->d_recs));
   dfree(op->d_splits);
+  dfree(op->d_gsz);
+  dfree(reinterpret_cast<SzTerm*>(op->d_szt));
   delete op;
   return HSV_OK;
 }

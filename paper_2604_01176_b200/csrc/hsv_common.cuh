@@ -162,6 +162,12 @@ struct hsv_op_s {
   int* d_splits = nullptr;      // bucket boundaries for 2, 4, 8 splits: 3 + 5 + 9 ints
   double* d_tabs = nullptr;
   int64_t n_hashed = 0;
+  // term-loop groups whose terms differ from the first only by the flip
+  // pattern and at most one extra Z ("single-Z" form, the singles):
+  // d_gsz[g] = 1<<63 | z0 (0: generic loop), d_szt[t] per term
+  uint64_t* d_gsz = nullptr;
+  void* d_szt = nullptr;
+  int64_t n_single_z = 0;
   // host copies of the active group table (for CSR materialization)
   std::vector<int4> buckets, groups;
   std::vector<Term> terms;

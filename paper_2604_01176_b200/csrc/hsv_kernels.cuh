@@ -33,6 +33,8 @@ struct ApplyArgs {
   const double* diag;
   const GroupHash* ghash;
   const double* tabs;
+  const uint64_t* gsz;     // per group: 1<<63 | z0 for single-Z groups, else 0
+  const void* szt;         // SzTerm per term (single-Z groups)
   const double2* psi;
   const uint32_t* arow;  // alpha-row occupancy of psi (skip empty partner rows) or nullptr
   double2* out;      // nullptr: energy only
@@ -70,6 +72,17 @@ __device__ __forceinline__ Rec<W> ldrec(const Rec<W>* p) {
   for (int i = 0; i < (int)(sizeof(Rec<W>) / 16); ++i) d[i] = __ldg(q + i);
   return r;
 }
+
+// Term of a single-Z group: z_t = z_0 ^ (0 or the whole flip mask) ^ (0 or one
+// bit r).  For in-sector rows parity(s & flip) is fixed, so
+//   (-1)^popc(s & z_t) c_t = (-1)^popc(s & z_0) * (-1)^{s_r} c'_t,
+// c'_t = c_t with that fixed sign folded in; the sign bit of term t is
+// (s << sh) & fm for 32-bit rows (sh = 31 - r), ((s >> sh) << 31) & fm for
+// 64-bit rows (sh = r); fm = 0 when z_t has no extra Z.
+struct __align__(16) SzTerm {
+  double c;
+  uint32_t sh, fm;
+};
 
 // Matrix element of an x-local group at row s: (-1)^popc(s & z0) * A[h(s & x)].
 template <typename W>
