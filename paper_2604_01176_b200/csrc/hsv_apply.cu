@@ -124,34 +124,42 @@ __global__ void k_csr_rows(const uint32_t* __restrict__ Sa, const uint32_t* __re
 template <typename W, int SH, int R, int MINB>
 __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
   const int lane = threadIdx.x & 31;
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t tw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // 32-bit indices throughout (dim < 2^32 is checked at launch): fewer
+  // registers and integer instructions than 64-bit row arithmetic
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t tw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t units = (uint32_t)a.units, Nb = (uint32_t)a.Nb;
   double er = 0.0, ei = 0.0;
-  // Static schedule.  Contiguous unit blocks per warp keep a warp on one alpha
-  // row (L1 reuse) and win while psi fits in L2; interleaved units keep all warps
-  // on neighbouring alpha rows so the partner rows they gather stay in L2 when
-  // psi is far larger than L2 (H14/H16).
-  const int64_t u_begin = a.interleave ? gw : gw * a.units / tw;
-  const int64_t u_end = a.interleave ? a.units : (gw + 1) * a.units / tw;
-  const int64_t u_step = a.interleave ? tw : 1;
-  for (int64_t uw = u_begin; uw < u_end; uw += u_step) {
-    // a work unit = (row unit, bucket split); splits > 1 only when row units are scarce
-    const int64_t u = uw / a.nsplit;
-    const int sp = (int)(uw - u * a.nsplit);
+  // Static schedule.  Interleaved (default): warp gw takes work units gw,
+  // gw + tw, ..., so the warps of an SM work on neighbouring row units of one
+  // alpha row and the same bucket range at the same time and share the partner
+  // rows they gather in L1 (and in L2 when psi is far larger than L2).
+  // Contiguous unit blocks per warp remain as a tuning alternative.
+  const uint32_t u_begin = a.interleave ? gw : (uint32_t)((uint64_t)gw * units / tw);
+  const uint32_t u_end = a.interleave ? units : (uint32_t)((uint64_t)(gw + 1) * units / tw);
+  const uint32_t u_step = a.interleave ? tw : 1u;
+  for (uint32_t uw = u_begin; uw < u_end; uw += u_step) {
+    // a work unit = (row unit, bucket split), split-major: neighbouring work
+    // units are neighbouring row units with the same bucket range (measured
+    // -6% at H12 against unit-major)
+    const uint32_t units1 = units / (uint32_t)a.nsplit;
+    const int sp = (int)(uw / units1);
+    const uint32_t u = uw - (uint32_t)sp * units1;
     const int bk0 = a.nsplit > 1 ? __ldg(a.split_bk + sp) : 0;
     const int bk1 = a.nsplit > 1 ? __ldg(a.split_bk + sp + 1) : a.n_buckets;
-    const int64_t ra = a.a_lo + u / a.upr;
-    const int64_t rb0 = (u % a.upr) * (32 * R) + lane;
+    const uint32_t ur = u / (uint32_t)a.upr;
+    const uint32_t ra = (uint32_t)a.a_lo + ur;
+    const uint32_t rb0 = (u - ur * (uint32_t)a.upr) * (32 * R) + lane;
     const uint32_t sa = __ldg(a.Sa + ra);
-    const int64_t rowbase = ra * a.Nb;
+    const uint32_t rowbase = ra * Nb;
     W s[R];
     uint32_t sb[R];
     double2 acc[R];
     unsigned live = 0u;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      const int64_t rb = rb0 + k * 32;
-      const bool inr = rb < a.Nb;
+      const uint32_t rb = rb0 + k * 32;
+      const bool inr = rb < Nb;
       sb[k] = inr ? __ldg(a.Sb + rb) : 0u;
       s[k] = (W)sa | ((W)sb[k] << SH);
       const double2 pv = inr ? a.psi[rowbase + rb] : make_double2(0.0, 0.0);
@@ -258,11 +266,11 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      const int64_t rb = rb0 + k * 32;
-      if (rb >= a.Nb) continue;
+      const uint32_t rb = rb0 + k * 32;
+      if (rb >= Nb) continue;
       if (a.out) {
         if (a.nsplit > 1) {   // partial row, combined in split order by k_combine_splits
-          a.ypart[sp * a.part_stride + (rowbase + rb - a.a_lo * a.Nb)] = acc[k];
+          a.ypart[(int64_t)sp * a.part_stride + (rowbase + rb - (uint32_t)a.a_lo * Nb)] = acc[k];
         } else {
           double2 y = acc[k];
           if (a.prune > 0.0 && sqrt(y.x * y.x + y.y * y.y) < a.prune) y = make_double2(0.0, 0.0);
@@ -320,9 +328,9 @@ static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
   if (!a0.split_bk) S = 1;
   a.nsplit = S;
   a.split_bk = S == 1 ? nullptr : a0.split_bk + (S == 2 ? 0 : S == 4 ? 3 : 8);
-  // psi well inside L2 (126 MB): contiguous; otherwise interleaved (measured)
+  // interleaved unless forced off (measured best at H12 and H14)
   const int il = tuning().apply_interleave;   // -1 auto, 0 off, 1 on
-  a.interleave = il == 1 || (il < 0 && a0.dim_bytes > ((int64_t)64 << 20));
+  a.interleave = il != 0;
   a.units = units1 * S;
   int64_t grid = max_warps / 8;
   const int64_t need = (a.units + 7) / 8;
@@ -394,6 +402,7 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   if (R == 4) return launch_apply_t<W, SH, 4, 3>(a, n_warps);              \
   if (M == 3) return launch_apply_t<W, SH, 2, 3>(a, n_warps);              \
   if (M == 5) return launch_apply_t<W, SH, 2, 5>(a, n_warps);              \
+  if (M == 6) return launch_apply_t<W, SH, 2, 6>(a, n_warps);              \
   return launch_apply_t<W, SH, 2, 4>(a, n_warps);
   if (s->wide) { HSV_APPLY_CASES(uint64_t, 32) }
   HSV_APPLY_CASES(uint32_t, 16)

@@ -11,7 +11,7 @@ struct Tuning {
                           // alternatives R=2: 3 or 5, R=4: 2
   int screen_rows = 1024; // rows staged per chunk in the screen kernel
   int apply_split = 0;    // bucket splits per row unit in K1 (0 = auto, else 1/2/4/8)
-  int apply_interleave = -1;  // K1 unit schedule: -1 auto (psi > 64 MB), 0 contiguous, 1 interleaved
+  int apply_interleave = -1;  // K1 unit schedule: -1 auto (= interleaved), 0 contiguous, 1 interleaved
   int push = -1;          // sparse-psi push path: -1 auto, 0 off, 1 whenever it fits in memory
   int push_keys = 32;
   int sweep = 1;          // adjoint/forward sweeps: 1 one cooperative launch, 0 launch per op
