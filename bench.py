@@ -147,6 +147,20 @@ def step_roofline(sysm, ops, nnz, dim, ms, hbm):
             "unit": "GB/s"}
 
 
+def collective_elapsed(t0):
+    """Seconds since t0, maximised over ranks: loop exits decided on it are
+    identical on every rank (a rank-local decision can desynchronise the
+    collectives of the ranks)."""
+    import torch
+    import torch.distributed as dist
+    el = time.perf_counter() - t0
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        t = torch.tensor([el], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        el = float(t.item())
+    return el
+
+
 def cpu_reference(sysm, psi, steps, warmup):
     """Reference CPU algorithm (oracle port) on a bounded sample: mean seconds per
     extrapolated step over `steps` timed samples (after `warmup` untimed ones)."""
@@ -270,7 +284,7 @@ def run_hsv(args):
             for _ in range(args.warmup):
                 step_device()
             barrier()
-            if time.perf_counter() - t_w > 0.5:
+            if collective_elapsed(t_w) > 0.5:   # same decision on every rank
                 break
         N.lib().hsv_launch_count(1)
         N.call("hsv_prof_reset")

@@ -323,7 +323,8 @@ static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
   int S = tuning().apply_split;
   if (S <= 0) {
     S = 1;
-    while (S < 8 && units1 * S < 8 * max_warps) S *= 2;
+    // at most 4: S = 8 never won (H12 full / half / quarter shards, kbench)
+    while (S < 4 && units1 * S < 8 * max_warps) S *= 2;
   }
   if (!a0.split_bk) S = 1;
   a.nsplit = S;
