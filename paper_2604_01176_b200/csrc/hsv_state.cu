@@ -324,7 +324,8 @@ int hsv_state_set_sparse(hsv_state st, const int64_t* pos, const double* re, con
     dfree(d_bad);
   }
   st->arow_valid = false;
-  st->dense_hint = false;
+  // more than dim/8 entries is always past the push path's budget: skip its probe
+  st->dense_hint = n > st->sec->dim / 8;
   HSV_TRY(state_norm2_async(st));
   HSV_TRY(stream_sync());
   HSV_REQUIRE(!h_bad, HSV_ERR_INVALID, "position out of range for dimension %lld",
@@ -361,7 +362,7 @@ int hsv_state_set_keys(hsv_state st, const uint64_t* keys, const double* re, con
     dfree(d_i);
   }
   st->arow_valid = false;
-  st->dense_hint = false;
+  st->dense_hint = n > st->sec->dim / 8;
   HSV_TRY(state_norm2_async(st));
   return stream_sync();
 }
