@@ -10,6 +10,7 @@ rank order, so the result is deterministic for a fixed world size.
 """
 from __future__ import annotations
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -96,6 +97,15 @@ class DistributedSvAdaptEngine:
         self._psi = DeviceState(self.basis)
         self._w = DeviceState(self.basis)
         self._screens = {}
+        # Sparse states (early ADAPT) take the K1 push path, whose cost is a few
+        # launches and host syncs: there every rank computes all rows itself and
+        # nothing is exchanged (replicas), which beats owner-computes + NCCL.
+        # The switch uses nnz(psi), identical on every rank, so ranks stay in
+        # lock step; cap = the library's push budget (hsv_push.cu).
+        dim = self.na * self.nb
+        groups = self.matrix.info()["n_active_groups"]
+        self.replica_nnz = max(0, (32 * dim - (1 << 20)) // (1 + groups))
+        self._last_nnz = 1                            # HF
 
     def initial_state(self):
         return self.inner.initial_state()
@@ -118,7 +128,13 @@ class DistributedSvAdaptEngine:
             self._screens[key] = ShardedEnergyScreen(self.inner, key, self.rank, self.world)
         return self._screens[key]
 
+    def replicated(self, nnz: int) -> bool:
+        return nnz <= self.replica_nnz
+
     def energy_and_screen(self, state, pool):
+        if self.replicated(state.nnz):            # whole sector on every rank, no exchange
+            return self.inner.energy_and_screen(state, pool) if len(pool) else \
+                (self.inner.energy(state), np.zeros(0))
         sc = self._screen(pool)
         sc.launch(state)
         tot = gather_and_combine(sc.partial, self.group)
@@ -136,10 +152,16 @@ class DistributedSvAdaptEngine:
         occ, virt = self.inner._pool_masks(ops)
         th = np.ascontiguousarray(thetas, dtype=np.float64)
         cs, sn = N.as_f64(np.cos(th)), N.as_f64(np.sin(th))
+        # replica mode is predicted from the previous evaluation's nnz(psi); the
+        # ansatz grows by one operator per ADAPT iteration, so the support grows slowly
+        rep = self.replicated(self._last_nnz)
+        lo, hi = (0, self.na) if rep else (self.a_lo, self.a_hi)
         N.call("hsv_eg_forward_async", self.matrix.handle, int(self.system.hf.bits),
                N.ptr_u64(occ), N.ptr_u64(virt), N.ptr_f64(cs), N.ptr_f64(sn), th.size,
-               self.a_lo, self.a_hi, self._psi.handle, self._w.handle)
-        allgather_rows(self._w.torch_view(), self.na, self.nb, self.group)
+               lo, hi, self._psi.handle, self._w.handle)
+        if not rep:
+            allgather_rows(self._w.torch_view(), self.na, self.nb, self.group)
+        self._last_nnz = self._psi.nnz()
         g = np.empty(th.size)
         e = N.dbl()
         N.call("hsv_eg_backward", self.matrix.handle, self._psi.handle, self._w.handle,

@@ -45,13 +45,22 @@ def main():
         th = rng.uniform(-0.3, 0.3, 12)
         ops = [pool.ops[i] for i in idx]
         e1, g1 = se.energy_and_gradient(ops, th)
-        e2, g2 = de.energy_and_gradient(ops, th)
         st = se.rebuild(ops, th)
         s1 = se.screen(st, pool)
-        s2 = de.screen(st, pool)
         gmax = max(1.0, float(np.max(np.abs(g1))))
-        res = {"dE": abs(e1 - e2), "dG": float(np.max(np.abs(g1 - g2))) / gmax,
-               "dScreen": float(np.max(np.abs(s1 - s2))) / max(1.0, float(np.max(np.abs(s1))))}
+        res = {}
+        cap_default = de.replica_nnz
+        # both multi-GPU modes: replicas (sparse psi) and owner-computes + NCCL
+        for mode, cap in (("", cap_default), ("_sharded", -1)):
+            de.replica_nnz = cap
+            de._last_nnz = 1
+            de.energy_and_gradient(ops, th)           # sets the mode predictor
+            e2, g2 = de.energy_and_gradient(ops, th)
+            s2 = de.screen(st, pool)
+            res["dE" + mode] = abs(e1 - e2)
+            res["dG" + mode] = float(np.max(np.abs(g1 - g2))) / gmax
+            res["dScreen" + mode] = float(np.max(np.abs(s1 - s2))) / max(1.0, float(np.max(np.abs(s1))))
+        de.replica_nnz = cap_default
         t0 = time.perf_counter()
         ra = hsv.run_adapt(hsv.AdaptConfig(engine="sv", eps_grad=1e-6, max_iter=args.iters), s,
                            engine=de)
@@ -61,7 +70,8 @@ def main():
         res["adapt_dE"] = float(max(abs(a.energy - b.energy) for a, b in zip(ra.records, rb.records)))
         res["adapt_same_ops"] = [a.selected_op for a in ra.records] == [b.selected_op for b in rb.records]
         res["adapt_s_dist"] = t_d
-        res["ok"] = bool(res["dE"] <= 1e-11 and res["dG"] <= 1e-10 and res["dScreen"] <= 1e-10
+        res["ok"] = bool(all(res["dE" + m] <= 1e-11 and res["dG" + m] <= 1e-10
+                             and res["dScreen" + m] <= 1e-10 for m in ("", "_sharded"))
                          and res["adapt_dE"] <= 1e-8 and res["adapt_same_ops"])
         ok &= res["ok"]
         out[name] = res
