@@ -129,7 +129,9 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t tw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t units = (uint32_t)a.units, Nb = (uint32_t)a.Nb;
-  double er = 0.0, ei = 0.0;
+  // energy partials live in shared memory, not in registers across the group loop
+  __shared__ double esh[8][2];
+  if (lane == 0) { esh[threadIdx.x >> 5][0] = 0.0; esh[threadIdx.x >> 5][1] = 0.0; }
   // Static schedule.  Interleaved (default): warp gw takes work units gw,
   // gw + tw, ..., so the warps of an SM work on neighbouring row units of one
   // alpha row and the same bucket range at the same time and share the partner
@@ -277,20 +279,29 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
           a.out[rowbase + rb] = y;
         }
       }
-      if (a.epart && ((live >> k) & 1u)) {
-        const double2 pv = a.psi[rowbase + rb];
-        er += pv.x * acc[k].x + pv.y * acc[k].y;
-        ei += pv.x * acc[k].y - pv.y * acc[k].x;
+    }
+    if (a.epart) {   // this unit's <psi|H psi> share, added in unit order (fixed)
+      double er = 0.0, ei = 0.0;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        const uint32_t rb = rb0 + k * 32;
+        if (rb < Nb && ((live >> k) & 1u)) {
+          const double2 pv = a.psi[rowbase + rb];
+          er += pv.x * acc[k].x + pv.y * acc[k].y;
+          ei += pv.x * acc[k].y - pv.y * acc[k].x;
+        }
+      }
+      er = warp_sum(er);
+      ei = warp_sum(ei);
+      if (lane == 0) {
+        esh[threadIdx.x >> 5][0] += er;
+        esh[threadIdx.x >> 5][1] += ei;
       }
     }
   }
-  if (a.epart) {
-    er = warp_sum(er);
-    ei = warp_sum(ei);
-    if (lane == 0) {
-      a.epart[2 * gw] = er;
-      a.epart[2 * gw + 1] = ei;
-    }
+  if (a.epart && lane == 0) {
+    a.epart[2 * gw] = esh[threadIdx.x >> 5][0];
+    a.epart[2 * gw + 1] = esh[threadIdx.x >> 5][1];
   }
 }
 
