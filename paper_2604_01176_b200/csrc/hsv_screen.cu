@@ -70,7 +70,11 @@ __global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
     double g = 0.0;
     const uint32_t ra2 = (as || at) ? __ldg(a.Ra + (sa ^ fa)) : 0u;
     if ((as || at) && !w_zero && !(a.psi_arow && !__ldg(a.psi_arow + ra2))) {
-      const double2* __restrict__ prow = a.psi + (int64_t)ra2 * a.Nb;
+      // 32-bit row offsets (dim < 2^32, checked by K1) and two list entries per
+      // lane in flight: independent gathers instead of one latency per entry
+      // (0.87 -> 0.76 ms at H12)
+      const uint32_t poff = ra2 * (uint32_t)a.Nb;
+      const double2* __restrict__ prow = a.psi + poff;
       const int2 L = __ldg(a.opl + op);
       if (L.y < 0) {
         // empty beta half: every beta string is both source and target (alpha decides)
@@ -78,16 +82,32 @@ __global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
         if (!at) g = -g;
       } else {
         const int2* __restrict__ lst = a.blist + L.x;
-        if (as)   // own rows in source pattern: (T psi)_b = -psi_p
-          for (int j = lane; j < L.y; j += 32) {
-            const int2 e = __ldg(lst + j);
-            g -= re_conj_mul(wrow[e.x], prow[e.y]);
+        // own rows in source pattern: (T psi)_b = -psi_p; in target pattern: +psi_p
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+          if (!(side == 0 ? as : at)) continue;
+          double g4[4] = {0.0, 0.0, 0.0, 0.0};
+          int j = lane;
+          for (; j + 32 < L.y; j += 64) {   // 2 in flight: 36 registers (4: 54, 8: spills)
+            int2 e[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) e[q] = __ldg(lst + j + 32 * q);
+            double2 wv[2], pv[2];
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              wv[q] = wrow[side == 0 ? e[q].x : e[q].y];
+              pv[q] = prow[side == 0 ? e[q].y : e[q].x];
+            }
+#pragma unroll
+            for (int q = 0; q < 2; ++q) g4[q] += re_conj_mul(wv[q], pv[q]);
           }
-        if (at)   // own rows in target pattern: (T psi)_b = +psi_p
-          for (int j = lane; j < L.y; j += 32) {
+          for (; j < L.y; j += 32) {
             const int2 e = __ldg(lst + j);
-            g += re_conj_mul(wrow[e.y], prow[e.x]);
+            g4[0] += re_conj_mul(wrow[side == 0 ? e.x : e.y], prow[side == 0 ? e.y : e.x]);
           }
+          const double s4 = (g4[0] + g4[1]) + (g4[2] + g4[3]);
+          g = side == 0 ? g - s4 : g + s4;
+        }
       }
     }
     g = warp_sum(g);
