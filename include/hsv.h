@@ -194,6 +194,11 @@ HSV_API int hsv_energy_screen_pool_async(hsv_op op, hsv_state psi, hsv_pool pool
 /* synchronous full-range variant with host outputs */
 HSV_API int hsv_energy_screen_pool(hsv_op op, hsv_state psi, hsv_pool pool, double* energy,
                                    double* grads);
+/* d_out[j] = sum over i in ascending order of d_in[i * n_cols + j] (DEVICE
+ * pointers, one launch, no host synchronization): combines the per-rank
+ * partials all-gathered by NCCL in rank order, as the reference concatenates
+ * row blocks in worker order (sparse.py:199-201). */
+HSV_API int hsv_sum_rows_async(const double* d_in, int64_t n_rows, int64_t n_cols, double* d_out);
 
 /* ---- tuning knobs: "apply_r" (rows per lane, 1/2/4), "screen_rows" ---- */
 HSV_API int hsv_set_tuning(const char* key, int64_t value);

@@ -87,6 +87,7 @@ _SIGNATURES = {
     "hsv_pool_destroy": (C.c_int, [vp]),
     "hsv_energy_screen_pool_async": (C.c_int, [vp, vp, vp, i64, i64, vp]),
     "hsv_energy_screen_pool": (C.c_int, [vp, vp, vp, P_dbl, P_dbl]),
+    "hsv_sum_rows_async": (C.c_int, [vp, i64, i64, vp]),
     "hsv_set_tuning": (C.c_int, [C.c_char_p, i64]),
     "hsv_prof_enable": (C.c_int, [C.c_int]),
     "hsv_prof_collect": (C.c_int, []),

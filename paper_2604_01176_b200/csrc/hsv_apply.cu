@@ -334,8 +334,11 @@ static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
   int S = tuning().apply_split;
   if (S <= 0) {
     S = 1;
-    // at most 4: S = 8 never won (H12 full / half / quarter shards, kbench)
+    // at most 4 (S = 8 lost on the H12 full / half / quarter shards), unless even
+    // S = 4 leaves fewer than two units per warp (H12 eighth shard: S = 8 0.48 ms
+    // against S = 4 0.54 ms; kbench --shard 8)
     while (S < 4 && units1 * S < 8 * max_warps) S *= 2;
+    if (units1 * S < 2 * max_warps) S = 8;
   }
   if (!a0.split_bk) S = 1;
   a.nsplit = S;

@@ -218,6 +218,23 @@ int hsv_synchronize(void) {
   return stream_sync();
 }
 
+int hsv_sum_rows_async(const double* d_in, int64_t n_rows, int64_t n_cols, double* d_out) {
+  HSV_TRY(ensure_init());
+  HSV_REQUIRE(n_rows >= 0 && n_cols >= 0 && (n_cols == 0 || (d_in && d_out)), HSV_ERR_INVALID,
+              "bad argument");
+  if (n_cols == 0) return HSV_OK;
+  if (n_rows == 0) {
+    HSV_TRY_CUDA(cudaMemsetAsync(d_out, 0, n_cols * sizeof(double), stream()));
+    return HSV_OK;
+  }
+  // one chunk: ((0 + row 0) + row 1) + ... per column, the rank-order sum
+  dim3 grid((unsigned)((n_cols + 127) / 128), 1);
+  k_colsum_seq<<<grid, 128, 0, stream()>>>(d_in, n_rows, n_cols, n_cols, n_rows, d_out);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  return HSV_OK;
+}
+
 // ---------------------------------------------------------------- sector
 int hsv_sector_create(int n_qubits, int n_alpha, int n_beta, int ordering, hsv_sector* out) {
   HSV_TRY(ensure_init());
