@@ -200,7 +200,11 @@ HSV_API int hsv_energy_screen_pool(hsv_op op, hsv_state psi, hsv_pool pool, doub
  * row blocks in worker order (sparse.py:199-201). */
 HSV_API int hsv_sum_rows_async(const double* d_in, int64_t n_rows, int64_t n_cols, double* d_out);
 
-/* ---- tuning knobs: "apply_r" (rows per lane, 1/2/4), "screen_rows" ---- */
+/* ---- tuning knobs (defaults are the measured best): "apply_r" (rows per
+ * lane 0/1/2/4), "apply_minb", "apply_split" (0/1/2/4/8), "apply_interleave"
+ * (-1/0/1), "screen_rows", "push" (-1 auto, 0 pull only, 1 push whenever it
+ * fits), "push_keys" (push budget factor), "sweep" (1 fused cooperative
+ * sweeps, 0 one launch per rotation), "sweep_grid" (0 auto) ---- */
 HSV_API int hsv_set_tuning(const char* key, int64_t value);
 
 /* ---- live kernel timing (CUDA events on the launch stream) ---- */
