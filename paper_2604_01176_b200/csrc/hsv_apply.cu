@@ -320,6 +320,11 @@ __global__ void k_combine_splits(const double2* __restrict__ part, int S, int64_
   out[i] = y;
 }
 
+void launch_combine_splits(const double2* part, int S, int64_t rows, double2* out, double prune) {
+  k_combine_splits<<<(unsigned)((rows + 255) / 256), 256, 0, stream()>>>(part, S, rows, out,
+                                                                           prune);
+}
+
 template <typename W, int SH, int R, int MINB>
 static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
   ApplyArgs a = a0;
@@ -391,7 +396,7 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   a.buckets = op->d_buckets; a.n_buckets = (int)op->n_buckets;
   a.groups = op->d_groups; a.terms = op->d_terms; a.diag = op->d_diag;
   a.tabs = op->d_tabs; a.recs = op->d_recs; a.n_buckets_h = (int)op->n_buckets_h;
-  a.gsz = op->d_gsz; a.szt = op->d_szt;
+  a.gsz = op->d_gsz; a.szt = op->d_szt; a.gxa = op->d_gxa; a.g_hashed = (int)op->g_hashed;
   a.psi = psi; a.out = out; a.epart = epart;
   a.Nb = s->Nb; a.a_lo = a_lo; a.a_hi = a_hi; a.prune = prune; a.energy_only = energy_only;
   HSV_REQUIRE(s->dim < ((int64_t)1 << 32), HSV_ERR_UNSUPPORTED,
@@ -400,6 +405,11 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   if (tuning().push != 0) {   // sparse psi: scatter + sort-reduce (hsv_push.cu)
     bool done = false;
     HSV_TRY(launch_push(op, a, &done, n_warps, dense_hint));
+    if (done) return HSV_OK;
+  }
+  {   // small beta rows: partner rows staged on chip by TMA (hsv_apply_staged.cu)
+    bool done = false;
+    HSV_TRY(launch_apply_staged(op, a, n_warps, &done));
     if (done) return HSV_OK;
   }
   int R = tuning().apply_r;
@@ -710,6 +720,12 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
     ghash = nh;
     op->n_buckets = (int64_t)nb.size();
   }
+  // per-group alpha flip part and the hashed/term-loop boundary (push path)
+  std::vector<uint32_t> gxa(op->groups.size(), 0u);
+  for (const int4& B : op->buckets)
+    for (int q = B.z; q < B.w; ++q) gxa[q] = (uint32_t)B.x;
+  op->g_hashed = op->n_buckets_h < op->n_buckets ? op->buckets[op->n_buckets_h].z
+                                                  : (int64_t)op->groups.size();
   // single-Z form of the term-loop groups (see SzTerm)
   std::vector<uint64_t> gsz(op->groups.size(), 0ull);
   std::vector<SzTerm> szt(op->terms.size(), SzTerm{0.0, 0u, 0u});
@@ -799,9 +815,13 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
       (rc = dalloc(&op->d_ghash, ghash.size())) || (rc = dalloc(&op->d_tabs, tabs.size())) ||
       (rc = dalloc(reinterpret_cast<unsigned char**>(&op->d_recs), recs.size())) ||
       (rc = dalloc(&op->d_splits, splits.size())) || (rc = dalloc(&op->d_gsz, gsz.size())) ||
-      (rc = dalloc(reinterpret_cast<SzTerm**>(&op->d_szt), szt.size())))
+      (rc = dalloc(reinterpret_cast<SzTerm**>(&op->d_szt), szt.size())) ||
+      (rc = dalloc(&op->d_gxa, gxa.size())))
     return fail(rc);
   cudaStream_t st = stream();
+  if (!gxa.empty())
+    HSV_TRY_CUDA(cudaMemcpyAsync(op->d_gxa, gxa.data(), gxa.size() * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, st));
   if (!gsz.empty())
     HSV_TRY_CUDA(cudaMemcpyAsync(op->d_gsz, gsz.data(), gsz.size() * sizeof(uint64_t),
                                  cudaMemcpyHostToDevice, st));
@@ -845,6 +865,7 @@ int hsv_op_destroy(hsv_op op) {
   dfree(op->d_splits);
   dfree(op->d_gsz);
   dfree(reinterpret_cast<SzTerm*>(op->d_szt));
+  dfree(op->d_gxa);
   delete op;
   return HSV_OK;
 }

@@ -168,6 +168,8 @@ struct hsv_op_s {
   uint64_t* d_gsz = nullptr;
   void* d_szt = nullptr;
   int64_t n_single_z = 0;
+  uint32_t* d_gxa = nullptr;    // per group: alpha flip part (push path)
+  int64_t g_hashed = 0;         // groups [0, g_hashed) are x-local
   // host copies of the active group table (for CSR materialization)
   std::vector<int4> buckets, groups;
   std::vector<Term> terms;

@@ -15,7 +15,10 @@ struct Tuning {
   int push = -1;          // sparse-psi push path: -1 auto, 0 off, 1 whenever it fits in memory
   int push_keys = 32;
   int sweep = 1;          // adjoint/forward sweeps: 1 one cooperative launch, 0 launch per op
-  int sweep_grid = 0;     // sweep blocks: 0 = min(co-resident, work items)   // auto: push while nnz(psi) * (1 + groups) <= push_keys * rows - 2^20
+  int sweep_grid = 0;     // sweep blocks: 0 = min(co-resident, work items)
+  int staged = 0;         // K1s (TMA-staged partner rows) where the sector fits: 1 on, 0 off.
+                          // Off by default: it cuts K1's global load sectors 8.4x at H12
+                          // but not its time (K1 is issue-bound; 3.04 vs 3.07 ms)   // auto: push while nnz(psi) * (1 + groups) <= push_keys * rows - 2^20
 };
 Tuning& tuning();
 
@@ -35,6 +38,8 @@ struct ApplyArgs {
   const double* tabs;
   const uint64_t* gsz;     // per group: 1<<63 | z0 for single-Z groups, else 0
   const void* szt;         // SzTerm per term (single-Z groups)
+  const uint32_t* gxa;     // per group: alpha flip part (its bucket's x)
+  int g_hashed;            // groups [0, g_hashed) are x-local (hashed)
   const double2* psi;
   const uint32_t* arow;  // alpha-row occupancy of psi (skip empty partner rows) or nullptr
   double2* out;      // nullptr: energy only
@@ -100,6 +105,9 @@ int apply_warps(const hsv_op_s* op);
 // dense_hint (optional, per state): skip when set, set when psi is found dense.
 int launch_push(const hsv_op_s* op, const ApplyArgs& a, bool* done, int64_t* n_warps,
                 bool* dense_hint);
+// K1s (hsv_apply_staged.cu): *done = false when the sector does not fit on chip.
+int launch_apply_staged(const hsv_op_s* op, const ApplyArgs& a, int64_t* n_warps, bool* done);
+void launch_combine_splits(const double2* part, int S, int64_t rows, double2* out, double prune);
 int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* epart,
                  int64_t a_lo, int64_t a_hi, double prune, int energy_only, int64_t* n_warps,
                  const uint32_t* arow = nullptr, bool* dense_hint = nullptr);

@@ -76,6 +76,9 @@ int hsv_set_tuning(const char* key, int64_t value) {
   } else if (k == "sweep") {
     HSV_REQUIRE(value == 0 || value == 1, HSV_ERR_INVALID, "sweep must be 0 or 1");
     g_tuning.sweep = (int)value;
+  } else if (k == "staged") {
+    HSV_REQUIRE(value == 0 || value == 1, HSV_ERR_INVALID, "staged must be 0 or 1");
+    g_tuning.staged = (int)value;
   } else if (k == "sweep_grid") {
     HSV_REQUIRE(value >= 0 && value <= (1 << 20), HSV_ERR_INVALID, "sweep_grid out of range");
     g_tuning.sweep_grid = (int)value;

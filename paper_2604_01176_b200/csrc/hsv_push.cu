@@ -156,23 +156,31 @@ __global__ void __launch_bounds__(256) k_push_reduce(const PushArgs p,
           continue;
         }
         const int g = g1 - 1;
-        int lo = 0, hi = a.n_buckets - 1;   // bucket holding group g (contiguous ranges)
-        while (lo < hi) {
-          const int mid = (lo + hi + 1) >> 1;
-          if (__ldg(&a.buckets[mid].z) <= g) lo = mid; else hi = mid - 1;
-        }
-        const uint32_t xa = (uint32_t)__ldg(&a.buckets[lo].x);
+        const uint32_t xa = __ldg(a.gxa + g);   // alpha flip part of group g
         const int4 G = __ldg(a.groups + g);
         double amp;
-        if (lo < a.n_buckets_h) {
+        if (g < a.g_hashed) {
           amp = rec_amp<W>(ldrec(recs + g), s, a.tabs);
         } else {
           amp = 0.0;
-          for (int tt = G.z; tt < G.w; ++tt) {
-            const double c = __ldg(&a.terms[tt].c);
-            const W z = (W)__ldg(&a.terms[tt].z);
-            const int sgn = popc(s & z) << 31;
-            amp += __hiloint2double(__double2hiint(c) ^ sgn, __double2loint(c));
+          const uint64_t gz = __ldg(a.gsz + g);
+          if (gz >> 63) {   // single-Z group, as in the pull kernel (exact)
+            const SzTerm* __restrict__ sz = reinterpret_cast<const SzTerm*>(a.szt);
+            for (int tt = G.z; tt < G.w; ++tt) {
+              const uint4 q = __ldg(reinterpret_cast<const uint4*>(sz + tt));
+              const uint32_t sb31 = SH == 16 ? ((uint32_t)s << q.z) & q.w
+                                             : ((uint32_t)(s >> q.z) << 31) & q.w;
+              amp += __hiloint2double((int)q.y ^ (int)sb31, (int)q.x);
+            }
+            const int sgn = popc(s & (W)gz) << 31;
+            amp = __hiloint2double(__double2hiint(amp) ^ sgn, __double2loint(amp));
+          } else {
+            for (int tt = G.z; tt < G.w; ++tt) {
+              const double c = __ldg(&a.terms[tt].c);
+              const W z = (W)__ldg(&a.terms[tt].z);
+              const int sgn = popc(s & z) << 31;
+              amp += __hiloint2double(__double2hiint(c) ^ sgn, __double2loint(c));
+            }
           }
         }
         const int64_t src = (int64_t)__ldg(a.Ra + (sa ^ xa)) * a.Nb +
