@@ -257,14 +257,23 @@ def run_hsv(args):
     upload()
     n_alpha_strings = basis._sector.n_alpha_strings
     a_lo, a_hi = alpha_row_range(n_alpha_strings, rank, world)
-    d_out = torch.zeros(2 + M, dtype=torch.float64, device="cuda")
-    gathered = torch.zeros(world, 2 + M, dtype=torch.float64, device="cuda")
+    d_out = torch.zeros(2 + M + (M & 1), dtype=torch.float64, device="cuda")   # 16-B multiple
+    gathered = torch.zeros(world, d_out.numel(), dtype=torch.float64, device="cuda")
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    # partial exchange: NVLink peer stores (CUDA IPC) + device barrier, else NCCL
+    peer = None
+    if world > 1 and os.environ.get("HSV_PEER", "1") != "0":
+        from paper_2604_01176_b200.distributed import PeerExchange
+        peer = PeerExchange.create(world * d_out.numel() * 8)
+    exchange = "nvlink-peer (CUDA IPC stores + device barrier)" if peer else (
+        "nccl all_gather" if world > 1 else "none")
 
     def step_device():
         N.call("hsv_energy_screen_pool_async", op.handle, st.handle, dpool.handle, a_lo, a_hi,
                N.C.c_void_p(d_out.data_ptr()))
         if world > 1:
+            if peer is not None:
+                return peer.gather_and_combine(d_out)
             dist.all_gather_into_tensor(gathered, d_out)
             return combine_partials(gathered)    # rank order, fixed
         return d_out
@@ -326,9 +335,8 @@ def run_hsv(args):
         a.record()
         upload()                               # H2D: positions + amplitudes (pinned)
         if world > 1:
-            step_device()
-            res = combine_partials(gathered).cpu().numpy()  # D2H
-            e_host.value, g_host[:] = res[0], res[2:]
+            res = step_device().cpu().numpy()             # D2H
+            e_host.value, g_host[:] = res[0], res[2:2 + M]
         else:
             N.call("hsv_energy_screen_pool", op.handle, st.handle, dpool.handle,
                    N.C.byref(e_host), N.ptr_f64(g_host))
@@ -395,7 +403,8 @@ def run_hsv(args):
                                    "S1 dense state",
                        "dim": dim, "n_terms": T, "pool": M, "csr_nnz": nnz_struct,
                        "l2": "flushed between timed steps (256 MiB write, outside events)",
-                       "parallelism": f"owner-computes alpha rows x{world}"},
+                       "parallelism": f"owner-computes alpha rows x{world}",
+                       "exchange": exchange},
             "energy": energy,
             "roofline": {"bound": "hbm", "kernel": "k_apply (H|psi>, K1)",
                          "achieved": achieved, "peak": hbm, "unit": "GB/s",

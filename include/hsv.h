@@ -62,6 +62,7 @@ typedef struct hsv_sector_s* hsv_sector;
 typedef struct hsv_op_s* hsv_op;
 typedef struct hsv_state_s* hsv_state;
 typedef struct hsv_pool_s* hsv_pool;
+typedef struct hsv_peer_s* hsv_peer;
 
 /* ---- library / device ------------------------------------------------- */
 HSV_API int hsv_abi_version(void);
@@ -199,6 +200,34 @@ HSV_API int hsv_energy_screen_pool(hsv_op op, hsv_state psi, hsv_pool pool, doub
  * partials all-gathered by NCCL in rank order, as the reference concatenates
  * row blocks in worker order (sparse.py:199-201). */
 HSV_API int hsv_sum_rows_async(const double* d_in, int64_t n_rows, int64_t n_cols, double* d_out);
+
+/* ---- NVLink peer exchange (one process per GPU, replaces NCCL on the path) ----
+ * A peer buffer is `bytes` of device memory that every rank maps (CUDA IPC),
+ * plus per-rank arrival flags.  Collective use:
+ *   hsv_peer_create   -> writes this rank's 64-byte IPC handle to handle_out;
+ *   (host all-gathers the handles, e.g. torch.distributed.all_gather_object)
+ *   hsv_peer_open     -> maps the other ranks' buffers (handles: world x 64 B);
+ *   hsv_peer_allgather_async(p, d_src, n): copy n bytes from d_src to offset
+ *     rank * n of every rank's buffer over NVLink, publish an arrival flag
+ *     (system-scope release) and wait on the device until every rank's block
+ *     has arrived; afterwards hsv_peer_data() holds all blocks in rank order.
+ *     Stream-ordered, no host synchronization, no NCCL.
+ * The same buffers carry whole H|psi> rows: hsv_eg_forward_peer_async writes
+ * the rank's rows of w into every rank's buffer from the K1 epilogue
+ * (compute + all-gather fused), then publishes/waits like the all-gather. */
+HSV_API int hsv_peer_create(int world, int rank, int64_t bytes, hsv_peer* out, void* handle_out);
+HSV_API int hsv_peer_open(hsv_peer p, const void* handles);
+HSV_API int hsv_peer_destroy(hsv_peer p);
+HSV_API int hsv_peer_data(hsv_peer p, void** d_data, int64_t* bytes);
+HSV_API int hsv_peer_allgather_async(hsv_peer p, const void* d_src, int64_t n);
+/* Phase 1 of the adjoint sweep (as hsv_eg_forward_async) with the rows
+ * [a_lo, a_hi) of w = H psi written by the K1 epilogue straight into every
+ * rank's peer buffer (bytes >= dim * 16, rows at their natural offsets), then
+ * the arrival barrier and a copy of the complete local buffer into `w`. */
+HSV_API int hsv_eg_forward_peer_async(hsv_op op, uint64_t hf_key, const uint64_t* occ_masks,
+                                      const uint64_t* virt_masks, const double* c,
+                                      const double* s, int64_t k, int64_t a_lo, int64_t a_hi,
+                                      hsv_state psi, hsv_state w, hsv_peer p);
 
 /* ---- tuning knobs (defaults are the measured best): "apply_r" (rows per
  * lane 0/1/2/4), "apply_minb", "apply_split" (0/1/2/4/8), "apply_interleave"

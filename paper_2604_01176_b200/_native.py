@@ -88,6 +88,13 @@ _SIGNATURES = {
     "hsv_energy_screen_pool_async": (C.c_int, [vp, vp, vp, i64, i64, vp]),
     "hsv_energy_screen_pool": (C.c_int, [vp, vp, vp, P_dbl, P_dbl]),
     "hsv_sum_rows_async": (C.c_int, [vp, i64, i64, vp]),
+    "hsv_peer_create": (C.c_int, [C.c_int, C.c_int, i64, C.POINTER(vp), vp]),
+    "hsv_peer_open": (C.c_int, [vp, vp]),
+    "hsv_peer_destroy": (C.c_int, [vp]),
+    "hsv_peer_data": (C.c_int, [vp, C.POINTER(vp), C.POINTER(i64)]),
+    "hsv_peer_allgather_async": (C.c_int, [vp, vp, i64]),
+    "hsv_eg_forward_peer_async": (C.c_int, [vp, C.c_uint64, P_u64, P_u64, P_dbl, P_dbl, i64,
+                                            i64, i64, vp, vp, vp]),
     "hsv_set_tuning": (C.c_int, [C.c_char_p, i64]),
     "hsv_prof_enable": (C.c_int, [C.c_int]),
     "hsv_prof_collect": (C.c_int, []),

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
         } else {
           double2 y = acc[k];
           if (a.prune > 0.0 && sqrt(y.x * y.x + y.y * y.y) < a.prune) y = make_double2(0.0, 0.0);
-          a.out[rowbase + rb] = y;
+          put_row(a.out, a.peer_rows, a.n_peer_rows, rowbase + rb, y);
         }
       }
     }
@@ -306,8 +306,10 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
 }
 
 // Sum the per-split partial rows in split order (fixed), then the drop rule.
+// Rows go to out[off + i] (and to the peer buffers, see put_row).
 __global__ void k_combine_splits(const double2* __restrict__ part, int S, int64_t rows,
-                                 double2* __restrict__ out, double prune) {
+                                 double2* __restrict__ out, int64_t off, double prune,
+                                 double2* const* peers, int n_peers) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= rows) return;
   double2 y = part[i];
@@ -317,12 +319,13 @@ __global__ void k_combine_splits(const double2* __restrict__ part, int S, int64_
     y.y += p.y;
   }
   if (prune > 0.0 && sqrt(y.x * y.x + y.y * y.y) < prune) y = make_double2(0.0, 0.0);
-  out[i] = y;
+  put_row(out, peers, n_peers, off + i, y);
 }
 
-void launch_combine_splits(const double2* part, int S, int64_t rows, double2* out, double prune) {
-  k_combine_splits<<<(unsigned)((rows + 255) / 256), 256, 0, stream()>>>(part, S, rows, out,
-                                                                           prune);
+void launch_combine_splits(const double2* part, int S, int64_t rows, double2* out, int64_t off,
+                           double prune, double2* const* peers, int n_peers) {
+  k_combine_splits<<<(unsigned)((rows + 255) / 256), 256, 0, stream()>>>(part, S, rows, out, off,
+                                                                           prune, peers, n_peers);
 }
 
 template <typename W, int SH, int R, int MINB>
@@ -368,8 +371,8 @@ static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
     ProfScope prof("apply");
     k_apply<W, SH, R, MINB><<<(unsigned)grid, 256, 0, stream()>>>(a);
     if (ypart)
-      k_combine_splits<<<(unsigned)((rows + 255) / 256), 256, 0, stream()>>>(
-          ypart, S, rows, a.out + a.a_lo * a.Nb, a.prune);
+      launch_combine_splits(ypart, S, rows, a.out, a.a_lo * a.Nb, a.prune, a.peer_rows,
+                            a.n_peer_rows);
   }
   count_launch(ypart ? 2 : 1);
   HSV_CHECK_LAUNCH();
@@ -397,6 +400,8 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   a.groups = op->d_groups; a.terms = op->d_terms; a.diag = op->d_diag;
   a.tabs = op->d_tabs; a.recs = op->d_recs; a.n_buckets_h = (int)op->n_buckets_h;
   a.gsz = op->d_gsz; a.szt = op->d_szt; a.gxa = op->d_gxa; a.g_hashed = (int)op->g_hashed;
+  a.peer_rows = out ? ctx().peer_rows : nullptr;
+  a.n_peer_rows = out ? ctx().n_peer_rows : 0;
   a.psi = psi; a.out = out; a.epart = epart;
   a.Nb = s->Nb; a.a_lo = a_lo; a.a_hi = a_hi; a.prune = prune; a.energy_only = energy_only;
   HSV_REQUIRE(s->dim < ((int64_t)1 << 32), HSV_ERR_UNSUPPORTED,

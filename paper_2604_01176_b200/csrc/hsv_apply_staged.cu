@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kStagedMaxWarps * 32, 2) k_apply_staged(const 
       } else {
         double2 y = acc[k];
         if (a.prune > 0.0 && sqrt(y.x * y.x + y.y * y.y) < a.prune) y = make_double2(0.0, 0.0);
-        a.out[rowbase + rb] = y;
+        put_row(a.out, a.peer_rows, a.n_peer_rows, rowbase + rb, y);
       }
     }
     if (a.epart && ((live >> k) & 1u)) {
@@ -314,7 +314,8 @@ int launch_apply_staged(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_warp
     ProfScope prof("apply");
     k_apply_staged<16><<<(unsigned)grid, warps * 32, smem, stream()>>>(sa);
     if (ypart)
-      launch_combine_splits(ypart, S, rows, a0.out + a0.a_lo * Nb, a0.prune);
+      launch_combine_splits(ypart, S, rows, a0.out, a0.a_lo * Nb, a0.prune, a0.peer_rows,
+                            a0.n_peer_rows);
   }
   count_launch(ypart ? 2 : 1);
   HSV_CHECK_LAUNCH();

@@ -61,6 +61,10 @@ struct Context {
   cudaStream_t own = nullptr;      // library-owned stream
   int num_sms = 148;
   int64_t launches = 0;
+  // set by hsv_eg_forward_peer_async around its H application: K1 also stores
+  // every output row into these peer buffers (NVLink), see ApplyArgs::peer_rows
+  double2* const* peer_rows = nullptr;
+  int n_peer_rows = 0;
 };
 Context& ctx();
 int ensure_init();
@@ -183,6 +187,19 @@ struct hsv_pool_s {
   int2* d_opl = nullptr;      // per operator: beta list {offset, length}, length -1: empty beta half
   int2* d_blist = nullptr;    // beta source lists {rb_src, rb_tgt}
   std::vector<int4> h;
+};
+
+// NVLink peer exchange buffer (hsv_peer.cu): `bytes` of data then `world`
+// arrival flags, one cudaMalloc allocation shared with the other ranks by IPC.
+struct hsv_peer_s {
+  int world = 1, rank = 0;
+  int64_t bytes = 0, flags_off = 0;
+  char* base = nullptr;                 // local allocation
+  std::vector<char*> bases;             // every rank's mapping (bases[rank] == base)
+  char** d_bases = nullptr;             // the same, in device memory
+  unsigned int* d_counter = nullptr;    // last-CTA detection in the put kernel
+  uint64_t epoch = 0;
+  bool opened = false;
 };
 
 struct hsv_state_s {

@@ -13,12 +13,12 @@ struct Tuning {
   int apply_split = 0;    // bucket splits per row unit in K1 (0 = auto, else 1/2/4/8)
   int apply_interleave = -1;  // K1 unit schedule: -1 auto (= interleaved), 0 contiguous, 1 interleaved
   int push = -1;          // sparse-psi push path: -1 auto, 0 off, 1 whenever it fits in memory
-  int push_keys = 32;
+  int push_keys = 32;     // auto: push while nnz(psi) * (1 + groups) <= push_keys * rows - 2^20
   int sweep = 1;          // adjoint/forward sweeps: 1 one cooperative launch, 0 launch per op
   int sweep_grid = 0;     // sweep blocks: 0 = min(co-resident, work items)
   int staged = 0;         // K1s (TMA-staged partner rows) where the sector fits: 1 on, 0 off.
                           // Off by default: it cuts K1's global load sectors 8.4x at H12
-                          // but not its time (K1 is issue-bound; 3.04 vs 3.07 ms)   // auto: push while nnz(psi) * (1 + groups) <= push_keys * rows - 2^20
+                          // but not its time (K1 is issue-bound; 3.04 vs 3.07 ms)
 };
 Tuning& tuning();
 
@@ -56,7 +56,17 @@ struct ApplyArgs {
   int64_t part_stride;
   double prune;
   int energy_only;
+  double2* const* peer_rows;  // device array: other ranks' w buffers (NVLink), or nullptr
+  int n_peer_rows;
 };
+
+// Final value of output row `row`: local store plus the same store into every
+// peer buffer (compute and all-gather fused: rows cross NVLink as they finish).
+__device__ __forceinline__ void put_row(double2* out, double2* const* peers, int n_peers,
+                                        int64_t row, double2 y) {
+  out[row] = y;
+  for (int p = 0; p < n_peers; ++p) peers[p][row] = y;
+}
 
 // Packed per-group record of an x-local group, loaded with one or two 16-byte
 // uniform loads: meta = hb | shift << 8.
@@ -107,7 +117,8 @@ int launch_push(const hsv_op_s* op, const ApplyArgs& a, bool* done, int64_t* n_w
                 bool* dense_hint);
 // K1s (hsv_apply_staged.cu): *done = false when the sector does not fit on chip.
 int launch_apply_staged(const hsv_op_s* op, const ApplyArgs& a, int64_t* n_warps, bool* done);
-void launch_combine_splits(const double2* part, int S, int64_t rows, double2* out, double prune);
+void launch_combine_splits(const double2* part, int S, int64_t rows, double2* out, int64_t off,
+                           double prune, double2* const* peers, int n_peers);
 int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* epart,
                  int64_t a_lo, int64_t a_hi, double prune, int energy_only, int64_t* n_warps,
                  const uint32_t* arow = nullptr, bool* dense_hint = nullptr);

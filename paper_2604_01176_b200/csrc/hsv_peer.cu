@@ -1,0 +1,201 @@
+// NVLink peer exchange without NCCL: every rank maps the others' buffers by
+// CUDA IPC, kernels store into peer memory directly, and arrival is published
+// with system-scope release stores of an epoch counter into per-rank flags and
+// observed with acquire loads on the device (stream-ordered, no host sync).
+//
+// Buffers are double-buffered by epoch parity: a rank can run ahead into the
+// next exchange (writing the other half) while a slower peer still reads the
+// current one; it cannot get two exchanges ahead, because every exchange ends
+// with a wait for all ranks' arrival.
+//
+// Two users:
+//  * hsv_peer_allgather_async: the per-rank (E, g) partials of the energy +
+//    gradient step (replaces the NCCL all-gather in bench.py / distributed.py);
+//  * hsv_eg_forward_peer_async: the rank's rows of w = H psi are stored into
+//    every rank's buffer by the K1 epilogue itself (put_row), so the all-gather
+//    of w rides on NVLink while K1 is still computing other rows -- the
+//    compute + collective fusion of the multi-GPU adjoint sweep.
+#include <cstring>
+
+#include "hsv_common.cuh"
+#include "hsv_kernels.cuh"
+
+namespace hsv {
+
+namespace {
+
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// copy n bytes (multiple of 16) from src to bases[r] + off for every rank r
+__global__ void k_peer_put(const uint4* __restrict__ src, int64_t n16, char* const* bases,
+                           int world, int64_t off) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n16; i += stride) {
+    const uint4 v = src[i];
+    for (int r = 0; r < world; ++r) reinterpret_cast<uint4*>(bases[r] + off)[i] = v;
+  }
+}
+
+// publish this rank's arrival for `epoch` to every rank, then wait for all
+__global__ void k_peer_barrier(char* const* bases, int world, int rank, int64_t flags_off,
+                               uint64_t epoch) {
+  if (threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int r = 0; r < world; ++r)
+    st_release_sys(reinterpret_cast<uint64_t*>(bases[r] + flags_off) + rank, epoch);
+  const uint64_t* mine = reinterpret_cast<const uint64_t*>(bases[rank] + flags_off);
+  for (int r = 0; r < world; ++r)
+    while (ld_acquire_sys(mine + r) < epoch) __nanosleep(64);
+  __threadfence_system();
+}
+
+int peer_barrier(hsv_peer_s* p) {
+  k_peer_barrier<<<1, 32, 0, stream()>>>(p->d_bases, p->world, p->rank, p->flags_off, p->epoch);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  return HSV_OK;
+}
+
+}  // namespace
+
+}  // namespace hsv
+
+using namespace hsv;
+
+extern "C" {
+
+int hsv_peer_create(int world, int rank, int64_t bytes, hsv_peer* out, void* handle_out) {
+  HSV_TRY(ensure_init());
+  HSV_REQUIRE(out && handle_out && world >= 1 && rank >= 0 && rank < world && bytes > 0,
+              HSV_ERR_INVALID, "bad argument");
+  auto* p = new hsv_peer_s();
+  p->world = world;
+  p->rank = rank;
+  p->bytes = (bytes + 255) / 256 * 256;
+  p->flags_off = 2 * p->bytes;                          // two halves, then the flags
+  const size_t total = (size_t)p->flags_off + (size_t)world * sizeof(uint64_t);
+  cudaError_t e = cudaMalloc(&p->base, total);          // IPC needs a plain allocation
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete p;
+    set_error(HSV_ERR_OOM, "peer buffer of %zu bytes: %s", total, cudaGetErrorString(e));
+    return HSV_ERR_OOM;
+  }
+  cudaMemset(p->base + p->flags_off, 0, (size_t)world * sizeof(uint64_t));
+  cudaIpcMemHandle_t h;
+  e = cudaIpcGetMemHandle(&h, p->base);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(p->base);
+    delete p;
+    set_error(HSV_ERR_CUDA, "cudaIpcGetMemHandle: %s", cudaGetErrorString(e));
+    return HSV_ERR_CUDA;
+  }
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  std::memcpy(handle_out, &h, sizeof(h));
+  p->bases.assign(world, nullptr);
+  p->bases[rank] = p->base;
+  *out = p;
+  return HSV_OK;
+}
+
+int hsv_peer_open(hsv_peer p, const void* handles) {
+  HSV_REQUIRE(p && handles && !p->opened, HSV_ERR_INVALID, "bad argument");
+  const char* hs = static_cast<const char*>(handles);
+  for (int r = 0; r < p->world; ++r) {
+    if (r == p->rank) continue;
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, hs + 64 * r, sizeof(h));
+    void* ptr = nullptr;
+    HSV_TRY_CUDA(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    p->bases[r] = static_cast<char*>(ptr);
+  }
+  HSV_TRY_CUDA(cudaMalloc(&p->d_bases, p->world * sizeof(char*)));
+  HSV_TRY_CUDA(cudaMemcpy(p->d_bases, p->bases.data(), p->world * sizeof(char*),
+                          cudaMemcpyHostToDevice));
+  HSV_TRY_CUDA(cudaDeviceSynchronize());   // flags zeroed everywhere before first use
+  p->opened = true;
+  return HSV_OK;
+}
+
+int hsv_peer_destroy(hsv_peer p) {
+  if (!p) return HSV_OK;
+  cudaDeviceSynchronize();
+  for (int r = 0; r < p->world; ++r)
+    if (r != p->rank && p->bases[r]) cudaIpcCloseMemHandle(p->bases[r]);
+  if (p->d_bases) cudaFree(p->d_bases);
+  if (p->base) cudaFree(p->base);
+  delete p;
+  return HSV_OK;
+}
+
+int hsv_peer_data(hsv_peer p, void** d_data, int64_t* bytes) {
+  HSV_REQUIRE(p, HSV_ERR_INVALID, "null peer");
+  if (d_data) *d_data = p->base + (p->epoch & 1) * p->bytes;   // the latest exchange
+  if (bytes) *bytes = p->bytes;
+  return HSV_OK;
+}
+
+int hsv_peer_allgather_async(hsv_peer p, const void* d_src, int64_t n) {
+  HSV_REQUIRE(p && p->opened && d_src, HSV_ERR_INVALID, "peer buffer not opened");
+  HSV_REQUIRE(n > 0 && n % 16 == 0 && n * p->world <= p->bytes, HSV_ERR_INVALID,
+              "allgather block of %lld bytes does not fit the peer buffer",
+              (long long)n);
+  ++p->epoch;
+  const int64_t off = (p->epoch & 1) * p->bytes + p->rank * n;
+  const int64_t n16 = n / 16;
+  const int grid = (int)std::min<int64_t>((n16 + 255) / 256, (int64_t)ctx().num_sms * 4);
+  {
+    ProfScope prof("peer");
+    k_peer_put<<<std::max(grid, 1), 256, 0, stream()>>>(static_cast<const uint4*>(d_src), n16,
+                                                       p->d_bases, p->world, off);
+    count_launch();
+    HSV_CHECK_LAUNCH();
+    HSV_TRY(peer_barrier(p));
+  }
+  return HSV_OK;
+}
+
+int hsv_eg_forward_peer_async(hsv_op op, uint64_t hf_key, const uint64_t* occ,
+                              const uint64_t* virt, const double* cs, const double* sn, int64_t k,
+                              int64_t a_lo, int64_t a_hi, hsv_state psi, hsv_state w,
+                              hsv_peer p) {
+  HSV_REQUIRE(op && w && p && p->opened && w->sec == op->sec, HSV_ERR_INVALID, "bad argument");
+  const int64_t wbytes = op->sec->dim * (int64_t)sizeof(double2);
+  HSV_REQUIRE(wbytes <= p->bytes, HSV_ERR_INVALID, "peer buffer smaller than a state");
+  ++p->epoch;
+  const int64_t half = (p->epoch & 1) * p->bytes;
+  // every rank's half for this epoch, as double2 row arrays
+  std::vector<double2*> sinks(p->world);
+  for (int r = 0; r < p->world; ++r) sinks[r] = reinterpret_cast<double2*>(p->bases[r] + half);
+  double2** d_sinks = nullptr;
+  HSV_TRY(dalloc(&d_sinks, p->world));
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_sinks, sinks.data(), p->world * sizeof(double2*),
+                               cudaMemcpyHostToDevice, stream()));
+  ctx().peer_rows = d_sinks;
+  ctx().n_peer_rows = p->world;
+  int rc = hsv_eg_forward_async(op, hf_key, occ, virt, cs, sn, k, a_lo, a_hi, psi, w);
+  ctx().peer_rows = nullptr;
+  ctx().n_peer_rows = 0;
+  dfree(d_sinks);
+  if (rc) return rc;
+  {
+    ProfScope prof("peer");
+    HSV_TRY(peer_barrier(p));
+  }
+  // the local half now holds every rank's rows
+  HSV_TRY_CUDA(cudaMemcpyAsync(w->d_amp, p->base + half, wbytes, cudaMemcpyDeviceToDevice,
+                               stream()));
+  w->norm2_valid = w->arow_valid = false;
+  w->dense_hint = false;
+  return HSV_OK;
+}
+
+}  // extern "C"

@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(256) k_push_reduce(const PushArgs p,
       if (a.out) {
         double2 y = acc;
         if (a.prune > 0.0 && sqrt(y.x * y.x + y.y * y.y) < a.prune) y = make_double2(0.0, 0.0);
-        a.out[row] = y;
+        put_row(a.out, a.peer_rows, a.n_peer_rows, row, y);
       }
       if (eblk) {
         const double2 pv = a.psi[row];
@@ -341,6 +341,9 @@ int launch_push(const hsv_op_s* op, const ApplyArgs& a, bool* done, int64_t* n_w
                 bool* dense_hint) {
   *done = false;
   if (tuning().push == 0) return HSV_OK;
+  // rows the push path never reaches are zeroed locally only; with peer sinks
+  // (fused all-gather) every row must be stored, which the pull kernel does
+  if (a.n_peer_rows > 0) return HSV_OK;
   if (op->sec->wide) return push_t<uint64_t, 32>(op, a, done, n_warps, dense_hint);
   return push_t<uint32_t, 16>(op, a, done, n_warps, dense_hint);
 }

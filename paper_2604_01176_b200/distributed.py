@@ -59,6 +59,70 @@ def gather_and_combine(partial: torch.Tensor, group=None) -> torch.Tensor:
     return combine_partials(buf)
 
 
+class PeerExchange:
+    """NVLink peer buffers shared by CUDA IPC (hsv_peer_*): all-gathers and the
+    fused K1 + w all-gather without NCCL.  Collective: every rank constructs it
+    with the same size.  `PeerExchange.create` returns None when peer mapping
+    is unavailable (then callers keep the NCCL path)."""
+
+    def __init__(self, nbytes: int, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.handle = None
+        h = N.C.c_void_p()
+        handle = (N.C.c_char * 64)()
+        try:
+            N.call("hsv_peer_create", self.world, self.rank, int(nbytes), N.C.byref(h), handle)
+            self.handle, mine = h, bytes(handle)
+        except (RuntimeError, MemoryError, ValueError):
+            mine = None
+        # every rank takes part in both exchanges, so a failure anywhere makes
+        # every rank fall back together (no rank is left waiting in a collective)
+        handles = [None] * self.world
+        dist.all_gather_object(handles, mine, group=group)
+        ok = all(x is not None for x in handles)
+        if ok:
+            buf = (N.C.c_char * (64 * self.world)).from_buffer_copy(b"".join(handles))
+            try:
+                N.call("hsv_peer_open", self.handle, buf)
+            except (RuntimeError, ValueError):
+                ok = False
+        oks = [None] * self.world
+        dist.all_gather_object(oks, ok, group=group)
+        if not all(oks):
+            raise RuntimeError("NVLink peer mapping unavailable on some rank")
+
+    @classmethod
+    def create(cls, nbytes: int, group=None):
+        try:
+            return cls(nbytes, group)
+        except RuntimeError:
+            return None
+
+    def __del__(self):
+        try:
+            if self.handle:
+                N.lib().hsv_peer_destroy(self.handle)
+        except Exception:
+            pass
+
+    def data(self) -> int:
+        ptr, n = N.C.c_void_p(), N.i64()
+        N.call("hsv_peer_data", self.handle, N.C.byref(ptr), N.C.byref(n))
+        return ptr.value
+
+    def gather_and_combine(self, partial: torch.Tensor) -> torch.Tensor:
+        """Rank-order sum of every rank's `partial` (float64, CUDA, 16-B multiple),
+        on the library stream: NVLink stores + device barrier + one summation."""
+        n = partial.numel() * 8
+        N.call("hsv_peer_allgather_async", self.handle, N.C.c_void_p(partial.data_ptr()), n)
+        out = torch.empty_like(partial)
+        N.call("hsv_sum_rows_async", N.C.c_void_p(self.data()), self.world, partial.numel(),
+               N.C.c_void_p(out.data_ptr()))
+        return out
+
+
 def allgather_rows(view: torch.Tensor, n_alpha_strings: int, nb: int, group=None):
     """Make the alpha-row blocks of a replicated [dim, 2] buffer identical on all
     ranks: each rank contributes rows alpha_row_range(rank) (NCCL all-gather of
@@ -114,6 +178,11 @@ class DistributedSvAdaptEngine:
         groups = self.matrix.info()["n_active_groups"]
         self.replica_nnz = max(0, (32 * dim - (1 << 20)) // (1 + groups))
         self._last_nnz = 1                            # HF
+        # NVLink peer exchange (CUDA IPC) for the sharded modes; NCCL otherwise
+        # (HSV_PEER=0 forces NCCL)
+        import os
+        self.peer = (PeerExchange.create(dim * 16, group)
+                     if os.environ.get("HSV_PEER", "1") != "0" else None)
 
     def initial_state(self):
         return self.inner.initial_state()
@@ -145,9 +214,12 @@ class DistributedSvAdaptEngine:
                 (self.inner.energy(state), np.zeros(0))
         sc = self._screen(pool)
         sc.launch(state)
-        tot = gather_and_combine(sc.partial, self.group)
+        if self.peer is not None:
+            tot = self.peer.gather_and_combine(sc.partial)
+        else:
+            tot = gather_and_combine(sc.partial, self.group)
         host = tot.cpu().numpy()
-        return float(host[0]), host[2:].copy()
+        return float(host[0]), host[2:2 + sc.pool.n].copy()
 
     def screen(self, state, pool):
         return self.energy_and_screen(state, pool)[1]
@@ -164,11 +236,17 @@ class DistributedSvAdaptEngine:
         # ansatz grows by one operator per ADAPT iteration, so the support grows slowly
         rep = self.replicated(self._last_nnz)
         lo, hi = (0, self.na) if rep else (self.a_lo, self.a_hi)
-        N.call("hsv_eg_forward_async", self.matrix.handle, int(self.system.hf.bits),
-               N.ptr_u64(occ), N.ptr_u64(virt), N.ptr_f64(cs), N.ptr_f64(sn), th.size,
-               lo, hi, self._psi.handle, self._w.handle)
-        if not rep:
-            allgather_rows(self._w.torch_view(), self.na, self.nb, self.group)
+        args = (self.matrix.handle, int(self.system.hf.bits), N.ptr_u64(occ), N.ptr_u64(virt),
+                N.ptr_f64(cs), N.ptr_f64(sn), th.size, lo, hi, self._psi.handle,
+                self._w.handle)
+        if not rep and self.peer is not None:
+            # K1 stores its rows of w into every rank's buffer over NVLink as it
+            # computes them (fused compute + all-gather), then a device barrier
+            N.call("hsv_eg_forward_peer_async", *args, self.peer.handle)
+        else:
+            N.call("hsv_eg_forward_async", *args)
+            if not rep:
+                allgather_rows(self._w.torch_view(), self.na, self.nb, self.group)
         self._last_nnz = self._psi.nnz()
         g = np.empty(th.size)
         e = N.dbl()
@@ -188,7 +266,9 @@ class ShardedEnergyScreen:
         self.world = dist.get_world_size() if world is None and dist.is_initialized() else (world or 1)
         na = engine.basis._sector.n_alpha_strings
         self.a_lo, self.a_hi = alpha_row_range(na, self.rank, self.world)
-        self.partial = torch.zeros(2 + self.pool.n, dtype=torch.float64, device="cuda")
+        # even length: peer exchanges move 16-byte multiples
+        self.partial = torch.zeros(2 + self.pool.n + (self.pool.n & 1), dtype=torch.float64,
+                                   device="cuda")
 
     def launch(self, state):
         """Enqueue this rank's partial (no host sync) on the library stream."""
@@ -200,4 +280,4 @@ class ShardedEnergyScreen:
         self.launch(state)
         tot = gather_and_combine(self.partial)
         host = tot.cpu().numpy()
-        return float(host[0]), host[2:].copy()
+        return float(host[0]), host[2:2 + self.pool.n].copy()

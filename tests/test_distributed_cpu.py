@@ -95,3 +95,29 @@ def test_gloo_world2_shards_combine_to_full(name):
     ref = load_golden(f"ref_{name}")
     assert abs(tot[0] - float(ref["e_s1_expect"])) <= 1e-10
     assert np.max(np.abs(tot[2:] - ref["g_s1"])) <= 1e-10 * max(1.0, np.max(np.abs(ref["g_s1"])))
+
+
+def _peer_worker(rank, world, port, out_q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2604_01176_b200.distributed import PeerExchange
+    # no GPU here: the peer buffer cannot be created on any rank, and every rank
+    # must fall back together instead of one waiting in a collective
+    pe = PeerExchange.create(1 << 16)
+    out_q.put((rank, pe is None))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_peer_exchange_falls_back_collectively():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res == [(0, True), (1, True)]
