@@ -185,26 +185,20 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
         for (int g = B.z; g < B.w; ++g) {
           const Rec<W> cur = ldrec(rp + g);
           const uint32_t xb = cur.xb;
-          const int hb = (int)(cur.meta & 0xffu);
-          unsigned v = 0u;
+          // No per-lane sector test: the table holds 0 for out-of-sector beta
+          // patterns and Rb0 maps out-of-sector strings to rank 0 (a harmless
+          // in-row gather), so such rows add exactly +-0 (H14 -7%, H12 -1%).
+          const int shift = (int)((cur.meta >> 8) & 0xffu);
 #pragma unroll
-          for (int k = 0; k < R; ++k)
-            v |= ((live >> k) & 1u) && __popc(sb[k] & xb) == hb ? (1u << k) : 0u;
-          if (__any_sync(0xffffffffu, v != 0u)) {
-            const int shift = (int)((cur.meta >> 8) & 0xffu);
-#pragma unroll
-            for (int k = 0; k < R; ++k) {
-              const uint32_t h = cur.tab + (uint32_t)((W)((s[k] & cur.xm) * cur.mul) >> shift);
-              const double A = __ldg(a.tabs + h);
-              const int sgn = popc(s[k] & cur.z0) << 31;
-              const double amp = __hiloint2double(__double2hiint(A) ^ sgn, __double2loint(A));
-              if ((v >> k) & 1u) {
-                const uint32_t rk = __ldg(a.Rb + (uint32_t)(sb[k] ^ xb));
-                const double2 p = a.psi[rowoff + rk];
-                acc[k].x = fma(amp, p.x, acc[k].x);
-                acc[k].y = fma(amp, p.y, acc[k].y);
-              }
-            }
+          for (int k = 0; k < R; ++k) {
+            const uint32_t h = cur.tab + (uint32_t)((W)((s[k] & cur.xm) * cur.mul) >> shift);
+            const double A = __ldg(a.tabs + h);
+            const int sgn = popc(s[k] & cur.z0) << 31;
+            const double amp = __hiloint2double(__double2hiint(A) ^ sgn, __double2loint(A));
+            const uint32_t rk = __ldg(a.Rb0 + (uint32_t)(sb[k] ^ xb));
+            const double2 p = a.psi[rowoff + rk];
+            acc[k].x = fma(amp, p.x, acc[k].x);
+            acc[k].y = fma(amp, p.y, acc[k].y);
           }
         }
       }
@@ -395,7 +389,7 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   a.arow = arow;
   a.split_bk = op->d_splits;
   a.dim_bytes = s->dim * (int64_t)sizeof(double2);
-  a.Sa = s->d_Sa; a.Sb = s->d_Sb; a.Ra = s->d_Ra; a.Rb = s->d_Rb;
+  a.Sa = s->d_Sa; a.Sb = s->d_Sb; a.Ra = s->d_Ra; a.Rb = s->d_Rb; a.Rb0 = s->d_Rb0;
   a.buckets = op->d_buckets; a.n_buckets = (int)op->n_buckets;
   a.groups = op->d_groups; a.terms = op->d_terms; a.diag = op->d_diag;
   a.tabs = op->d_tabs; a.recs = op->d_recs; a.n_buckets_h = (int)op->n_buckets_h;
@@ -468,10 +462,14 @@ bool build_group_hash(const std::vector<Term>& terms, int t0, int t1, uint64_t x
     uint64_t t = 0;
     for (size_t i = 0; i < bits.size(); ++i)
       if ((m >> i) & 1u) t |= 1ull << bits[i];
-    if (__builtin_popcountll(t & amask) != ha || __builtin_popcountll(t & ~amask) != hb) continue;
+    // every pattern with an in-sector alpha part (K1 tests alpha per warp);
+    // out-of-sector beta patterns get A = 0, so K1 needs no per-lane beta test
+    if (__builtin_popcountll(t & amask) != ha) continue;
+    const bool bvalid = __builtin_popcountll(t & ~amask) == hb;
     double A = 0.0;
-    for (int q = t0; q < t1; ++q)
-      A += (__builtin_popcountll(t & (terms[q].z ^ z0)) & 1) ? -terms[q].c : terms[q].c;
+    if (bvalid)
+      for (int q = t0; q < t1; ++q)
+        A += (__builtin_popcountll(t & (terms[q].z ^ z0)) & 1) ? -terms[q].c : terms[q].c;
     pats.push_back(t);
     vals.push_back(A);
   }

@@ -111,6 +111,7 @@ struct hsv_sector_s {
   std::vector<uint32_t> Sa, Sb;     // host: compressed string of each rank
   std::vector<uint32_t> Ra, Rb;     // host: rank of each compressed string (or ~0u)
   uint32_t *d_Sa = nullptr, *d_Sb = nullptr, *d_Ra = nullptr, *d_Rb = nullptr;
+  uint32_t* d_Rb0 = nullptr;        // Rb with out-of-sector strings mapped to rank 0
   int64_t* d_perm = nullptr;        // internal row -> reference position
   int64_t* d_iperm = nullptr;       // reference position -> internal row
   int64_t* d_binom = nullptr;       // kBinomN x kBinomN

@@ -285,7 +285,7 @@ int hsv_sector_create(int n_qubits, int n_alpha, int n_beta, int ordering, hsv_s
   int rc = HSV_OK;
   auto fail = [&](int code) { hsv_sector_destroy(s); return code; };
   if ((rc = dalloc(&s->d_Sa, s->Na)) || (rc = dalloc(&s->d_Sb, s->Nb)) ||
-      (rc = dalloc(&s->d_Ra, nv)) || (rc = dalloc(&s->d_Rb, nv)) ||
+      (rc = dalloc(&s->d_Ra, nv)) || (rc = dalloc(&s->d_Rb, nv)) || (rc = dalloc(&s->d_Rb0, nv)) ||
       (rc = dalloc(&s->d_perm, s->dim)) || (rc = dalloc(&s->d_iperm, s->dim)) ||
       (rc = dalloc(&s->d_binom, kBinomN * kBinomN)) || (rc = dalloc(&s->d_spin, 64)) ||
       (rc = dalloc(&s->d_aslot, 64)) || (rc = dalloc(&s->d_bslot, 64)))
@@ -309,6 +309,10 @@ int hsv_sector_create(int n_qubits, int n_alpha, int n_beta, int ordering, hsv_s
   e = e ? e : cudaMemcpyAsync(s->d_Sb, s->Sb.data(), s->Nb * 4, cudaMemcpyHostToDevice, st);
   e = e ? e : cudaMemcpyAsync(s->d_Ra, s->Ra.data(), nv * 4ull, cudaMemcpyHostToDevice, st);
   e = e ? e : cudaMemcpyAsync(s->d_Rb, s->Rb.data(), nv * 4ull, cudaMemcpyHostToDevice, st);
+  std::vector<uint32_t> rb0(s->Rb);
+  for (auto& r : rb0)
+    if (r == ~0u) r = 0u;
+  e = e ? e : cudaMemcpy(s->d_Rb0, rb0.data(), nv * 4ull, cudaMemcpyHostToDevice);
   e = e ? e : cudaMemcpyAsync(s->d_binom, binom_host().c, sizeof(BinomTable), cudaMemcpyHostToDevice, st);
   e = e ? e : cudaMemcpyAsync(s->d_spin, spin.data(), 64, cudaMemcpyHostToDevice, st);
   e = e ? e : cudaMemcpyAsync(s->d_aslot, aslot.data(), 64 * 4, cudaMemcpyHostToDevice, st);
@@ -336,7 +340,7 @@ int hsv_sector_create(int n_qubits, int n_alpha, int n_beta, int ordering, hsv_s
 
 int hsv_sector_destroy(hsv_sector s) {
   if (!s) return HSV_OK;
-  dfree(s->d_Sa); dfree(s->d_Sb); dfree(s->d_Ra); dfree(s->d_Rb);
+  dfree(s->d_Sa); dfree(s->d_Sb); dfree(s->d_Ra); dfree(s->d_Rb); dfree(s->d_Rb0);
   dfree(s->d_perm); dfree(s->d_iperm); dfree(s->d_binom); dfree(s->d_spin);
   dfree(s->d_aslot); dfree(s->d_bslot);
   delete s;

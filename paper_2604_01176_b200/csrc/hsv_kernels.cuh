@@ -27,6 +27,7 @@ struct ApplyArgs {
   const uint32_t* Sb;
   const uint32_t* Ra;
   const uint32_t* Rb;
+  const uint32_t* Rb0;     // Rb with out-of-sector strings mapped to rank 0 (K1 pass 1)
   const int4* buckets;
   int n_buckets;
   int n_buckets_h;     // buckets [0, n_buckets_h) hold x-local (hashed) groups
