@@ -414,11 +414,12 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   int R = tuning().apply_r;
   const int M = tuning().apply_minb;
   if (R == 0) {
-    // auto: 4 rows per lane amortize group overhead better, but only if every
-    // warp still gets several units (else the tail of the static schedule wins)
+    // auto: 4 rows per lane amortize group overhead better, but only while
+    // there is at least one 128-row unit per resident warp (kbench: H12 full /
+    // half shard and H14 prefer 4, H12 quarter / eighth shards and H10 prefer 2)
     const int64_t units4 = (a_hi - a_lo) * ((s->Nb + 127) / 128);
     const int64_t warps4 = (int64_t)ctx().num_sms * 3 * 8;
-    R = units4 >= 6 * warps4 ? 4 : 2;
+    R = units4 >= warps4 ? 4 : 2;
   }
 #define HSV_APPLY_CASES(W, SH)                                              \
   if (R == 1) return launch_apply_t<W, SH, 1, 6>(a, n_warps);              \

@@ -6,7 +6,7 @@ namespace hsv {
 
 // Runtime tuning knobs (hsv_set_tuning); defaults are the measured best.
 struct Tuning {
-  int apply_r = 2;        // rows per lane in the K1 apply kernel (1, 2, 4; 0 = auto)
+  int apply_r = 0;        // rows per lane in the K1 apply kernel (1, 2, 4; 0 = auto)
   int apply_minb = 0;     // __launch_bounds__ min blocks/SM: 0 = default (R=2: 4, R=4: 3);
                           // alternatives R=2: 3 or 5, R=4: 2
   int screen_rows = 1024; // rows staged per chunk in the screen kernel
