@@ -186,6 +186,8 @@ struct hsv_pool_s {
   int4* d = nullptr;          // {oa, va, ob, vb} compressed masks
   int* d_order = nullptr;     // operators in alpha-part order (screen kernel)
   int2* d_opl = nullptr;      // per operator: beta list {offset, length}, length -1: empty beta half
+  int4* d_qa = nullptr;       // per screen slot q (alpha-part order): {oa, va, op, list offset}
+  int* d_qn = nullptr;        // per slot: beta list length (-1: empty beta half)
   int2* d_blist = nullptr;    // beta source lists {rb_src, rb_tgt}
   std::vector<int4> h;
 };

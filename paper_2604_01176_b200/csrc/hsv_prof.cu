@@ -158,6 +158,8 @@ int hsv_pool_destroy(hsv_pool p) {
   dfree(p->d);
   dfree(p->d_order);
   dfree(p->d_opl);
+  dfree(p->d_qa);
+  dfree(p->d_qn);
   dfree(p->d_blist);
   delete p;
   return HSV_OK;

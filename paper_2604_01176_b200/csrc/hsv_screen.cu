@@ -35,6 +35,8 @@ struct ScreenArgs {
   const uint32_t* Ra;
   const int4* ops;       // {oa, va, ob, vb} (compressed)
   const int* order;      // operator indices in alpha-part order
+  const int4* qa;        // per slot: {oa, va, op, beta list offset}
+  const int* qn;         // per slot: beta list length (-1: empty beta half)
   const int2* opl;       // per operator: {beta list offset, length}; length < 0: empty beta half
   const int2* blist;     // beta source lists: {rb_src, rb_tgt}
   int n_ops;
@@ -60,10 +62,21 @@ __global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
   const double2* __restrict__ wrow = a.w + ra * a.Nb;
   const int stride = a.slices * kScreenWarps;
   const bool w_zero = a.w_arow && !__ldg(a.w_arow + ra);   // own rows all zero
-  for (int q = blockIdx.x * kScreenWarps + warp; q < a.n_ops; q += stride) {
-    const int op = __ldg(a.order + q);
-    const int4 O = __ldg(a.ops + op);
-    const uint32_t oa = (uint32_t)O.x, va = (uint32_t)O.y;
+  // per-slot records in screen order, the next one loaded while the current
+  // operator's list is walked (the per-operator setup was a chain of dependent
+  // loads: order -> masks -> partner rank -> flag -> list)
+  int q = blockIdx.x * kScreenWarps + warp;
+  int4 Qn = q < a.n_ops ? __ldg(a.qa + q) : make_int4(0, 0, 0, 0);
+  int Ln = q < a.n_ops ? __ldg(a.qn + q) : 0;
+  for (; q < a.n_ops; q += stride) {
+    const int4 Q = Qn;
+    const int Ly = Ln;
+    if (q + stride < a.n_ops) {
+      Qn = __ldg(a.qa + q + stride);
+      Ln = __ldg(a.qn + q + stride);
+    }
+    const int op = Q.z;
+    const uint32_t oa = (uint32_t)Q.x, va = (uint32_t)Q.y;
     const uint32_t fa = oa | va;
     const uint32_t ma = sa & fa;
     const bool as = ma == oa, at = ma == va;   // both for an empty alpha half
@@ -75,7 +88,7 @@ __global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
       // (0.87 -> 0.76 ms at H12)
       const uint32_t poff = ra2 * (uint32_t)a.Nb;
       const double2* __restrict__ prow = a.psi + poff;
-      const int2 L = __ldg(a.opl + op);
+      const int2 L = make_int2(Q.w, Ly);
       if (L.y < 0) {
         // empty beta half: every beta string is both source and target (alpha decides)
         for (int64_t j = lane; j < a.Nb; j += 32) g += re_conj_mul(wrow[j], prow[j]);
@@ -168,8 +181,18 @@ int pool_prepare(hsv_pool_s* p) {
     const uint32_t fx = (uint32_t)(p->h[x].x | p->h[x].y), fy = (uint32_t)(p->h[y].x | p->h[y].y);
     return fx != fy ? fx < fy : (uint32_t)p->h[x].x < (uint32_t)p->h[y].x;
   });
+  // per-slot records in screen order: no dependent order -> op -> masks chain
+  std::vector<int4> qa(n);
+  std::vector<int> qn(n);
+  for (int64_t q = 0; q < n; ++q) {
+    const int op = order[q];
+    qa[q] = make_int4(p->h[op].x, p->h[op].y, op, opl[op].x);
+    qn[q] = opl[op].y;
+  }
   HSV_TRY(dalloc(&p->d_order, n));
   HSV_TRY(dalloc(&p->d_opl, n));
+  HSV_TRY(dalloc(&p->d_qa, n));
+  HSV_TRY(dalloc(&p->d_qn, n));
   HSV_TRY(dalloc(&p->d_blist, total));
   int4* d_pats = nullptr;
   HSV_TRY(dalloc(&d_pats, pats.size()));
@@ -177,6 +200,8 @@ int pool_prepare(hsv_pool_s* p) {
   if (n) {
     HSV_TRY_CUDA(cudaMemcpyAsync(p->d_order, order.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
     HSV_TRY_CUDA(cudaMemcpyAsync(p->d_opl, opl.data(), n * sizeof(int2), cudaMemcpyHostToDevice, st));
+    HSV_TRY_CUDA(cudaMemcpyAsync(p->d_qa, qa.data(), n * sizeof(int4), cudaMemcpyHostToDevice, st));
+    HSV_TRY_CUDA(cudaMemcpyAsync(p->d_qn, qn.data(), n * sizeof(int), cudaMemcpyHostToDevice, st));
   }
   if (!pats.empty()) {
     HSV_TRY_CUDA(cudaMemcpyAsync(d_pats, pats.data(), pats.size() * sizeof(int4), cudaMemcpyHostToDevice, st));
@@ -211,6 +236,7 @@ int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
   ScreenArgs a{};
   a.Sa = s->d_Sa; a.Ra = s->d_Ra;
   a.ops = pool->d; a.order = pool->d_order; a.opl = pool->d_opl; a.blist = pool->d_blist;
+  a.qa = pool->d_qa; a.qn = pool->d_qn;
   a.n_ops = n_ops; a.psi = psi; a.w = w; a.Nb = s->Nb; a.a_lo = a_lo; a.slices = slices;
   a.part = part;
   a.psi_arow = psi_arow;
