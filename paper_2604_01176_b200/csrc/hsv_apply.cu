@@ -414,16 +414,20 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   int R = tuning().apply_r;
   const int M = tuning().apply_minb;
   if (R == 0) {
-    // auto: 4 rows per lane amortize group overhead better, but only while
-    // there is at least one 128-row unit per resident warp (kbench: H12 full /
-    // half shard and H14 prefer 4, H12 quarter / eighth shards and H10 prefer 2)
+    // auto: more rows per lane amortize the per-group overhead and keep more
+    // independent gathers in flight, but only while every resident warp still
+    // gets a unit (kbench: 8 rows win at H12 full / half shard, H14 and H16 by
+    // 4-13%; the H12 quarter / eighth shards and H10 keep 2)
+    const int64_t units8 = (a_hi - a_lo) * ((s->Nb + 255) / 256);
+    const int64_t warps8 = (int64_t)ctx().num_sms * 2 * 8;
     const int64_t units4 = (a_hi - a_lo) * ((s->Nb + 127) / 128);
     const int64_t warps4 = (int64_t)ctx().num_sms * 3 * 8;
-    R = units4 >= warps4 ? 4 : 2;
+    R = 4 * units8 >= 3 * warps8 ? 8 : units4 >= warps4 ? 4 : 2;
   }
 #define HSV_APPLY_CASES(W, SH)                                              \
   if (R == 1) return launch_apply_t<W, SH, 1, 6>(a, n_warps);              \
   if (R == 4 && M == 2) return launch_apply_t<W, SH, 4, 2>(a, n_warps);    \
+  if (R == 8) return launch_apply_t<W, SH, 8, 2>(a, n_warps);              \
   if (R == 4) return launch_apply_t<W, SH, 4, 3>(a, n_warps);              \
   if (M == 3) return launch_apply_t<W, SH, 2, 3>(a, n_warps);              \
   if (M == 5) return launch_apply_t<W, SH, 2, 5>(a, n_warps);              \

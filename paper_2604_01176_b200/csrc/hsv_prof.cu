@@ -57,8 +57,8 @@ int hsv_set_tuning(const char* key, int64_t value) {
   HSV_REQUIRE(key, HSV_ERR_INVALID, "null key");
   const std::string k(key);
   if (k == "apply_r") {
-    HSV_REQUIRE(value == 0 || value == 1 || value == 2 || value == 4, HSV_ERR_INVALID,
-                "apply_r must be 0 (auto), 1, 2 or 4");
+    HSV_REQUIRE(value == 0 || value == 1 || value == 2 || value == 4 || value == 8,
+                HSV_ERR_INVALID, "apply_r must be 0 (auto), 1, 2, 4 or 8");
     g_tuning.apply_r = (int)value;
   } else if (k == "apply_minb") {
     HSV_REQUIRE(value >= 0 && value <= 6, HSV_ERR_INVALID, "apply_minb must be in [0, 6]");
