@@ -336,10 +336,12 @@ static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
   int S = tuning().apply_split;
   if (S <= 0) {
     S = 1;
-    // at most 4 (S = 8 lost on the H12 full / half / quarter shards), unless even
-    // S = 4 leaves fewer than two units per warp (H12 eighth shard: S = 8 0.48 ms
-    // against S = 4 0.54 ms; kbench --shard 8)
-    while (S < 4 && units1 * S < 8 * max_warps) S *= 2;
+    // With 2 rows per lane at most 4 (S = 8 lost on the H12 quarter shard),
+    // unless even S = 4 leaves fewer than two units per warp (H12 eighth shard:
+    // S = 8 0.48 against 0.54 ms).  With 8 rows per lane (few, long units) up
+    // to 8 (H12 full: 2.71 against 2.78 ms; kbench --split).
+    const int smax = R >= 8 ? 8 : 4;
+    while (S < smax && units1 * S < 8 * max_warps) S *= 2;
     if (units1 * S < 2 * max_warps) S = 8;
   }
   if (!a0.split_bk) S = 1;
