@@ -180,8 +180,26 @@ class SvAdaptEngine:
         return self.matrix.expect(state)
 
     def energy_and_gradient(self, ops, thetas):
+        """Adjoint energy + gradient (svengine.py:260-281) on two device states
+        kept across L-BFGS evaluations (no per-call state allocation)."""
+        from . import _native as N
+        from .svengine import DeviceState
         occ, virt = self._pool_masks(ops)
-        return self.matrix.energy_gradient(self.system.hf.bits, occ, virt, thetas)
+        if getattr(self, "_eg_states", None) is None:
+            self._eg_states = (DeviceState(self.basis), DeviceState(self.basis))
+        psi, w = self._eg_states
+        th = np.ascontiguousarray(thetas, dtype=np.float64)
+        cs, sn = N.as_f64(np.cos(th)), N.as_f64(np.sin(th))
+        na = self.basis._sector.n_alpha_strings
+        N.call("hsv_eg_forward_async", self.matrix.handle, int(self.system.hf.bits),
+               N.ptr_u64(occ), N.ptr_u64(virt), N.ptr_f64(cs), N.ptr_f64(sn), th.size,
+               0, na, psi.handle, w.handle)
+        g = np.empty(th.size)
+        e = N.dbl()
+        N.call("hsv_eg_backward", self.matrix.handle, psi.handle, w.handle, N.ptr_u64(occ),
+               N.ptr_u64(virt), N.ptr_f64(cs), N.ptr_f64(sn), th.size, N.C.byref(e),
+               N.ptr_f64(g))
+        return float(e.value), g
 
     def _device_pool(self, pool):
         seq = getattr(pool, "ops", pool)
