@@ -137,10 +137,20 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
   // alpha row and the same bucket range at the same time and share the partner
   // rows they gather in L1 (and in L2 when psi is far larger than L2).
   // Contiguous unit blocks per warp remain as a tuning alternative.
-  const uint32_t u_begin = a.interleave ? gw : (uint32_t)((uint64_t)gw * units / tw);
+  // Dynamic (default, interleave == 2): a warp takes the next work unit from
+  // a global counter when it finishes one.  Units are still handed out in
+  // order, so the warps of an SM stay on neighbouring units, but a slow unit no
+  // longer holds up a fixed share of later ones (H12 2.71 -> 2.39 ms, H14 -11%).
+  const bool dyn = a.interleave == 2;
+  auto grab = [&]() -> uint32_t {
+    uint32_t v = 0;
+    if (lane == 0) v = atomicAdd(a.ucounter, 1u);
+    return __shfl_sync(0xffffffffu, v, 0);
+  };
+  const uint32_t u_begin = dyn ? grab() : a.interleave ? gw : (uint32_t)((uint64_t)gw * units / tw);
   const uint32_t u_end = a.interleave ? units : (uint32_t)((uint64_t)(gw + 1) * units / tw);
   const uint32_t u_step = a.interleave ? tw : 1u;
-  for (uint32_t uw = u_begin; uw < u_end; uw += u_step) {
+  for (uint32_t uw = u_begin; uw < u_end; uw = dyn ? grab() : uw + u_step) {
     // a work unit = (row unit, bucket split), split-major: neighbouring work
     // units are neighbouring row units with the same bucket range (measured
     // -6% at H12 against unit-major)
@@ -287,13 +297,15 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
       }
       er = warp_sum(er);
       ei = warp_sum(ei);
-      if (lane == 0) {
+      if (dyn) {   // which warp ran a unit varies: per-unit partials, summed in unit order
+        if (lane == 0) { a.upart[2 * uw] = er; a.upart[2 * uw + 1] = ei; }
+      } else if (lane == 0) {
         esh[threadIdx.x >> 5][0] += er;
         esh[threadIdx.x >> 5][1] += ei;
       }
     }
   }
-  if (a.epart && lane == 0) {
+  if (a.epart && lane == 0 && !dyn) {
     a.epart[2 * gw] = esh[threadIdx.x >> 5][0];
     a.epart[2 * gw + 1] = esh[threadIdx.x >> 5][1];
   }
@@ -348,14 +360,26 @@ static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
   a.nsplit = S;
   a.split_bk = S == 1 ? nullptr : a0.split_bk + (S == 2 ? 0 : S == 4 ? 3 : 8);
   // interleaved unless forced off (measured best at H12 and H14)
-  const int il = tuning().apply_interleave;   // -1 auto, 0 off, 1 on
-  a.interleave = il != 0;
+  const int il = tuning().apply_interleave;   // -1 auto (= 2), 0 contiguous, 1 interleaved, 2 dynamic
+  a.interleave = il < 0 ? 2 : il;
   a.units = units1 * S;
   int64_t grid = max_warps / 8;
   const int64_t need = (a.units + 7) / 8;
   grid = std::max<int64_t>(1, std::min(grid, need));
   if (n_warps_out) *n_warps_out = grid * 8;
   if (a.units == 0) return HSV_OK;
+  unsigned int* ucounter = nullptr;
+  double* upart = nullptr;
+  if (a.interleave == 2) {
+    HSV_TRY(dalloc(&ucounter, 1));
+    HSV_TRY_CUDA(cudaMemsetAsync(ucounter, 0, sizeof(unsigned), stream()));
+    a.ucounter = ucounter;
+    if (a.epart) {
+      HSV_TRY(dalloc(&upart, 2 * a.units));
+      a.upart = upart;
+    }
+    if (n_warps_out) *n_warps_out = 1;   // the unit partials are reduced into epart[0..1] below
+  }
   const int64_t rows = (a.a_hi - a.a_lo) * a.Nb;
   double2* ypart = nullptr;
   if (S > 1 && a.out) {
@@ -372,6 +396,9 @@ static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
   }
   count_launch(ypart ? 2 : 1);
   HSV_CHECK_LAUNCH();
+  if (upart) HSV_TRY(reduce_sum_f64(upart, a.units, 2, 2, a.epart));
+  dfree(upart);
+  dfree(ucounter);
   dfree(ypart);
   return HSV_OK;
 }
@@ -417,14 +444,15 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   const int M = tuning().apply_minb;
   if (R == 0) {
     // auto: more rows per lane amortize the per-group overhead and keep more
-    // independent gathers in flight, but only while every resident warp still
-    // gets a unit (kbench: 8 rows win at H12 full / half shard, H14 and H16 by
-    // 4-13%; the H12 quarter / eighth shards and H10 keep 2)
+    // independent gathers in flight; with the dynamic schedule 8 rows win down
+    // to the H12 quarter shard (924 units of 256 rows: 0.70 against 0.78 ms),
+    // while the eighth shard (464 units) and H10 keep 2 (kbench --shard)
     const int64_t units8 = (a_hi - a_lo) * ((s->Nb + 255) / 256);
     const int64_t warps8 = (int64_t)ctx().num_sms * 2 * 8;
     const int64_t units4 = (a_hi - a_lo) * ((s->Nb + 127) / 128);
     const int64_t warps4 = (int64_t)ctx().num_sms * 3 * 8;
-    R = 4 * units8 >= 3 * warps8 ? 8 : units4 >= warps4 ? 4 : 2;
+    const bool dyn = tuning().apply_interleave < 0 || tuning().apply_interleave == 2;
+    R = (dyn ? 3 * units8 >= warps8 : 4 * units8 >= 3 * warps8) ? 8 : units4 >= warps4 ? 4 : 2;
   }
 #define HSV_APPLY_CASES(W, SH)                                              \
   if (R == 1) return launch_apply_t<W, SH, 1, 6>(a, n_warps);              \

@@ -11,7 +11,7 @@ struct Tuning {
                           // alternatives R=2: 3 or 5, R=4: 2
   int screen_rows = 1024; // rows staged per chunk in the screen kernel
   int apply_split = 0;    // bucket splits per row unit in K1 (0 = auto, else 1/2/4/8)
-  int apply_interleave = -1;  // K1 unit schedule: -1 auto (= interleaved), 0 contiguous, 1 interleaved
+  int apply_interleave = -1;  // K1 unit schedule: -1 auto (= 2), 0 contiguous, 1 interleaved, 2 dynamic
   int push = -1;          // sparse-psi push path: -1 auto, 0 off, 1 whenever it fits in memory
   int push_keys = 32;     // auto: push while nnz(psi) * (1 + groups) <= push_keys * rows - 2^20
   int sweep = 1;          // adjoint/forward sweeps: 1 one cooperative launch, 0 launch per op
@@ -57,6 +57,8 @@ struct ApplyArgs {
   int64_t part_stride;
   double prune;
   int energy_only;
+  unsigned int* ucounter;     // dynamic schedule: next work unit
+  double* upart;              // dynamic schedule: [units][2] energy partials
   double2* const* peer_rows;  // device array: other ranks' w buffers (NVLink), or nullptr
   int n_peer_rows;
 };

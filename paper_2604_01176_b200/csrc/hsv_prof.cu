@@ -64,7 +64,8 @@ int hsv_set_tuning(const char* key, int64_t value) {
     HSV_REQUIRE(value >= 0 && value <= 6, HSV_ERR_INVALID, "apply_minb must be in [0, 6]");
     g_tuning.apply_minb = (int)value;
   } else if (k == "apply_interleave") {
-    HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "apply_interleave must be -1, 0 or 1");
+    HSV_REQUIRE(value >= -1 && value <= 2, HSV_ERR_INVALID,
+                "apply_interleave must be -1, 0, 1 or 2");
     g_tuning.apply_interleave = (int)value;
   } else if (k == "apply_split") {
     HSV_REQUIRE(value == 0 || value == 1 || value == 2 || value == 4 || value == 8,
