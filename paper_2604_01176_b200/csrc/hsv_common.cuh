@@ -60,6 +60,7 @@ struct Context {
   cudaStream_t stream = nullptr;   // stream all work goes to
   cudaStream_t own = nullptr;      // library-owned stream
   int num_sms = 148;
+  int64_t l2_bytes = 126ll << 20;
   int64_t launches = 0;
   // set by hsv_eg_forward_peer_async around its H application: K1 also stores
   // every output row into these peer buffers (NVLink), see ApplyArgs::peer_rows

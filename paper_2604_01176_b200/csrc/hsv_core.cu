@@ -198,6 +198,7 @@ int hsv_init(int device) {
               "libhsv is built for sm_100a (B200); device %d is sm_%d%d", device, prop.major,
               prop.minor);
   g_ctx.num_sms = prop.multiProcessorCount;
+  g_ctx.l2_bytes = prop.l2CacheSize;
   if (!g_ctx.own) HSV_TRY_CUDA(cudaStreamCreateWithFlags(&g_ctx.own, cudaStreamNonBlocking));
   g_ctx.stream = g_ctx.own;
   g_ctx.device = device;

@@ -54,6 +54,10 @@ __device__ __forceinline__ double re_conj_mul(double2 a, double2 b) {
   return a.x * b.x + a.y * b.y;   // Re(conj(a) b)
 }
 
+// D list entries per lane in flight: 2 (44 registers) while psi sits in L2, 4
+// (54 registers, fewer resident warps) once the gathers go to DRAM: H12 0.72 vs
+// 0.77 ms with 2, H16 0.68 vs 0.59 s with 4; 8 spills.
+template <int D>
 __global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t rloc = blockIdx.y;
@@ -85,7 +89,7 @@ __global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
     if ((as || at) && !w_zero && !(a.psi_arow && !__ldg(a.psi_arow + ra2))) {
       // 32-bit row offsets (dim < 2^32, checked by K1) and two list entries per
       // lane in flight: independent gathers instead of one latency per entry
-      // (0.87 -> 0.76 ms at H12)
+      // (0.87 -> 0.72 ms at H12)
       const uint32_t poff = ra2 * (uint32_t)a.Nb;
       const double2* __restrict__ prow = a.psi + poff;
       const int2 L = make_int2(Q.w, Ly);
@@ -101,18 +105,18 @@ __global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
           if (!(side == 0 ? as : at)) continue;
           double g4[4] = {0.0, 0.0, 0.0, 0.0};
           int j = lane;
-          for (; j + 32 < L.y; j += 64) {   // 2 in flight: 36 registers (4: 54, 8: spills)
-            int2 e[2];
+          for (; j + 32 * (D - 1) < L.y; j += 32 * D) {
+            int2 e[D];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) e[q] = __ldg(lst + j + 32 * q);
-            double2 wv[2], pv[2];
+            for (int q = 0; q < D; ++q) e[q] = __ldg(lst + j + 32 * q);
+            double2 wv[D], pv[D];
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
+            for (int q = 0; q < D; ++q) {
               wv[q] = wrow[side == 0 ? e[q].x : e[q].y];
               pv[q] = prow[side == 0 ? e[q].y : e[q].x];
             }
 #pragma unroll
-            for (int q = 0; q < 2; ++q) g4[q] += re_conj_mul(wv[q], pv[q]);
+            for (int q = 0; q < D; ++q) g4[q] += re_conj_mul(wv[q], pv[q]);
           }
           for (; j < L.y; j += 32) {
             const int2 e = __ldg(lst + j);
@@ -243,7 +247,11 @@ int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
   a.w_arow = w_arow;
   {
     ProfScope prof("screen");
-    k_screen<<<dim3((unsigned)slices, (unsigned)rows), kScreenBlock, 0, stream()>>>(a);
+    const dim3 grid((unsigned)slices, (unsigned)rows);
+    if (2 * s->dim * (int64_t)sizeof(double2) > ctx().l2_bytes)
+      k_screen<4><<<grid, kScreenBlock, 0, stream()>>>(a);
+    else
+      k_screen<2><<<grid, kScreenBlock, 0, stream()>>>(a);
   }
   count_launch();
   HSV_CHECK_LAUNCH();
