@@ -157,8 +157,8 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
     const uint32_t units1 = units / (uint32_t)a.nsplit;
     const int sp = (int)(uw / units1);
     const uint32_t u = uw - (uint32_t)sp * units1;
-    const int bk0 = a.nsplit > 1 ? __ldg(a.split_bk + sp) : 0;
-    const int bk1 = a.nsplit > 1 ? __ldg(a.split_bk + sp + 1) : a.n_buckets;
+    const int bk0 = a.split_bk ? __ldg(a.split_bk + sp) : 0;
+    const int bk1 = a.split_bk ? __ldg(a.split_bk + sp + 1) : a.n_buckets;
     const uint32_t ur = u / (uint32_t)a.upr;
     const uint32_t ra = (uint32_t)a.a_lo + ur;
     const uint32_t rb0 = (u - ur * (uint32_t)a.upr) * (32 * R) + lane;
@@ -334,8 +334,21 @@ void launch_combine_splits(const double2* part, int S, int64_t rows, double2* ou
                                                                            prune, peers, n_peers);
 }
 
+// Point a launch at the split table for S parts (virtual buckets + cuts).
+void use_split_table(const hsv_op_s* op, int St, ApplyArgs& a) {
+  if (St <= 1) {
+    a.split_bk = nullptr;
+    return;
+  }
+  const SplitTable& T = op->split[__builtin_ctz((unsigned)St) - 1];
+  a.buckets = op->d_vbuckets + T.vb_off;
+  a.n_buckets = T.nb;
+  a.n_buckets_h = T.nbh;
+  a.split_bk = op->d_splits + T.cut_off;
+}
+
 template <typename W, int SH, int R, int MINB>
-static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
+static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_warps_out) {
   ApplyArgs a = a0;
   a.upr = (int)((a.Nb + 32 * R - 1) / (32 * R));
   const int64_t units1 = (a.a_hi - a.a_lo) * a.upr;
@@ -343,22 +356,23 @@ static int launch_apply_t(const ApplyArgs& a0, int64_t* n_warps_out) {
   HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<W, SH, R, MINB>, 256, 0));
   occ = std::max(occ, 1);
   const int64_t max_warps = (int64_t)ctx().num_sms * occ * 8;
-  // Split the bucket range of each row unit when row units alone cannot give
-  // every warp several units (small problems, or a rank's shard at N > 1).
+  // Split the bucket range of each row unit.  Split-major unit order keeps the
+  // warps of the machine on one bucket range at a time (tables and partner rows
+  // shared in L1/L2), so 8 parts win even when row units are plentiful (H14
+  // 57.3 against 57.9 ms unsplit, H16 1.40 against 1.43 s); more parts, up to
+  // 32, while that leaves fewer than 8 units per warp (rank shards: H12 / 8
+  // 0.354 against 0.42 ms with the earlier at-most-8 rule).  Capped so the
+  // partial rows stay under 32 GB.
   int S = tuning().apply_split;
   if (S <= 0) {
-    S = 1;
-    // With 2 rows per lane at most 4 (S = 8 lost on the H12 quarter shard),
-    // unless even S = 4 leaves fewer than two units per warp (H12 eighth shard:
-    // S = 8 0.48 against 0.54 ms).  With 8 rows per lane (few, long units) up
-    // to 8 (H12 full: 2.71 against 2.78 ms; kbench --split).
-    const int smax = R >= 8 ? 8 : 4;
-    while (S < smax && units1 * S < 8 * max_warps) S *= 2;
-    if (units1 * S < 2 * max_warps) S = 8;
+    S = 8;
+    while (S < 32 && units1 * S < 8 * max_warps) S *= 2;
+    const int64_t rows_all = (a.a_hi - a.a_lo) * a.Nb;
+    while (S > 1 && a.out && S * rows_all * (int64_t)sizeof(double2) > (32ll << 30)) S /= 2;
   }
   if (!a0.split_bk) S = 1;
   a.nsplit = S;
-  a.split_bk = S == 1 ? nullptr : a0.split_bk + (S == 2 ? 0 : S == 4 ? 3 : 8);
+  use_split_table(op, S, a);
   // interleaved unless forced off (measured best at H12 and H14)
   const int il = tuning().apply_interleave;   // -1 auto (= 2), 0 contiguous, 1 interleaved, 2 dynamic
   a.interleave = il < 0 ? 2 : il;
@@ -444,25 +458,25 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   const int M = tuning().apply_minb;
   if (R == 0) {
     // auto: more rows per lane amortize the per-group overhead and keep more
-    // independent gathers in flight; with the dynamic schedule 8 rows win down
-    // to the H12 quarter shard (924 units of 256 rows: 0.70 against 0.78 ms),
-    // while the eighth shard (464 units) and H10 keep 2 (kbench --shard)
+    // independent gathers in flight; with the dynamic schedule and up to 32
+    // bucket splits 8 rows win whenever there is a unit per warp (H12 sixteenth
+    // shard 0.207 against 0.215 ms with 2, H10 0.126 against 0.14 ms)
     const int64_t units8 = (a_hi - a_lo) * ((s->Nb + 255) / 256);
     const int64_t warps8 = (int64_t)ctx().num_sms * 2 * 8;
     const int64_t units4 = (a_hi - a_lo) * ((s->Nb + 127) / 128);
     const int64_t warps4 = (int64_t)ctx().num_sms * 3 * 8;
     const bool dyn = tuning().apply_interleave < 0 || tuning().apply_interleave == 2;
-    R = (dyn ? 3 * units8 >= warps8 : 4 * units8 >= 3 * warps8) ? 8 : units4 >= warps4 ? 4 : 2;
+    R = (dyn ? 32 * units8 >= warps8 : 4 * units8 >= 3 * warps8) ? 8 : units4 >= warps4 ? 4 : 2;
   }
 #define HSV_APPLY_CASES(W, SH)                                              \
-  if (R == 1) return launch_apply_t<W, SH, 1, 6>(a, n_warps);              \
-  if (R == 4 && M == 2) return launch_apply_t<W, SH, 4, 2>(a, n_warps);    \
-  if (R == 8) return launch_apply_t<W, SH, 8, 2>(a, n_warps);              \
-  if (R == 4) return launch_apply_t<W, SH, 4, 3>(a, n_warps);              \
-  if (M == 3) return launch_apply_t<W, SH, 2, 3>(a, n_warps);              \
-  if (M == 5) return launch_apply_t<W, SH, 2, 5>(a, n_warps);              \
-  if (M == 6) return launch_apply_t<W, SH, 2, 6>(a, n_warps);              \
-  return launch_apply_t<W, SH, 2, 4>(a, n_warps);
+  if (R == 1) return launch_apply_t<W, SH, 1, 6>(op, a, n_warps);              \
+  if (R == 4 && M == 2) return launch_apply_t<W, SH, 4, 2>(op, a, n_warps);    \
+  if (R == 8) return launch_apply_t<W, SH, 8, 2>(op, a, n_warps);              \
+  if (R == 4) return launch_apply_t<W, SH, 4, 3>(op, a, n_warps);              \
+  if (M == 3) return launch_apply_t<W, SH, 2, 3>(op, a, n_warps);              \
+  if (M == 5) return launch_apply_t<W, SH, 2, 5>(op, a, n_warps);              \
+  if (M == 6) return launch_apply_t<W, SH, 2, 6>(op, a, n_warps);              \
+  return launch_apply_t<W, SH, 2, 4>(op, a, n_warps);
   if (s->wide) { HSV_APPLY_CASES(uint64_t, 32) }
   HSV_APPLY_CASES(uint32_t, 16)
 #undef HSV_APPLY_CASES
@@ -801,28 +815,75 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
       }
     }
   }
-  // bucket split boundaries (S = 2, 4, 8) balancing an estimated per-group cost
-  std::vector<int> splits;
+  // Split tables (S = 2, 4, 8, 16, 32) cutting the group range at equal
+  // estimated cost, inside buckets where needed: a bucket cut in two becomes two
+  // "virtual" buckets with the same alpha flip and disjoint group ranges, so the
+  // kernel loops stay bucket-granular.  Cost per group: 1 (hashed) or
+  // 1 + terms / 8, times the fraction of alpha strings for which the bucket's
+  // alpha flip stays in the sector (C(k, y) C(norb - k, na - y) / C(norb, na)
+  // for a flip of k orbitals needing y occupied).  Unweighted bucket cuts left
+  // the parts of an 8-way bucket split 1.5x apart in time (H12).
+  std::vector<int4> vbk;
+  std::vector<int> cuts;
   {
-    std::vector<double> cum(op->buckets.size() + 1, 0.0);
-    for (size_t b = 0; b < op->buckets.size(); ++b) {
-      double c = 0.0;
-      for (int q = op->buckets[b].z; q < op->buckets[b].w; ++q)
-        c += ghash[q].tab >= 0 ? 1.0 : 1.0 + (op->groups[q].w - op->groups[q].z) / 8.0;
-      cum[b + 1] = cum[b] + c;
-    }
+    auto binom = [](int n, int k) -> double {
+      if (k < 0 || k > n) return 0.0;
+      double r = 1.0;
+      for (int i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+      return r;
+    };
+    const int na = s->n_alpha, no = s->norb;
+    const double call = binom(no, na);
     const int nb = (int)op->buckets.size();
-    for (int S : {2, 4, 8}) {
-      int prev = 0;
-      splits.push_back(0);
-      for (int k = 1; k < S; ++k) {
-        const double target = cum[nb] * k / S;
-        int b = prev;
-        while (b < nb && cum[b] < target) ++b;
-        splits.push_back(b);
-        prev = b;
+    const int ng = nb ? op->buckets[nb - 1].w : 0;
+    std::vector<int> gb(ng, 0);   // bucket of each group (buckets own consecutive ranges)
+    std::vector<double> cum(ng + 1, 0.0), cum0(ng + 1, 0.0);
+    for (int b = 0; b < nb; ++b) {
+      const int4 B = op->buckets[b];
+      const int k = __builtin_popcount((uint32_t)B.x);
+      const double frac = binom(k, B.y) * binom(no - k, na - B.y) / call;
+      for (int q = B.z; q < B.w; ++q) {
+        gb[q] = b;
+        const double c = ghash[q].tab >= 0 ? 1.0 : 1.0 + (op->groups[q].w - op->groups[q].z) / 8.0;
+        cum[q + 1] = cum[q] + frac * c + (q == B.z ? 0.01 : 0.0);
+        cum0[q + 1] = cum0[q] + c;
       }
-      splits.push_back(nb);
+    }
+    for (int li = 0; li < kSplitTables; ++li) {
+      const int S = 2 << li;
+      std::vector<int> cut(S + 1, ng);
+      cut[0] = 0;
+      if (S <= 8) {
+        // up to 8 parts: bucket boundaries by unweighted group cost, the cut
+        // measured best at full size (H12 2.39 against 2.42 ms weighted)
+        for (int k = 1, b = 0; k < S; ++k) {
+          const double target = cum0[ng] * k / S;
+          while (b < nb && cum0[op->buckets[b].z] < target) ++b;
+          cut[k] = b < nb ? op->buckets[b].z : ng;
+        }
+      } else {
+        for (int k = 1, g = 0; k < S; ++k) {
+          const double target = cum[ng] * k / S;
+          while (g < ng && cum[g] < target) ++g;
+          cut[k] = g;
+        }
+      }
+      SplitTable& T = op->split[li];
+      T.vb_off = (int)vbk.size();
+      T.cut_off = (int)cuts.size();
+      T.nbh = 0;
+      for (int k = 0; k < S; ++k) {
+        cuts.push_back((int)vbk.size() - T.vb_off);
+        for (int g0 = cut[k]; g0 < cut[k + 1];) {   // pieces of buckets inside [cut k, cut k+1)
+          const int4 B = op->buckets[gb[g0]];
+          const int g1 = std::min(B.w, cut[k + 1]);
+          vbk.push_back(make_int4(B.x, B.y, g0, g1));
+          if (gb[g0] < op->n_buckets_h) ++T.nbh;
+          g0 = g1;
+        }
+      }
+      T.nb = (int)vbk.size() - T.vb_off;
+      cuts.push_back(T.nb);
     }
   }
   std::vector<unsigned char> recs;
@@ -852,7 +913,7 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
       (rc = dalloc(&op->d_terms, op->terms.size())) ||
       (rc = dalloc(&op->d_ghash, ghash.size())) || (rc = dalloc(&op->d_tabs, tabs.size())) ||
       (rc = dalloc(reinterpret_cast<unsigned char**>(&op->d_recs), recs.size())) ||
-      (rc = dalloc(&op->d_splits, splits.size())) || (rc = dalloc(&op->d_gsz, gsz.size())) ||
+      (rc = dalloc(&op->d_splits, cuts.size())) || (rc = dalloc(&op->d_vbuckets, vbk.size())) || (rc = dalloc(&op->d_gsz, gsz.size())) ||
       (rc = dalloc(reinterpret_cast<SzTerm**>(&op->d_szt), szt.size())) ||
       (rc = dalloc(&op->d_gxa, gxa.size())))
     return fail(rc);
@@ -866,7 +927,9 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
   if (!szt.empty())
     HSV_TRY_CUDA(cudaMemcpyAsync(op->d_szt, szt.data(), szt.size() * sizeof(SzTerm),
                                  cudaMemcpyHostToDevice, st));
-  HSV_TRY_CUDA(cudaMemcpyAsync(op->d_splits, splits.data(), splits.size() * sizeof(int),
+  HSV_TRY_CUDA(cudaMemcpyAsync(op->d_vbuckets, vbk.data(), vbk.size() * sizeof(int4),
+                               cudaMemcpyHostToDevice, stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(op->d_splits, cuts.data(), cuts.size() * sizeof(int),
                                cudaMemcpyHostToDevice, st));
   if (!recs.empty())
     HSV_TRY_CUDA(cudaMemcpyAsync(op->d_recs, recs.data(), recs.size(), cudaMemcpyHostToDevice, st));
@@ -901,6 +964,7 @@ int hsv_op_destroy(hsv_op op) {
   dfree(op->d_tabs);
   dfree(reinterpret_cast<unsigned char*>(op->d_recs));
   dfree(op->d_splits);
+  dfree(op->d_vbuckets);
   dfree(op->d_gsz);
   dfree(reinterpret_cast<SzTerm*>(op->d_szt));
   dfree(op->d_gxa);

@@ -292,7 +292,7 @@ int launch_apply_staged(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_warp
   }
   if (!a0.split_bk) S = 1;
   sa.a.nsplit = S;
-  sa.a.split_bk = S == 1 ? nullptr : a0.split_bk + (S == 2 ? 0 : S == 4 ? 3 : 8);
+  use_split_table(op, S, sa.a);
   const int64_t grid = arows * S;
   if (n_warps) *n_warps = grid;   // one energy partial per CTA
   if (a0.epart) HSV_REQUIRE(grid <= (int64_t)ctx().num_sms * 64, HSV_ERR_UNSUPPORTED,

@@ -155,6 +155,14 @@ struct GroupHash {
   int32_t tab;
 };
 
+// Bucket split table for S = 2 << i parts (hsv_op_create): S runs of virtual
+// buckets; split k is [cut[k], cut[k + 1]) of the table's virtual buckets.
+constexpr int kSplitTables = 5;   // S = 2, 4, 8, 16, 32
+struct SplitTable {
+  int vb_off = 0, nb = 0, nbh = 0;   // in d_vbuckets; entries; of them hashed (first)
+  int cut_off = 0;                   // S + 1 entries in d_splits
+};
+
 struct hsv_op_s {
   hsv_sector sec = nullptr;
   int64_t n_terms = 0, n_groups = 0, n_active = 0, n_buckets = 0;
@@ -165,7 +173,9 @@ struct hsv_op_s {
   GroupHash* d_ghash = nullptr;
   void* d_recs = nullptr;       // packed Rec<W> per group (kernel layout)
   int64_t n_buckets_h = 0;      // buckets [0, n_buckets_h) are x-local (hashed)
-  int* d_splits = nullptr;      // bucket boundaries for 2, 4, 8 splits: 3 + 5 + 9 ints
+  int* d_splits = nullptr;      // split cuts (SplitTable::cut_off)
+  int4* d_vbuckets = nullptr;   // virtual buckets of the split tables
+  SplitTable split[kSplitTables];
   double* d_tabs = nullptr;
   int64_t n_hashed = 0;
   // term-loop groups whose terms differ from the first only by the flip

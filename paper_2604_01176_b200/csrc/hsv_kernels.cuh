@@ -10,7 +10,7 @@ struct Tuning {
   int apply_minb = 0;     // __launch_bounds__ min blocks/SM: 0 = default (R=2: 4, R=4: 3);
                           // alternatives R=2: 3 or 5, R=4: 2
   int screen_rows = 1024; // rows staged per chunk in the screen kernel
-  int apply_split = 0;    // bucket splits per row unit in K1 (0 = auto, else 1/2/4/8)
+  int apply_split = 0;    // bucket splits per row unit in K1 (0 = auto, else 1/2/4/8/16/32)
   int apply_interleave = -1;  // K1 unit schedule: -1 auto (= 2), 0 contiguous, 1 interleaved, 2 dynamic
   int push = -1;          // sparse-psi push path: -1 auto, 0 off, 1 whenever it fits in memory
   int push_keys = 32;     // auto: push while nnz(psi) * (1 + groups) <= push_keys * rows - 2^20
@@ -52,7 +52,7 @@ struct ApplyArgs {
   int nsplit;              // bucket splits per row unit (1: none)
   int interleave;          // unit schedule: 0 contiguous blocks per warp, 1 interleaved
   int64_t dim_bytes;       // size of psi in bytes (schedule choice)
-  const int* split_bk;     // nsplit + 1 bucket boundaries (combined bucket index space)
+  const int* split_bk;     // nsplit + 1 bucket boundaries (in this launch's buckets)
   double2* ypart;          // [nsplit][rows of a_lo..a_hi] partial rows when nsplit > 1
   int64_t part_stride;
   double prune;
@@ -113,6 +113,7 @@ __device__ __forceinline__ double rec_amp(const Rec<W>& r, W s, const double* __
 }
 
 int grid_for(int64_t n, int block);
+void use_split_table(const hsv_op_s* op, int St, ApplyArgs& a);
 int apply_warps(const hsv_op_s* op);
 // Push (scatter + sort-reduce) K1 for sparse psi; *done = false: use the pull kernel.
 // dense_hint (optional, per state): skip when set, set when psi is found dense.

@@ -68,8 +68,8 @@ int hsv_set_tuning(const char* key, int64_t value) {
                 "apply_interleave must be -1, 0, 1 or 2");
     g_tuning.apply_interleave = (int)value;
   } else if (k == "apply_split") {
-    HSV_REQUIRE(value == 0 || value == 1 || value == 2 || value == 4 || value == 8,
-                HSV_ERR_INVALID, "apply_split must be 0 (auto), 1, 2, 4 or 8");
+    HSV_REQUIRE(value >= 0 && value <= 32 && (value & (value - 1)) == 0, HSV_ERR_INVALID,
+                "apply_split must be 0 (auto), 1, 2, 4, 8, 16 or 32");
     g_tuning.apply_split = (int)value;
   } else if (k == "push") {
     HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "push must be -1, 0 or 1");

@@ -34,6 +34,8 @@ def main():
     ap.add_argument("--split", nargs="+", type=int, default=[0])
     ap.add_argument("--shard", nargs="+", type=int, default=[1],
                     help="time the rank-0 alpha-row shard of a W-way split")
+    ap.add_argument("--shard-index", nargs="+", type=int, default=[0],
+                    help="which shard of the --shard split to time (default the rank-0 one)")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--lib", default=None, help="alternative libhsv build (A/B runs)")
     args = ap.parse_args()
@@ -53,21 +55,22 @@ def main():
         info = op.info()
         na = basis._sector.n_alpha_strings
         d_out = None
-        for r, sr, mb, sp, sh in [(r, sr, mb, sp, sh) for r in args.apply_r
-                                  for sr in args.screen_rows for mb in args.minb
-                                  for sp in args.split for sh in args.shard]:
+        for r, sr, mb, sp, sh, si in [(r, sr, mb, sp, sh, si) for r in args.apply_r
+                                      for sr in args.screen_rows for mb in args.minb
+                                      for sp in args.split for sh in args.shard
+                                      for si in args.shard_index if si < sh]:
             N.call("hsv_set_tuning", b"apply_r", r)
             N.call("hsv_set_tuning", b"apply_minb", mb)
             N.call("hsv_set_tuning", b"screen_rows", sr)
             N.call("hsv_set_tuning", b"apply_split", sp)
-            a_hi = na // sh            # rank-0 shard of an sh-way owner-computes split
+            a_lo, a_hi = si * na // sh, (si + 1) * na // sh   # one shard of an sh-way split
             out = np.empty(2 + pool.n)
 
             def step():
                 if sh == 1:
                     return op.energy_screen_pool(st, pool)
                 N.call("hsv_energy_screen_pool_async", op.handle, st.device.handle, pool.handle,
-                       0, a_hi, N.C.c_void_p(d_dev))
+                       a_lo, a_hi, N.C.c_void_p(d_dev))
                 N.call("hsv_synchronize")
                 return None, None
             if sh > 1 and d_out is None:
@@ -84,10 +87,10 @@ def main():
             N.call("hsv_prof_enable", 0)
             ta, _ = prof("apply")
             ts, _ = prof("screen")
-            bytes_apply = (16.0 * nnz + 24.0 * dim) * a_hi / na
+            bytes_apply = (16.0 * nnz + 24.0 * dim) * (a_hi - a_lo) / na
             print(json.dumps({
                 "system": name, "dim": dim, "apply_r": r, "minb": mb, "screen_rows": sr,
-                "split": sp, "shard": sh, "apply_ms": ta, "screen_ms": ts,
+                "split": sp, "shard": sh, "shard_index": si, "apply_ms": ta, "screen_ms": ts,
                 "apply_GBs_alg": bytes_apply / ta / 1e6, "energy": e,
                 "gmax": None if g is None else float(np.max(np.abs(g))), "nnz": nnz, **info}),
                 flush=True)
