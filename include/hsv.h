@@ -220,6 +220,13 @@ HSV_API int hsv_peer_open(hsv_peer p, const void* handles);
 HSV_API int hsv_peer_destroy(hsv_peer p);
 HSV_API int hsv_peer_data(hsv_peer p, void** d_data, int64_t* bytes);
 HSV_API int hsv_peer_allgather_async(hsv_peer p, const void* d_src, int64_t n);
+/* All-gather + rank-order sum in ONE launch: the n float64 values at d_src go
+ * to every rank's buffer, then (after the arrival barrier) d_out[j] =
+ * ((0 + x_0[j]) + x_1[j]) + ... in rank order -- the same bits on every rank
+ * and the same sum as hsv_sum_rows_async over hsv_peer_data().  n * 8 must be a
+ * multiple of 16.  Replaces the NCCL all-reduce of the (E, gradients) partials
+ * (bench.py; reference engine: the scalar combine of SURVEY.md 8(e)). */
+HSV_API int hsv_peer_allreduce_async(hsv_peer p, const double* d_src, int64_t n, double* d_out);
 /* Phase 1 of the adjoint sweep (as hsv_eg_forward_async) with the rows
  * [a_lo, a_hi) of w = H psi written by the K1 epilogue straight into every
  * rank's peer buffer (bytes >= dim * 16, rows at their natural offsets), then

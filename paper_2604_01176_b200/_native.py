@@ -93,6 +93,7 @@ _SIGNATURES = {
     "hsv_peer_destroy": (C.c_int, [vp]),
     "hsv_peer_data": (C.c_int, [vp, C.POINTER(vp), C.POINTER(i64)]),
     "hsv_peer_allgather_async": (C.c_int, [vp, vp, i64]),
+    "hsv_peer_allreduce_async": (C.c_int, [vp, vp, i64, vp]),
     "hsv_eg_forward_peer_async": (C.c_int, [vp, C.c_uint64, P_u64, P_u64, P_dbl, P_dbl, i64,
                                             i64, i64, vp, vp, vp]),
     "hsv_set_tuning": (C.c_int, [C.c_char_p, i64]),

@@ -111,6 +111,8 @@ int reduce_sum_f64(const double* d_in, int64_t n, int64_t stride, int64_t count,
       const int64_t want = std::max<int64_t>(1, 2 * (int64_t)ctx().num_sms / gx);
       chunk = std::max<int64_t>(16, std::min<int64_t>(256, (src_n + want - 1) / want));
       if (src_n <= 256) chunk = src_n;   // short tail: finish in one launch
+    } else if (src_n <= (1 << 20)) {
+      chunk = src_n;   // few columns (energy partials of K1's units): one launch
     }
     int64_t nch = (src_n + chunk - 1) / chunk;
     double* dst;
@@ -125,7 +127,8 @@ int reduce_sum_f64(const double* d_in, int64_t n, int64_t stride, int64_t count,
       k_colsum_seq<<<grid, 128, 0, stream()>>>(src, src_n, src_stride, count, chunk, dst);
     } else {
       dim3 grid((unsigned)count, (unsigned)nch);
-      k_colsum_tree<<<grid, 256, 0, stream()>>>(src, src_n, src_stride, count, chunk, dst);
+      k_colsum_tree<<<grid, chunk >= 8192 ? 1024 : 256, 0, stream()>>>(src, src_n, src_stride,
+                                                                        count, chunk, dst);
     }
     count_launch();
     HSV_CHECK_LAUNCH();

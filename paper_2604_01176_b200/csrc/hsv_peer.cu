@@ -56,6 +56,39 @@ __global__ void k_peer_barrier(char* const* bases, int world, int rank, int64_t 
   __threadfence_system();
 }
 
+// all-gather + barrier + rank-order sum in one CTA: puts, then thread 0 publishes
+// and waits (its system-scope fence is cumulative over the CTA's stores ordered
+// before it by the barrier), then the sums read every rank's block
+__global__ void __launch_bounds__(1024) k_peer_allreduce(const double* __restrict__ src,
+                                                         int64_t n, char* const* bases,
+                                                         int world, int rank, int64_t half,
+                                                         int64_t flags_off, uint64_t epoch,
+                                                         double* __restrict__ out) {
+  const int64_t n16 = n / 2;
+  for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) {
+    const uint4 v = reinterpret_cast<const uint4*>(src)[i];
+    for (int r = 0; r < world; ++r)
+      reinterpret_cast<uint4*>(bases[r] + half + rank * n * (int64_t)sizeof(double))[i] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int r = 0; r < world; ++r)
+      st_release_sys(reinterpret_cast<uint64_t*>(bases[r] + flags_off) + rank, epoch);
+    const uint64_t* mine = reinterpret_cast<const uint64_t*>(bases[rank] + flags_off);
+    for (int r = 0; r < world; ++r)
+      while (ld_acquire_sys(mine + r) < epoch) __nanosleep(32);
+    __threadfence_system();
+  }
+  __syncthreads();
+  const double* data = reinterpret_cast<const double*>(bases[rank] + half);
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    double acc = 0.0;
+    for (int r = 0; r < world; ++r) acc += data[r * n + j];
+    out[j] = acc;
+  }
+}
+
 int peer_barrier(hsv_peer_s* p) {
   k_peer_barrier<<<1, 32, 0, stream()>>>(p->d_bases, p->world, p->rank, p->flags_off, p->epoch);
   count_launch();
@@ -159,6 +192,22 @@ int hsv_peer_allgather_async(hsv_peer p, const void* d_src, int64_t n) {
     count_launch();
     HSV_CHECK_LAUNCH();
     HSV_TRY(peer_barrier(p));
+  }
+  return HSV_OK;
+}
+
+int hsv_peer_allreduce_async(hsv_peer p, const double* d_src, int64_t n, double* d_out) {
+  HSV_REQUIRE(p && p->opened && d_src && d_out, HSV_ERR_INVALID, "peer buffer not opened");
+  HSV_REQUIRE(n > 0 && n % 2 == 0 && n * 8 * p->world <= p->bytes, HSV_ERR_INVALID,
+              "allreduce block of %lld doubles does not fit the peer buffer", (long long)n);
+  ++p->epoch;
+  {
+    ProfScope prof("peer");
+    k_peer_allreduce<<<1, 1024, 0, stream()>>>(d_src, n, p->d_bases, p->world, p->rank,
+                                               (p->epoch & 1) * p->bytes, p->flags_off, p->epoch,
+                                               d_out);
+    count_launch();
+    HSV_CHECK_LAUNCH();
   }
   return HSV_OK;
 }

@@ -114,12 +114,11 @@ class PeerExchange:
 
     def gather_and_combine(self, partial: torch.Tensor) -> torch.Tensor:
         """Rank-order sum of every rank's `partial` (float64, CUDA, 16-B multiple),
-        on the library stream: NVLink stores + device barrier + one summation."""
-        n = partial.numel() * 8
-        N.call("hsv_peer_allgather_async", self.handle, N.C.c_void_p(partial.data_ptr()), n)
+        on the library stream: NVLink stores, device barrier and the summation in
+        one launch (hsv_peer_allreduce_async)."""
         out = torch.empty_like(partial)
-        N.call("hsv_sum_rows_async", N.C.c_void_p(self.data()), self.world, partial.numel(),
-               N.C.c_void_p(out.data_ptr()))
+        N.call("hsv_peer_allreduce_async", self.handle, N.C.c_void_p(partial.data_ptr()),
+               partial.numel(), N.C.c_void_p(out.data_ptr()))
         return out
 
 
