@@ -265,7 +265,7 @@ def run_hsv(args):
     if world > 1 and os.environ.get("HSV_PEER", "1") != "0":
         from paper_2604_01176_b200.distributed import PeerExchange
         peer = PeerExchange.create(world * d_out.numel() * 8)
-    exchange = "nvlink-peer (CUDA IPC stores + device barrier)" if peer else (
+    exchange = "nvlink-peer all-reduce (CUDA IPC stores, device barrier, rank-order sum: one launch)" if peer else (
         "nccl all_gather" if world > 1 else "none")
 
     def step_device():
