@@ -245,14 +245,13 @@ def run_hsv(args):
     M = dpool.n
     nnz_struct = op.nnz                       # structural nonzeros (== reference CSR nnz)
     psi_vals = s1_values(dim)
-    pos_pinned = torch.arange(dim, dtype=torch.int64).pin_memory()
     val_pinned = torch.from_numpy(psi_vals).pin_memory()
     st = hsv.svengine.DeviceState(basis)
 
     def upload():
-        N.call("hsv_state_set_sparse", st.handle,
-               N.C.cast(pos_pinned.data_ptr(), N.P_i64), N.C.cast(val_pinned.data_ptr(), N.P_dbl),
-               None, dim)
+        # the binding's transfer of a SparseVector with full support (DeviceState.from_sparse):
+        # values only, in reference position order
+        N.call("hsv_state_set_dense", st.handle, N.C.cast(val_pinned.data_ptr(), N.P_dbl), None)
 
     upload()
     n_alpha_strings = basis._sector.n_alpha_strings
@@ -333,7 +332,7 @@ def run_hsv(args):
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        upload()                               # H2D: positions + amplitudes (pinned)
+        upload()                               # H2D: amplitudes (pinned)
         if world > 1:
             res = step_device().cpu().numpy()             # D2H
             e_host.value, g_host[:] = res[0], res[2:2 + M]
@@ -417,7 +416,7 @@ def run_hsv(args):
             "kernels_ms": {"apply": apply_ms, "screen": screen_ms},
             "step_roofline": step_roofline(sysm, pool_ops, nnz_struct, dim, ms_per_step, hbm),
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_t,
-                    "h2d_bytes_per_step": dim * 16, "d2h_bytes_per_step": (2 + M) * 8},
+                    "h2d_bytes_per_step": dim * 8, "d2h_bytes_per_step": (2 + M) * 8},
             "gpu_launches": launches,
             "adapt_iteration": adapt,
             "clocks": clk.summary(),

@@ -117,6 +117,10 @@ HSV_API int hsv_state_set_basis(hsv_state st, uint64_t key, double re, double im
  * (re, im) pairs, amps_im may be NULL for real input. */
 HSV_API int hsv_state_set_sparse(hsv_state st, const int64_t* pos, const double* amps_re,
                          const double* amps_im, int64_t n);
+/* Replace contents from all dim amplitudes in reference position order (a
+ * SparseVector whose support is the whole sector: the binding sends the values
+ * only, half the host-to-device bytes of hsv_state_set_sparse for real input). */
+HSV_API int hsv_state_set_dense(hsv_state st, const double* amps_re, const double* amps_im);
 HSV_API int hsv_state_set_keys(hsv_state st, const uint64_t* keys, const double* amps_re,
                        const double* amps_im, int64_t n);
 HSV_API int hsv_state_nnz(hsv_state st, int64_t* nnz);

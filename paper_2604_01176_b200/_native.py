@@ -57,6 +57,7 @@ _SIGNATURES = {
     "hsv_state_zero": (C.c_int, [vp]),
     "hsv_state_set_basis": (C.c_int, [vp, u64, dbl, dbl]),
     "hsv_state_set_sparse": (C.c_int, [vp, P_i64, P_dbl, P_dbl, i64]),
+    "hsv_state_set_dense": (C.c_int, [vp, P_dbl, P_dbl]),
     "hsv_state_set_keys": (C.c_int, [vp, P_u64, P_dbl, P_dbl, i64]),
     "hsv_state_nnz": (C.c_int, [vp, P_i64]),
     "hsv_state_get_sparse": (C.c_int, [vp, dbl, P_i64, P_dbl, P_dbl, i64, P_i64]),

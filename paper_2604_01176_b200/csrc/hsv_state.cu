@@ -144,6 +144,15 @@ __global__ void k_scatter_pos(const int64_t* __restrict__ pos, const double* __r
   if (p < 0 || p >= dim) { *bad = 1; return; }
   a[iperm[p]] = make_double2(re[i], im ? im[i] : 0.0);
 }
+// dense input: internal row j takes reference position perm[j] (coalesced stores)
+__global__ void k_gather_dense(const double* __restrict__ re, const double* __restrict__ im,
+                               int64_t dim, const int64_t* __restrict__ perm,
+                               double2* __restrict__ a) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= dim) return;
+  const int64_t p = perm[j];
+  a[j] = make_double2(re[p], im ? im[p] : 0.0);
+}
 __global__ void k_scatter_idx(const int64_t* __restrict__ idx, const double2* __restrict__ v,
                               int64_t n, double2* __restrict__ a) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -330,6 +339,29 @@ int hsv_state_set_sparse(hsv_state st, const int64_t* pos, const double* re, con
   HSV_TRY(stream_sync());
   HSV_REQUIRE(!h_bad, HSV_ERR_INVALID, "position out of range for dimension %lld",
               (long long)st->sec->dim);
+  return HSV_OK;
+}
+
+int hsv_state_set_dense(hsv_state st, const double* re, const double* im) {
+  HSV_REQUIRE(st && re, HSV_ERR_INVALID, "null argument");
+  const int64_t dim = st->sec->dim;
+  // every amplitude in reference position order: no positions to move or check,
+  // no zero fill (every row is written)
+  double *d_re = nullptr, *d_im = nullptr;
+  HSV_TRY(dalloc(&d_re, dim));
+  if (im) HSV_TRY(dalloc(&d_im, dim));
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_re, re, dim * 8, cudaMemcpyHostToDevice, stream()));
+  if (im) HSV_TRY_CUDA(cudaMemcpyAsync(d_im, im, dim * 8, cudaMemcpyHostToDevice, stream()));
+  k_gather_dense<<<(unsigned)((dim + 255) / 256), 256, 0, stream()>>>(d_re, d_im, dim,
+                                                                       st->sec->d_perm, st->d_amp);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  dfree(d_re);
+  dfree(d_im);
+  st->arow_valid = false;
+  st->dense_hint = true;
+  HSV_TRY(state_norm2_async(st));
+  HSV_TRY(stream_sync());   // host buffers may be reused on return
   return HSV_OK;
 }
 

@@ -110,7 +110,13 @@ class DeviceState:
             pim = N.ptr_f64(im)
         else:
             re, pim = N.as_f64(vec.values), None
-        N.call("hsv_state_set_sparse", st.handle, N.ptr_i64(idx), N.ptr_f64(re), pim, idx.size)
+        if idx.size == vec.dim and idx.size and idx[0] == 0 and idx[-1] == vec.dim - 1:
+            # SparseVector indices are ascending and unique, so a full support is
+            # every position in order: send the values only
+            N.call("hsv_state_set_dense", st.handle, N.ptr_f64(re), pim)
+        else:
+            N.call("hsv_state_set_sparse", st.handle, N.ptr_i64(idx), N.ptr_f64(re), pim,
+                   idx.size)
         return st
 
     @classmethod
