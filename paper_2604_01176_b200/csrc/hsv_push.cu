@@ -34,6 +34,11 @@ struct PushArgs {
   unsigned long long* n_keys;
   int gbits;
   int64_t lo;                      // first row of the range (a_lo * Nb)
+  // device-sized launch (one host sync per call): the source count is read
+  // from here; more than n_src sources means the keys buffer is too small and
+  // the kernel writes nothing (the host re-runs it at the exact size)
+  const unsigned long long* n_src_dev;
+  int64_t target_items;
 };
 
 // Nonzero rows of psi, compacted in any order (the sort fixes the order).
@@ -70,6 +75,15 @@ __global__ void k_push_collect(const double2* __restrict__ psi, int64_t n, int64
 template <typename W, int SH>
 __global__ void __launch_bounds__(256) k_push_keys(const PushArgs p, int bchunk, int64_t n_items) {
   const ApplyArgs& a = p.a;
+  if (p.n_src_dev) {   // same sizing rule as the host path, from the device count
+    const int64_t n_src = (int64_t)*p.n_src_dev;
+    if (n_src > p.n_src) return;
+    const int64_t nbk = a.n_buckets > 1 ? a.n_buckets : 1;
+    int64_t bc = (n_src * nbk + p.target_items - 1) / p.target_items;
+    bc = bc < 1 ? 1 : bc > nbk ? nbk : bc;
+    bchunk = (int)bc;
+    n_items = n_src * ((nbk + bchunk - 1) / bchunk);
+  }
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -245,6 +259,7 @@ static int push_t(const hsv_op_s* op, const ApplyArgs& a0, bool* done, int64_t* 
   p.a = a0;
   p.gbits = gbits;
   p.lo = a0.a_lo * s->Nb;
+  p.target_items = (int64_t)ctx().num_sms * 32;   // about 32 warps' worth of items per SM
   int64_t* src = nullptr;
   unsigned long long* cnt = nullptr;
   HSV_TRY(dalloc(&src, cap_src));
@@ -259,40 +274,73 @@ static int push_t(const hsv_op_s* op, const ApplyArgs& a0, bool* done, int64_t* 
   }
   count_launch();
   HSV_CHECK_LAUNCH();
-  HSV_TRY_CUDA(cudaMemcpyAsync(h, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                               stream()));
-  HSV_TRY(stream_sync());
+  p.src = src;
+  p.n_keys = cnt + 1;
+  const int nbk = (int)std::max<int64_t>(op->n_buckets, 1);
+  auto launch_keys = [&](bool device_sized) -> int {
+    ProfScope prof("push");
+    int bchunk = 1;
+    int64_t n_items = 0, grid = (int64_t)ctx().num_sms * 8;
+    if (!device_sized) {
+      if (p.n_src == 0) return HSV_OK;
+      bchunk = (int)std::min<int64_t>(
+          nbk, std::max<int64_t>(1, (p.n_src * nbk + p.target_items - 1) / p.target_items));
+      n_items = p.n_src * ((nbk + bchunk - 1) / bchunk);
+      grid = std::min<int64_t>((n_items + 7) / 8, grid);
+    }
+    k_push_keys<W, SH><<<(unsigned)std::max<int64_t>(grid, 1), 256, 0, stream()>>>(p, bchunk,
+                                                                                   n_items);
+    count_launch();
+    HSV_CHECK_LAUNCH();
+    return HSV_OK;
+  };
+  // Source count of the previous call (ADAPT evaluations come in runs of
+  // similar supports): size the keys buffer for 4x that and let the keys kernel
+  // read the real count on the device -- one host sync instead of two.
+  static int64_t last_nsrc = -1;
+  uint64_t *keys = nullptr, *keys2 = nullptr;
+  bool sized = false;
+  if (last_nsrc >= 0) {
+    const int64_t guess = std::min<int64_t>(cap_src, std::max<int64_t>(4 * last_nsrc, 64));
+    p.n_src = guess;
+    p.n_src_dev = cnt;
+    p.cap_keys = (unsigned long long)(guess * per_src);
+    HSV_TRY(dalloc(&keys, guess * per_src));
+    p.keys = keys;
+    HSV_TRY(launch_keys(true));
+    HSV_TRY_CUDA(cudaMemcpyAsync(h, cnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 stream()));
+    HSV_TRY(stream_sync());
+    sized = h[0] <= (unsigned long long)guess;
+    if (!sized) {
+      dfree(keys);
+      keys = nullptr;
+    }
+  } else {
+    HSV_TRY_CUDA(cudaMemcpyAsync(h, cnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                 stream()));
+    HSV_TRY(stream_sync());
+  }
+  last_nsrc = (int64_t)std::min<unsigned long long>(h[0], (unsigned long long)cap_src + 1);
   if (h[0] > (unsigned long long)cap_src) {   // dense psi
     if (dense_hint) *dense_hint = true;
+    dfree(keys);
     dfree(src);
     dfree(cnt);
     return HSV_OK;
   }
-  p.src = src;
-  p.n_src = (int64_t)h[0];
-  p.cap_keys = (unsigned long long)(p.n_src * per_src);
-  p.n_keys = cnt + 1;
-  uint64_t *keys = nullptr, *keys2 = nullptr;
-  HSV_TRY(dalloc(&keys, std::max<int64_t>(1, p.n_src * per_src)));
-  p.keys = keys;
-  {
-    ProfScope prof("push");
-    if (p.n_src > 0) {
-      // about 32 warps' worth of items per SM: small supports split each source's buckets
-      const int64_t target = (int64_t)ctx().num_sms * 32;
-      const int nbk = (int)std::max<int64_t>(op->n_buckets, 1);
-      const int bchunk = (int)std::min<int64_t>(
-          nbk, std::max<int64_t>(1, (p.n_src * nbk + target - 1) / target));
-      const int64_t n_items = p.n_src * ((nbk + bchunk - 1) / bchunk);
-      const int64_t grid = std::min<int64_t>((n_items + 7) / 8, (int64_t)ctx().num_sms * 8);
-      k_push_keys<W, SH><<<(unsigned)grid, 256, 0, stream()>>>(p, bchunk, n_items);
-      count_launch();
-      HSV_CHECK_LAUNCH();
-    }
+  if (!sized) {   // exact size: the second sync of the first call (or of a larger support)
+    p.n_src = (int64_t)h[0];
+    p.n_src_dev = nullptr;
+    p.cap_keys = (unsigned long long)(p.n_src * per_src);
+    HSV_TRY(dalloc(&keys, std::max<int64_t>(1, p.n_src * per_src)));
+    p.keys = keys;
+    HSV_TRY_CUDA(cudaMemsetAsync(cnt + 1, 0, sizeof(unsigned long long), stream()));
+    HSV_TRY(launch_keys(false));
+    HSV_TRY_CUDA(cudaMemcpyAsync(h + 1, cnt + 1, sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, stream()));
+    HSV_TRY(stream_sync());
   }
-  HSV_TRY_CUDA(cudaMemcpyAsync(h + 1, cnt + 1, sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                               stream()));
-  HSV_TRY(stream_sync());
   const int64_t nk = (int64_t)h[1];
   if (h[1] > p.cap_keys) {   // cannot happen (per-source bound); stay safe
     dfree(keys); dfree(src); dfree(cnt);
