@@ -157,6 +157,12 @@ HSV_API int hsv_apply_generator(hsv_state in, hsv_state out, uint64_t occ_mask, 
 HSV_API int hsv_energy_screen(hsv_op op, hsv_state psi, const uint64_t* occ_masks,
                       const uint64_t* virt_masks, int64_t n_ops, double* energy,
                       double* grads);
+/* psi <- exp(t_{k-1}T_{k-1})...exp(t_0 T_0)|hf> (apply_ansatz, svengine.py:240-244)
+ * in one fused sweep; rotations with (c, s) == (1, 0) are skipped as theta == 0 is.
+ * Synchronizes (norm-drift check, like hsv_apply_qeb). */
+HSV_API int hsv_ansatz_state(hsv_sector sector, uint64_t hf_key, const uint64_t* occ_masks,
+                             const uint64_t* virt_masks, const double* c, const double* s,
+                             int64_t k, hsv_state psi_out);
 /* Adjoint energy + analytic gradient of exp(t_{k-1}T_{k-1})...exp(t_0 T_0)|hf>
  * (ansatz_energy_gradient, svengine.py:260-281); cs[i], sn[i] = cos/sin(theta_i). */
 HSV_API int hsv_energy_gradient(hsv_op op, uint64_t hf_key, const uint64_t* occ_masks,

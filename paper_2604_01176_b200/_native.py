@@ -69,6 +69,7 @@ _SIGNATURES = {
     "hsv_apply_h": (C.c_int, [vp, vp, vp, dbl]),
     "hsv_expect_h": (C.c_int, [vp, vp, P_dbl, P_dbl]),
     "hsv_apply_qeb": (C.c_int, [vp, vp, u64, u64, dbl, dbl]),
+    "hsv_ansatz_state": (C.c_int, [vp, u64, P_u64, P_u64, P_dbl, P_dbl, i64, vp]),
     "hsv_apply_generator": (C.c_int, [vp, vp, u64, u64]),
     "hsv_energy_screen": (C.c_int, [vp, vp, P_u64, P_u64, i64, P_dbl, P_dbl]),
     "hsv_energy_gradient": (C.c_int, [vp, u64, P_u64, P_u64, P_dbl, P_dbl, i64, P_dbl, P_dbl]),

@@ -645,16 +645,12 @@ static int check_eg_args(hsv_op op, const uint64_t* occ, const uint64_t* virt, c
   return HSV_OK;
 }
 
-// Phase 1 of the adjoint sweep: psi <- prod_i exp(theta_i T_i)|hf> (all rows;
-// occupancy flags and norm maintained), w rows [a_lo, a_hi) <- (H psi) rows.
-int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const uint64_t* virt,
-                         const double* cs, const double* sn, int64_t k, int64_t a_lo,
-                         int64_t a_hi, hsv_state psi, hsv_state w) {
-  HSV_TRY(check_eg_args(op, occ, virt, cs, sn, k));
-  HSV_REQUIRE(psi && w && psi != w && psi->sec == op->sec && w->sec == op->sec,
-              HSV_ERR_INVALID, "bad state argument");
-  const hsv_sector_s* sec = op->sec;
-  HSV_REQUIRE(0 <= a_lo && a_lo <= a_hi && a_hi <= sec->Na, HSV_ERR_INVALID, "bad alpha-row range");
+// psi <- prod_i exp(theta_i T_i)|hf> on all rows, occupancy flags and norm
+// maintained (fused sweep, or one launch per rotation); drift errors are left
+// in `sc` for the caller's sc.check().
+static int forward_psi(const hsv_sector_s* sec, uint64_t hf_key, const uint64_t* occ,
+                       const uint64_t* virt, const double* cs, const double* sn, int64_t k,
+                       hsv_state psi, PairScratch& sc, PairLists& pl) {
   const uint32_t sa = sec->compress_a(hf_key), sb = sec->compress_b(hf_key);
   HSV_REQUIRE((sec->n_qubits >= 64 || (hf_key >> sec->n_qubits) == 0) && sec->Ra[sa] != ~0u &&
                   sec->Rb[sb] != ~0u,
@@ -675,9 +671,6 @@ int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const 
                                stream()));
   HSV_TRY_CUDA(cudaMemcpyAsync(psi->d_arow + sec->Ra[sa], &one_flag, sizeof(uint32_t),
                                cudaMemcpyHostToDevice, stream()));
-  PairScratch sc;
-  HSV_TRY(sc.init(sec, 2));
-  PairLists pl;
   if (tuning().sweep) {
     static thread_local std::vector<SweepOp> ops;
     ops.clear();
@@ -698,6 +691,23 @@ int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const 
   }
   psi->norm2_valid = psi->arow_valid = true;
   psi->dense_hint = false;
+  return HSV_OK;
+}
+
+// Phase 1 of the adjoint sweep: psi <- prod_i exp(theta_i T_i)|hf> (all rows;
+// occupancy flags and norm maintained), w rows [a_lo, a_hi) <- (H psi) rows.
+int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const uint64_t* virt,
+                         const double* cs, const double* sn, int64_t k, int64_t a_lo,
+                         int64_t a_hi, hsv_state psi, hsv_state w) {
+  HSV_TRY(check_eg_args(op, occ, virt, cs, sn, k));
+  HSV_REQUIRE(psi && w && psi != w && psi->sec == op->sec && w->sec == op->sec,
+              HSV_ERR_INVALID, "bad state argument");
+  const hsv_sector_s* sec = op->sec;
+  HSV_REQUIRE(0 <= a_lo && a_lo <= a_hi && a_hi <= sec->Na, HSV_ERR_INVALID, "bad alpha-row range");
+  PairScratch sc;
+  HSV_TRY(sc.init(sec, 2));
+  PairLists pl;
+  HSV_TRY(forward_psi(sec, hf_key, occ, virt, cs, sn, k, psi, sc, pl));
   int64_t used = 0;
   HSV_TRY(launch_apply(op, psi->d_amp, w->d_amp, nullptr, a_lo, a_hi, 0.0, 0, &used, psi->d_arow,
                        &psi->dense_hint));
@@ -705,6 +715,25 @@ int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const 
   w->dense_hint = false;
   // drift errors surface here (synchronizes)
   const int rc = sc.check();
+  dfree(pl.la); dfree(pl.lb);
+  sc.release();
+  return rc;
+}
+
+// The ansatz state alone (apply_ansatz, svengine.py:240-244): one fused sweep
+// instead of one rotation call (and host sync) per operator.
+int hsv_ansatz_state(hsv_sector s, uint64_t hf_key, const uint64_t* occ, const uint64_t* virt,
+                     const double* cs, const double* sn, int64_t k, hsv_state psi) {
+  HSV_REQUIRE(s && psi && psi->sec == s, HSV_ERR_INVALID, "bad state argument");
+  HSV_REQUIRE(k == 0 || (occ && virt && cs && sn), HSV_ERR_INVALID, "null argument");
+  for (int64_t i = 0; i < k; ++i)
+    HSV_REQUIRE((occ[i] & virt[i]) == 0 && occ[i] && virt[i], HSV_ERR_INVALID,
+                "excitation indices must be distinct");
+  PairScratch sc;
+  HSV_TRY(sc.init(s, 2));
+  PairLists pl;
+  HSV_TRY(forward_psi(s, hf_key, occ, virt, cs, sn, k, psi, sc, pl));
+  const int rc = sc.check();   // synchronizes; drift errors surface here
   dfree(pl.la); dfree(pl.lb);
   sc.release();
   return rc;

@@ -409,15 +409,17 @@ def apply_qeb_exponential(op: ExcitationOperator, theta: float, s: SvState) -> S
 
 
 def apply_ansatz(basis: CiBasis, hf: Configuration, ops, thetas) -> SvState:
-    """HF reference followed by the ansatz rotations (svengine.py:240-244), in place."""
-    st = SvState.from_configuration(basis, hf)
-    dev = st.device
-    for op, theta in zip(ops, thetas):
-        theta = float(theta)
-        if theta == 0.0:
-            continue
-        N.call("hsv_apply_qeb", dev.handle, dev.handle, op.occ_mask, op.virt_mask,
-               float(np.cos(theta)), float(np.sin(theta)))
+    """HF reference followed by the ansatz rotations (svengine.py:240-244): one fused
+    device sweep (hsv_ansatz_state), bitwise equal to rotating one operator at a time."""
+    ops = list(ops)
+    th = np.asarray([float(t) for t in thetas], dtype=np.float64)
+    n = min(len(ops), th.size)                  # zip() semantics
+    occ, virt = _masks(ops[:n])
+    th = np.ascontiguousarray(th[:n])
+    cs, sn = N.as_f64(np.cos(th)), N.as_f64(np.sin(th))
+    dev = DeviceState(basis)
+    N.call("hsv_ansatz_state", basis.sector, int(hf.bits), N.ptr_u64(occ), N.ptr_u64(virt),
+           N.ptr_f64(cs), N.ptr_f64(sn), n, dev.handle)
     return SvState(basis, _dev=dev)
 
 
