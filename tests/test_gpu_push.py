@@ -140,3 +140,20 @@ def test_push_prune_and_determinism(hsv, N):
     g1 = eng.screen(st, pool)
     g2 = eng.screen(st, pool)
     assert np.array_equal(g1, g2)
+
+
+def test_push_device_sized_keys_across_supports(hsv, N):
+    """K1p sizes its keys launch from the previous call's source count: supports
+    that grow past 4x (re-run at the exact size), shrink, and repeat must all give
+    the pull kernel's rows bit for bit."""
+    sysm, eng, pool = setup(hsv, "h10")
+    dim = len(sysm.basis)
+    rng = np.random.default_rng(23)
+    for n in (1, 3, 50, 12, 12, 400, 2, 2000, 2000):
+        pos = np.sort(rng.choice(dim, size=n, replace=False))
+        st = hsv.SvState(sysm.basis, hsv.SparseVector(dim, pos, rng.standard_normal(n)))
+        wp, ep = apply_with(N, eng.matrix, st, 1)
+        wq, eq = apply_with(N, eng.matrix, st, 0)
+        assert np.array_equal(wp.indices, wq.indices), n
+        assert np.array_equal(wp.values, wq.values), n
+        assert abs(ep - eq) <= 1e-14 * max(1.0, abs(eq)), n

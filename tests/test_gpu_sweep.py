@@ -69,3 +69,27 @@ def test_sweep_forward_state_and_two_phase(hsv, N):
     assert np.array_equal(w1.indices, w0.indices) and np.array_equal(w1.values, w0.values)
     ref = hsv.apply_ansatz(sysm.basis, sysm.hf, ops, th).vec
     assert np.array_equal(ref.indices, p1.indices) and np.array_equal(ref.values, p1.values)
+
+
+@pytest.mark.parametrize("name,k", [("h4", 12), ("h8", 40), ("h12", 16)])
+def test_ansatz_state_equals_rotation_by_rotation(hsv, N, name, k):
+    """hsv_ansatz_state (apply_ansatz: one fused sweep) against exp(theta T) applied
+    one operator at a time (apply_qeb_exponential), bit for bit; theta = 0 skipped."""
+    sysm = hsv.MolecularSystem.bundled(name)
+    pool = hsv.build_qeb_pool(sysm.n_qubits, sysm.integrals.nelec)
+    rng = np.random.default_rng(17)
+    idx = rng.integers(0, len(pool), size=k)
+    th = rng.uniform(-0.5, 0.5, size=k)
+    th[::4] = 0.0
+    ops = [pool.ops[i] for i in idx]
+    for sweep in (1, 0):
+        N.call("hsv_set_tuning", b"sweep", sweep)
+        fused = hsv.apply_ansatz(sysm.basis, sysm.hf, ops, th).vec
+        st = hsv.SvState.from_configuration(sysm.basis, sysm.hf)
+        for op, t in zip(ops, th):
+            st = hsv.apply_qeb_exponential(op, t, st)
+        ref = st.vec
+        assert np.array_equal(fused.indices, ref.indices), sweep
+        assert np.array_equal(fused.values, ref.values), sweep
+    empty = hsv.apply_ansatz(sysm.basis, sysm.hf, [], [])
+    assert empty.nnz == 1
