@@ -377,8 +377,10 @@ def run_hsv(args):
                  "final_abs_error": float(res.records[-1].abs_error),
                  "final_nnz": int(res.records[-1].nnz),
                  "mode": "free run, eps_grad=1e-6, wall clock incl. host L-BFGS"
-                         + (f"; {world} ranks: H psi rows owner-computed + NCCL all-gather"
+                         + (f"; {world} ranks: replicas while psi is sparse, owner-computed "
+                            "H psi rows + NVLink peer all-gather once it is dense"
                             if world > 1 else "")}
+        adapt["replay_h10"] = adapt_replay(world)
 
     if rank == 0:
         pk, pk_kind = peaks()
@@ -431,6 +433,47 @@ def run_hsv(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def adapt_replay(world):
+    """ADAPT iteration time in replay mode: the operator sequence
+    of the unmodified reference's own H10 run (tests/golden/adapt_h10.npz, made by
+    tests/golden/make_golden_adapt_h10.py) is replayed; energies are compared with
+    the reference trace per iteration."""
+    import paper_2604_01176_b200 as hsv
+    path = ROOT / "tests" / "golden" / "adapt_h10.npz"
+    if not path.exists():
+        return None
+    tr = np.load(path)
+    sysm = hsv.MolecularSystem.bundled("h10")
+    if world > 1:
+        from paper_2604_01176_b200.distributed import DistributedSvAdaptEngine
+        eng = DistributedSvAdaptEngine(sysm, hsv.AdaptConfig())
+    else:
+        eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
+    replay = [int(i) for i in tr["selected"][1:]]
+    cfg = hsv.AdaptConfig(engine="sv", eps_grad=float(tr["eps"]), max_iter=int(tr["max_iter"]))
+    hsv.run_adapt(hsv.AdaptConfig(engine="sv", eps_grad=float(tr["eps"]), max_iter=2), sysm,
+                  engine=eng, replay=replay)                      # warm-up (untimed)
+    res = hsv.run_adapt(cfg, sysm, engine=eng, replay=replay)
+    wall = np.array([r.wall_elapsed for r in res.records])
+    evals = np.array([r.energy_evals for r in res.records])
+    it_s = np.diff(wall)
+    half = len(it_s) // 2
+    e = np.array([r.energy for r in res.records])
+    n = min(len(e), len(tr["energy"]))
+    return {"iterations": int(len(it_s)),
+            "iter_ms_mean_second_half": float(np.mean(it_s[half:]) * 1e3),
+            "iter_ms": [round(float(x) * 1e3, 2) for x in it_s],
+            "lbfgs_evals_per_iter": np.diff(evals).tolist(),
+            "reference_evals_per_iter": np.diff(tr["evals"]).tolist(),
+            "max_abs_energy_diff_vs_reference": float(np.max(np.abs(e[:n] - tr["energy"][:n]))),
+            "reference_iter_ms_mean_second_half": (
+                float(np.mean(np.diff(tr["wall_s"])[half:]) * 1e3) if "wall_s" in tr else None),
+            "reference_timing": "the unmodified reference run that made the trace (build "
+                                "container CPU, 8 cores), not this box",
+            "mode": "replay of the reference's H10 operator sequence (eps_grad 1e-6, 16 "
+                    "iterations), wall clock incl. host L-BFGS"}
 
 
 def main():

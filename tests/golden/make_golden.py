@@ -152,6 +152,7 @@ def adapt_trace(name: str, system: MolecularSystem, eps: float, max_iter: int):
         selected=np.array([labels.index(r.selected_op) if r.selected_op else -1
                            for r in res.records]),
         thetas=res.thetas,
+        wall_s=np.array([r.wall_elapsed for r in res.records]),   # this container's CPU
     )
     print(f"adapt {name}: {len(res.records)} records, status={res.status}, "
           f"E={res.records[-1].energy:.12f}")

@@ -289,7 +289,7 @@ def test_adapt_h4_criterion_2(hsv):
     assert hits and hits[0] <= 40
 
 
-@pytest.mark.parametrize("name", ["h4", "h6"])
+@pytest.mark.parametrize("name", ["h4", "h6", "h10"])
 def test_adapt_replay_matches_reference_trace(hsv, name):
     sysm = hsv.MolecularSystem.bundled(name)
     tr = load_golden(f"adapt_{name}")
