@@ -247,10 +247,11 @@ HSV_API int hsv_eg_forward_peer_async(hsv_op op, uint64_t hf_key, const uint64_t
                                       hsv_state psi, hsv_state w, hsv_peer p);
 
 /* ---- tuning knobs (defaults are the measured best): "apply_r" (rows per
- * lane 0/1/2/4), "apply_minb", "apply_split" (0/1/2/4/8/16/32), "apply_interleave"
- * (-1/0/1), "screen_rows", "push" (-1 auto, 0 pull only, 1 push whenever it
- * fits), "push_keys" (push budget factor), "sweep" (1 fused cooperative
- * sweeps, 0 one launch per rotation), "sweep_grid" (0 auto) ---- */
+ * lane 0 auto/1/2/4/8), "apply_minb", "apply_split" (0 auto/1/2/4/8/16/32),
+ * "apply_interleave" (-1 auto = 2 dynamic, 0 contiguous, 1 interleaved),
+ * "screen_rows", "push" (-1 auto, 0 pull only, 1 push whenever it fits),
+ * "push_keys" (push budget factor), "sweep" (1 fused cooperative sweeps, 0 one
+ * launch per rotation), "sweep_grid" (0 auto), "staged" (1: TMA-staged K1s) ---- */
 HSV_API int hsv_set_tuning(const char* key, int64_t value);
 
 /* ---- live kernel timing (CUDA events on the launch stream) ---- */

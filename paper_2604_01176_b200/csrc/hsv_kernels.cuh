@@ -6,9 +6,9 @@ namespace hsv {
 
 // Runtime tuning knobs (hsv_set_tuning); defaults are the measured best.
 struct Tuning {
-  int apply_r = 0;        // rows per lane in the K1 apply kernel (1, 2, 4; 0 = auto)
-  int apply_minb = 0;     // __launch_bounds__ min blocks/SM: 0 = default (R=2: 4, R=4: 3);
-                          // alternatives R=2: 3 or 5, R=4: 2
+  int apply_r = 0;        // rows per lane in the K1 apply kernel (1, 2, 4, 8; 0 = auto)
+  int apply_minb = 0;     // __launch_bounds__ min blocks/SM: 0 = default (R=2: 4, R=4: 3,
+                          // R=8: 2); alternatives R=2: 3, 5 or 6, R=4: 2
   int screen_rows = 1024; // rows staged per chunk in the screen kernel
   int apply_split = 0;    // bucket splits per row unit in K1 (0 = auto, else 1/2/4/8/16/32)
   int apply_interleave = -1;  // K1 unit schedule: -1 auto (= 2), 0 contiguous, 1 interleaved, 2 dynamic
@@ -49,8 +49,8 @@ struct ApplyArgs {
   int64_t a_lo, a_hi;
   int64_t units;
   int upr;
-  int nsplit;              // bucket splits per row unit (1: none)
-  int interleave;          // unit schedule: 0 contiguous blocks per warp, 1 interleaved
+  int nsplit;              // bucket splits per row unit (1: none), 2..32 (use_split_table)
+  int interleave;          // unit schedule: 0 contiguous, 1 interleaved, 2 dynamic (counter)
   int64_t dim_bytes;       // size of psi in bytes (schedule choice)
   const int* split_bk;     // nsplit + 1 bucket boundaries (in this launch's buckets)
   double2* ypart;          // [nsplit][rows of a_lo..a_hi] partial rows when nsplit > 1
