@@ -750,10 +750,10 @@ int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
   HSV_REQUIRE(psi && w && psi != w && psi->sec == op->sec && w->sec == op->sec,
               HSV_ERR_INVALID, "bad state argument");
   const hsv_sector_s* sec = op->sec;
-  double e_re = 0.0, e_im = 0.0;
-  HSV_TRY(hsv_state_dot(psi, w, &e_re, &e_im));
+  // [0, k): gradients, [k, k + 2): <psi|w>; one copy back at the end (no sync here)
   double* d_grad = nullptr;
-  HSV_TRY(dalloc(&d_grad, std::max<int64_t>(k, 1)));
+  HSV_TRY(dalloc(&d_grad, k + 2));
+  HSV_TRY(state_dot_async(psi, w, d_grad + k));
   HSV_TRY(state_arow_async(psi));
   HSV_TRY(state_arow_async(w));
   if (k > 0) HSV_TRY(state_norm2_async(w));   // <lam|lam> for the drift checks
@@ -780,8 +780,10 @@ int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
     a.fpsi = psi->d_arow; a.flam = w->d_arow;
     HSV_TRY(launch_pairs<kAdjoint>(pl, a));
   }
-  if (k > 0)
-    HSV_TRY_CUDA(cudaMemcpyAsync(grads, d_grad, k * sizeof(double), cudaMemcpyDeviceToHost, stream()));
+  static thread_local std::vector<double> h;
+  h.resize(k + 2);
+  HSV_TRY_CUDA(cudaMemcpyAsync(h.data(), d_grad, (k + 2) * sizeof(double),
+                               cudaMemcpyDeviceToHost, stream()));
   const int rc = sc.check();
   dfree(pl.la); dfree(pl.lb);
   sc.release();
@@ -789,7 +791,8 @@ int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
   psi->norm2_valid = false;
   psi->dense_hint = w->dense_hint = false;
   HSV_TRY(stream_sync());
-  *energy = e_re;
+  for (int64_t i = 0; i < k; ++i) grads[i] = h[i];
+  *energy = h[k];
   return rc;
 }
 

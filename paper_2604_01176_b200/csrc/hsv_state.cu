@@ -228,6 +228,19 @@ int upload_amps(const double* re, const double* im, int64_t n, double2** d_out) 
   return stream_sync();
 }
 
+// <a|b> into d_r[0..1] (re, im), stream-ordered
+int state_dot_async(hsv_state a, hsv_state b, double* d_r) {
+  const int64_t n = a->sec->dim;
+  const int grid = grid_for(n, 256);
+  double* part = nullptr;
+  HSV_TRY(dalloc(&part, 2 * (int64_t)grid));
+  k_dot<<<grid, 256, 0, stream()>>>(a->d_amp, b->d_amp, n, part);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  HSV_TRY(reduce_sum_f64(part, grid, 2, 2, d_r));
+  dfree(part);
+  return HSV_OK;
+}
 }  // namespace hsv
 
 using namespace hsv;
@@ -494,22 +507,16 @@ int hsv_state_get_positions(hsv_state st, const int64_t* pos, int64_t n, double*
   return HSV_OK;
 }
 
+
 int hsv_state_dot(hsv_state a, hsv_state b, double* re, double* im) {
   HSV_REQUIRE(a && b, HSV_ERR_INVALID, "null state");
   HSV_REQUIRE(a->sec == b->sec, HSV_ERR_INVALID, "dimension mismatch in dot");
-  const int64_t n = a->sec->dim;
-  const int grid = grid_for(n, 256);
-  double *part = nullptr, *d_r = nullptr;
-  HSV_TRY(dalloc(&part, 2 * (int64_t)grid));
+  double* d_r = nullptr;
   HSV_TRY(dalloc(&d_r, 2));
-  k_dot<<<grid, 256, 0, stream()>>>(a->d_amp, b->d_amp, n, part);
-  count_launch();
-  HSV_CHECK_LAUNCH();
-  HSV_TRY(reduce_sum_f64(part, grid, 2, 2, d_r));
+  HSV_TRY(state_dot_async(a, b, d_r));
   double h[2];
   HSV_TRY_CUDA(cudaMemcpyAsync(h, d_r, 16, cudaMemcpyDeviceToHost, stream()));
   HSV_TRY(stream_sync());
-  dfree(part);
   dfree(d_r);
   if (re) *re = h[0];
   if (im) *im = h[1];
