@@ -170,7 +170,8 @@ HSV_API int hsv_energy_gradient(hsv_op op, uint64_t hf_key, const uint64_t* occ_
                         int64_t k, double* energy, double* grads);
 /* The same sweep in two phases for multi-GPU (owner computes H psi rows):
  * forward: psi <- exp(...)|hf> on all rows (replicated), w rows [a_lo, a_hi)
- * <- (H psi) rows (returns after a stream sync, to report norm drift); the caller makes
+ * <- (H psi) rows (stream-ordered: a norm drift of the forward sweep is reported by
+ * the hsv_eg_backward that consumes psi); the caller makes
  * w complete on every rank (all-gather of the row blocks);
  * backward: E = Re<psi|w> and the adjoint sweep; psi and w are consumed. */
 HSV_API int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ_masks,

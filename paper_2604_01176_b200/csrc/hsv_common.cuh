@@ -229,6 +229,11 @@ struct hsv_state_s {
   // Set when the K1 push path found psi too dense (skip its probe next time);
   // cleared by every write.  Only ever disables the push path.
   bool dense_hint = false;
+  // Norm-drift flags of the forward sweep that built this state
+  // (hsv_eg_forward_async), read by the hsv_eg_backward that consumes it: the
+  // forward call does not wait for the device.
+  int* d_pend_err = nullptr;
+  double* d_pend_val = nullptr;
 };
 
 namespace hsv {

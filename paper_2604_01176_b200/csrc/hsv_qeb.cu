@@ -694,6 +694,23 @@ static int forward_psi(const hsv_sector_s* sec, uint64_t hf_key, const uint64_t*
   return HSV_OK;
 }
 
+// Reads (synchronously) and clears the forward sweep's drift flags left on psi.
+static int take_pending_drift(hsv_state psi) {
+  int h_err = 0;
+  double h_val = 0.0;
+  HSV_TRY_CUDA(cudaMemcpyAsync(&h_err, psi->d_pend_err, sizeof(int), cudaMemcpyDeviceToHost,
+                               stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(&h_val, psi->d_pend_val, sizeof(double), cudaMemcpyDeviceToHost,
+                               stream()));
+  HSV_TRY(stream_sync());
+  dfree(psi->d_pend_err);
+  dfree(psi->d_pend_val);
+  psi->d_pend_err = nullptr;
+  psi->d_pend_val = nullptr;
+  HSV_REQUIRE(!h_err, HSV_ERR_NORM_DRIFT, "norm drift %.3e in qeb exponential", h_val);
+  return HSV_OK;
+}
+
 // Phase 1 of the adjoint sweep: psi <- prod_i exp(theta_i T_i)|hf> (all rows;
 // occupancy flags and norm maintained), w rows [a_lo, a_hi) <- (H psi) rows.
 int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const uint64_t* virt,
@@ -713,8 +730,14 @@ int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const 
                        &psi->dense_hint));
   w->norm2_valid = w->arow_valid = false;
   w->dense_hint = false;
-  // drift errors surface here (synchronizes)
-  const int rc = sc.check();
+  // drift errors are read by hsv_eg_backward (no host sync here); an unread
+  // earlier report on psi is checked first
+  int rc = HSV_OK;
+  if (psi->d_pend_err) rc = take_pending_drift(psi);
+  psi->d_pend_err = sc.err;
+  psi->d_pend_val = sc.err_val;
+  sc.err = nullptr;
+  sc.err_val = nullptr;
   dfree(pl.la); dfree(pl.lb);
   sc.release();
   return rc;
@@ -793,6 +816,10 @@ int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
   HSV_TRY(stream_sync());
   for (int64_t i = 0; i < k; ++i) grads[i] = h[i];
   *energy = h[k];
+  if (psi->d_pend_err) {   // the forward sweep's drift report comes first
+    const int rf = take_pending_drift(psi);
+    if (rf) return rf;
+  }
   return rc;
 }
 

@@ -267,6 +267,8 @@ int hsv_state_destroy(hsv_state st) {
   dfree(st->d_amp);
   dfree(st->d_norm2);
   dfree(st->d_arow);
+  dfree(st->d_pend_err);
+  dfree(st->d_pend_val);
   delete st;
   return HSV_OK;
 }

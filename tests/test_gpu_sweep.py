@@ -93,3 +93,31 @@ def test_ansatz_state_equals_rotation_by_rotation(hsv, N, name, k):
         assert np.array_equal(fused.values, ref.values), sweep
     empty = hsv.apply_ansatz(sysm.basis, sysm.hf, [], [])
     assert empty.nnz == 1
+
+
+@pytest.mark.parametrize("sweep", [1, 0])
+def test_forward_drift_reported_by_backward(hsv, N, sweep):
+    """A non-unitary rotation (c^2 + s^2 != 1) in the forward sweep: the forward call
+    returns without waiting for the device and the consuming backward call raises
+    the reference's RuntimeError (svengine.py:234-236); the engine stays usable."""
+    sysm = hsv.MolecularSystem.bundled("h4")
+    eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
+    pool = hsv.build_qeb_pool(sysm.n_qubits, sysm.integrals.nelec)
+    ops = [pool.ops[-1], pool.ops[0]]
+    occ, virt = eng._pool_masks(ops)
+    from paper_2604_01176_b200.svengine import DeviceState
+    psi, w = DeviceState(sysm.basis), DeviceState(sysm.basis)
+    cs, sn = N.as_f64(np.array([1.5, 1.0])), N.as_f64(np.array([0.5, 0.0]))
+    na = sysm.basis._sector.n_alpha_strings
+    N.call("hsv_set_tuning", b"sweep", sweep)
+    N.call("hsv_eg_forward_async", eng.matrix.handle, int(sysm.hf.bits), N.ptr_u64(occ),
+           N.ptr_u64(virt), N.ptr_f64(cs), N.ptr_f64(sn), 2, 0, na, psi.handle, w.handle)
+    g = np.empty(2)
+    e = N.dbl()
+    with pytest.raises(RuntimeError, match="norm drift"):
+        N.call("hsv_eg_backward", eng.matrix.handle, psi.handle, w.handle, N.ptr_u64(occ),
+               N.ptr_u64(virt), N.ptr_f64(cs), N.ptr_f64(sn), 2, N.C.byref(e), N.ptr_f64(g))
+    th = np.array([0.1, -0.2])
+    e1, g1 = eng.energy_and_gradient(ops, th)
+    e2, g2 = eng.energy_and_gradient(ops, th)
+    assert e1 == e2 and np.array_equal(g1, g2)
