@@ -10,6 +10,7 @@ struct Tuning {
   int apply_minb = 0;     // __launch_bounds__ min blocks/SM: 0 = default (R=2: 4, R=4: 3,
                           // R=8: 2); alternatives R=2: 3, 5 or 6, R=4: 2
   int screen_rows = 1024; // rows staged per chunk in the screen kernel
+  int screen_pivot = -1;  // K4 rows: -1 auto (psi rows when psi is sparse), 0 w rows, 1 psi rows
   int apply_split = 0;    // bucket splits per row unit in K1 (0 = auto, else 1/2/4/8/16/32)
   int apply_interleave = -1;  // K1 unit schedule: -1 auto (= 2), 0 contiguous, 1 interleaved, 2 dynamic
   int push = -1;          // sparse-psi push path: -1 auto, 0 off, 1 whenever it fits in memory
@@ -145,7 +146,8 @@ int build_pair_lists_async(const hsv_sector_s* s, const OpMasks& m, PairLists& p
 
 int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
                   const hsv_pool_s* pool, int64_t a_lo, int64_t a_hi, double* d_grads,
-                  const uint32_t* psi_arow = nullptr, const uint32_t* w_arow = nullptr);
+                  const uint32_t* psi_arow = nullptr, const uint32_t* w_arow = nullptr,
+                  bool sparse_psi = false);
 int pool_prepare(hsv_pool_s* p);
 
 }  // namespace hsv

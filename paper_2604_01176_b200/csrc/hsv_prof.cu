@@ -86,6 +86,9 @@ int hsv_set_tuning(const char* key, int64_t value) {
   } else if (k == "push_keys") {
     HSV_REQUIRE(value >= 0 && value <= 4096, HSV_ERR_INVALID, "push_keys out of range");
     g_tuning.push_keys = (int)value;
+  } else if (k == "screen_pivot") {
+    HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "screen_pivot must be -1, 0 or 1");
+    g_tuning.screen_pivot = (int)value;
   } else if (k == "screen_rows") {
     HSV_REQUIRE(value >= 64 && value <= 8192, HSV_ERR_INVALID, "screen_rows out of range");
     g_tuning.screen_rows = (int)value;

@@ -45,7 +45,7 @@ struct ScreenArgs {
   const uint32_t* psi_arow;  // alpha-row occupancy of psi (or nullptr)
   const uint32_t* w_arow;    // alpha-row occupancy of w on owned rows (or nullptr)
   int64_t Nb;
-  int64_t a_lo;
+  int64_t a_lo, a_hi;
   int slices;
   double* part;          // [alpha rows][n_ops]
 };
@@ -57,19 +57,31 @@ __device__ __forceinline__ double re_conj_mul(double2 a, double2 b) {
 // D list entries per lane in flight: 2 (44 registers) while psi sits in L2, 4
 // (54 registers, fewer resident warps) once the gathers go to DRAM: H12 0.72 vs
 // 0.77 ms with 2, H16 0.68 vs 0.59 s with 4; 8 spills.
-template <int D>
+//
+// PIVOT (sparse psi): a CTA owns one alpha row rp of psi instead of one owned
+// row of w, and each operator pairs it with the w row Ra[s_p ^ f_a] (skipped
+// outside [a_lo, a_hi) or where w is zero).  The same (w row, psi row, beta
+// list) triples are summed, grouped by psi row: CTAs of empty psi rows write
+// zeros and leave, so the cost follows the support of psi.
+template <int D, bool PIVOT>
 __global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t rloc = blockIdx.y;
-  const int64_t ra = a.a_lo + rloc;
-  const uint32_t sa = __ldg(a.Sa + ra);
-  const double2* __restrict__ wrow = a.w + ra * a.Nb;
+  const int64_t rc = PIVOT ? rloc : a.a_lo + rloc;   // the CTA's row: w (own) or psi
+  const uint32_t sc = __ldg(a.Sa + rc);
+  const double2* __restrict__ crow = (PIVOT ? a.psi : a.w) + rc * a.Nb;
   const int stride = a.slices * kScreenWarps;
-  const bool w_zero = a.w_arow && !__ldg(a.w_arow + ra);   // own rows all zero
+  const bool c_zero = PIVOT ? (a.psi_arow && !__ldg(a.psi_arow + rc))
+                            : (a.w_arow && !__ldg(a.w_arow + rc));
+  int q = blockIdx.x * kScreenWarps + warp;
+  if (PIVOT && c_zero) {   // empty psi row: its partials are zero
+    if (lane == 0)
+      for (; q < a.n_ops; q += stride) a.part[rloc * a.n_ops + __ldg(a.qa + q).z] = 0.0;
+    return;
+  }
   // per-slot records in screen order, the next one loaded while the current
   // operator's list is walked (the per-operator setup was a chain of dependent
   // loads: order -> masks -> partner rank -> flag -> list)
-  int q = blockIdx.x * kScreenWarps + warp;
   int4 Qn = q < a.n_ops ? __ldg(a.qa + q) : make_int4(0, 0, 0, 0);
   int Ln = q < a.n_ops ? __ldg(a.qn + q) : 0;
   for (; q < a.n_ops; q += stride) {
@@ -82,16 +94,24 @@ __global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
     const int op = Q.z;
     const uint32_t oa = (uint32_t)Q.x, va = (uint32_t)Q.y;
     const uint32_t fa = oa | va;
-    const uint32_t ma = sa & fa;
-    const bool as = ma == oa, at = ma == va;   // both for an empty alpha half
+    const uint32_t m = sc & fa;
+    // as / at: the w row in source / target pattern (both for an empty alpha half);
+    // when pivoting the CTA row is the psi partner, whose pattern is the reverse
+    const bool as = PIVOT ? m == va : m == oa, at = PIVOT ? m == oa : m == va;
     double g = 0.0;
-    const uint32_t ra2 = (as || at) ? __ldg(a.Ra + (sa ^ fa)) : 0u;
-    if ((as || at) && !w_zero && !(a.psi_arow && !__ldg(a.psi_arow + ra2))) {
-      // 32-bit row offsets (dim < 2^32, checked by K1) and two list entries per
+    const uint32_t r2 = (as || at) ? __ldg(a.Ra + (sc ^ fa)) : 0u;
+    bool ok = (as || at) && !c_zero;
+    if (PIVOT)
+      ok = ok && r2 >= (uint32_t)a.a_lo && r2 < (uint32_t)a.a_hi &&
+           !(a.w_arow && !__ldg(a.w_arow + r2));
+    else
+      ok = ok && !(a.psi_arow && !__ldg(a.psi_arow + r2));
+    if (ok) {
+      // 32-bit row offsets (dim < 2^32, checked by K1) and D list entries per
       // lane in flight: independent gathers instead of one latency per entry
       // (0.87 -> 0.72 ms at H12)
-      const uint32_t poff = ra2 * (uint32_t)a.Nb;
-      const double2* __restrict__ prow = a.psi + poff;
+      const double2* __restrict__ wrow = PIVOT ? a.w + r2 * (uint32_t)a.Nb : crow;
+      const double2* __restrict__ prow = PIVOT ? crow : a.psi + r2 * (uint32_t)a.Nb;
       const int2 L = make_int2(Q.w, Ly);
       if (L.y < 0) {
         // empty beta half: every beta string is both source and target (alpha decides)
@@ -220,12 +240,14 @@ int pool_prepare(hsv_pool_s* p) {
 
 int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
                   const hsv_pool_s* pool, int64_t a_lo, int64_t a_hi, double* d_grads,
-                  const uint32_t* psi_arow, const uint32_t* w_arow) {
+                  const uint32_t* psi_arow, const uint32_t* w_arow, bool sparse_psi) {
   const hsv_sector_s* s = op->sec;
   const int n_ops = (int)pool->n;
   if (n_ops <= 0) return HSV_OK;
-  const int64_t rows = a_hi - a_lo;
-  if (rows <= 0) {
+  const int pv = tuning().screen_pivot;
+  const bool pivot = a_hi > a_lo && psi_arow && (pv > 0 || (pv < 0 && sparse_psi));
+  const int64_t rows = pivot ? s->Na : a_hi - a_lo;
+  if (a_hi <= a_lo) {
     HSV_TRY_CUDA(cudaMemsetAsync(d_grads, 0, n_ops * sizeof(double), stream()));
     return HSV_OK;
   }
@@ -241,17 +263,21 @@ int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
   a.Sa = s->d_Sa; a.Ra = s->d_Ra;
   a.ops = pool->d; a.order = pool->d_order; a.opl = pool->d_opl; a.blist = pool->d_blist;
   a.qa = pool->d_qa; a.qn = pool->d_qn;
-  a.n_ops = n_ops; a.psi = psi; a.w = w; a.Nb = s->Nb; a.a_lo = a_lo; a.slices = slices;
+  a.n_ops = n_ops; a.psi = psi; a.w = w; a.Nb = s->Nb; a.a_lo = a_lo; a.a_hi = a_hi;
+  a.slices = slices;
   a.part = part;
   a.psi_arow = psi_arow;
   a.w_arow = w_arow;
   {
     ProfScope prof("screen");
     const dim3 grid((unsigned)slices, (unsigned)rows);
-    if (2 * s->dim * (int64_t)sizeof(double2) > ctx().l2_bytes)
-      k_screen<4><<<grid, kScreenBlock, 0, stream()>>>(a);
+    const bool big = 2 * s->dim * (int64_t)sizeof(double2) > ctx().l2_bytes;
+    if (pivot)
+      big ? k_screen<4, true><<<grid, kScreenBlock, 0, stream()>>>(a)
+          : k_screen<2, true><<<grid, kScreenBlock, 0, stream()>>>(a);
     else
-      k_screen<2><<<grid, kScreenBlock, 0, stream()>>>(a);
+      big ? k_screen<4, false><<<grid, kScreenBlock, 0, stream()>>>(a)
+          : k_screen<2, false><<<grid, kScreenBlock, 0, stream()>>>(a);
   }
   count_launch();
   HSV_CHECK_LAUNCH();
@@ -284,7 +310,9 @@ static int energy_screen_dev(hsv_op op, hsv_state psi, const hsv_pool_s* pool, i
   uint32_t* wrow = nullptr;
   HSV_TRY(dalloc(&wrow, std::max<int64_t>(s->Na, 1)));
   HSV_TRY(arow_flags_async(w + a_lo * s->Nb, a_hi - a_lo, s->Nb, wrow + a_lo));
-  HSV_TRY(launch_screen(op, psi->d_amp, w, pool, a_lo, a_hi, d_out + 2, psi->d_arow, wrow));
+  // psi found sparse by K1 (push path taken, dense_hint still clear): pivot on psi rows
+  HSV_TRY(launch_screen(op, psi->d_amp, w, pool, a_lo, a_hi, d_out + 2, psi->d_arow, wrow,
+                        !psi->dense_hint));
   dfree(wrow);
   dfree(w);
   dfree(epart);
