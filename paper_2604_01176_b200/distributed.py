@@ -177,6 +177,7 @@ class DistributedSvAdaptEngine:
         groups = self.matrix.info()["n_active_groups"]
         self.replica_nnz = max(0, (32 * dim - (1 << 20)) // (1 + groups))
         self._last_nnz = 1                            # HF
+        self._evals = 0
         # NVLink peer exchange (CUDA IPC) for the sharded modes; NCCL otherwise
         # (HSV_PEER=0 forces NCCL)
         import os
@@ -208,7 +209,8 @@ class DistributedSvAdaptEngine:
         return nnz <= self.replica_nnz
 
     def energy_and_screen(self, state, pool):
-        if self.replicated(state.nnz):            # whole sector on every rank, no exchange
+        self._last_nnz = state.nnz                # once per ADAPT iteration
+        if self.replicated(self._last_nnz):       # whole sector on every rank, no exchange
             return self.inner.energy_and_screen(state, pool) if len(pool) else \
                 (self.inner.energy(state), np.zeros(0))
         sc = self._screen(pool)
@@ -246,7 +248,11 @@ class DistributedSvAdaptEngine:
             N.call("hsv_eg_forward_async", *args)
             if not rep:
                 allgather_rows(self._w.torch_view(), self.na, self.nb, self.group)
-        self._last_nnz = self._psi.nnz()
+        # the count is a host sync between the two phases: refresh it every 8th
+        # evaluation only (and at every screen); either mode gives the same result
+        self._evals += 1
+        if self._evals % 8 == 0:
+            self._last_nnz = self._psi.nnz()
         g = np.empty(th.size)
         e = N.dbl()
         N.call("hsv_eg_backward", self.matrix.handle, self._psi.handle, self._w.handle,
