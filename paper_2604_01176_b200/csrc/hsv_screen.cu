@@ -305,11 +305,18 @@ static int energy_screen_dev(hsv_op op, hsv_state psi, const hsv_pool_s* pool, i
   HSV_TRY(state_arow_async(psi));
   HSV_TRY(launch_apply(op, psi->d_amp, w, epart, a_lo, a_hi, 0.0, 0, &used, psi->d_arow,
                        &psi->dense_hint));
-  HSV_TRY(reduce_sum_f64(epart, used, 2, 2, d_out));
-  // occupancy of the owned rows of w (other rows of w are never read)
+  if (used == 1)   // already reduced to one (re, im) pair (dynamic schedule, push path)
+    HSV_TRY_CUDA(cudaMemcpyAsync(d_out, epart, 2 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                 stream()));
+  else
+    HSV_TRY(reduce_sum_f64(epart, used, 2, 2, d_out));
+  // occupancy of the owned rows of w (other rows of w are never read), which
+  // only lets K4 skip empty rows: not computed for a dense psi
   uint32_t* wrow = nullptr;
-  HSV_TRY(dalloc(&wrow, std::max<int64_t>(s->Na, 1)));
-  HSV_TRY(arow_flags_async(w + a_lo * s->Nb, a_hi - a_lo, s->Nb, wrow + a_lo));
+  if (!psi->dense_hint) {
+    HSV_TRY(dalloc(&wrow, std::max<int64_t>(s->Na, 1)));
+    HSV_TRY(arow_flags_async(w + a_lo * s->Nb, a_hi - a_lo, s->Nb, wrow + a_lo));
+  }
   // psi found sparse by K1 (push path taken, dense_hint still clear): pivot on psi rows
   HSV_TRY(launch_screen(op, psi->d_amp, w, pool, a_lo, a_hi, d_out + 2, psi->d_arow, wrow,
                         !psi->dense_hint));
