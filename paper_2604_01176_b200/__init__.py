@@ -16,7 +16,10 @@ from .svengine import (AnsatzElement, ExcitationOperator, PauliOperator, SvState
                        ansatz_energy_gradient, apply_ansatz, apply_generator,
                        apply_qeb_exponential, assemble_subspace_hamiltonian, expectation,
                        pool_gradient, pool_gradients)
-from .system import MolecularSystem
+from .system import MolecularSystem, bundled_fcidump
+from .chem import (IntegralSet, SecondQuantizedHamiltonian, hartree_fock_reference, jordan_wigner,
+                   load_fcidump, parse_fcidump, to_spin_orbital)
+from . import fcidump, mapping
 from .adapt import (AdaptConfig, OperatorPool, SvAdaptEngine, build_qeb_pool, run_adapt,
                     select_operator)
 

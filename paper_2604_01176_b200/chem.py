@@ -150,8 +150,51 @@ def _product(factors, scale: np.ndarray):
     return X.ravel(), Z.ravel(), C.ravel()
 
 
-def jordan_wigner(h: np.ndarray, g: np.ndarray, core_energy: float, n: int,
+@dataclass
+class SecondQuantizedHamiltonian:
+    """Spin-orbital coefficient tables, plain chemists' two-body form
+    (the reference's `mapping.py:33-45`)."""
+
+    n_spin_orbitals: int
+    core_energy: float
+    h: np.ndarray
+    g: np.ndarray
+    ordering: str
+    convention: str = "chemists-plain"
+
+    def validate(self):
+        if np.max(np.abs(self.h - self.h.T), initial=0.0) > 1e-12:
+            raise ValueError("one-body spin-orbital table is not symmetric")
+
+
+def to_spin_orbital(ints: IntegralSet, ordering: str = "interleaved") -> SecondQuantizedHamiltonian:
+    """Spatial integrals over 2*norb spin orbitals (reference `mapping.py:48-76`)."""
+    h, g = spin_orbital_tables(ints, ordering)
+    sq = SecondQuantizedHamiltonian(n_spin_orbitals=2 * ints.norb, core_energy=ints.core_energy,
+                                    h=h, g=g, ordering=ordering)
+    sq.validate()
+    return sq
+
+
+def hartree_fock_reference(n_electrons: int, n_qubits: int, ordering: str = "interleaved",
+                           ms2: int = 0):
+    """HF determinant (reference `mapping.py:129-132`)."""
+    return hartree_fock_configuration(n_electrons, n_qubits, ordering, ms2)
+
+
+def jordan_wigner(h, g=None, core_energy: float | None = None, n: int | None = None,
                   drop_tol: float = JW_DROP_TOL) -> PauliSum:
+    """JW image of H.  Called as the reference does, `jordan_wigner(sq, drop_tol)`
+    (`mapping.py:102`), or on the raw tables `jordan_wigner(h, g, core_energy, n)`."""
+    if isinstance(h, SecondQuantizedHamiltonian):
+        if isinstance(g, float):        # positional drop_tol, as in the reference
+            drop_tol, g = g, None
+        return _jordan_wigner_tables(h.h, h.g, h.core_energy, h.n_spin_orbitals, drop_tol)
+    return _jordan_wigner_tables(h, g, core_energy, n, drop_tol)
+
+
+def _jordan_wigner_tables(h: np.ndarray, g: np.ndarray, core_energy: float, n: int,
+                          drop_tol: float = JW_DROP_TOL) -> PauliSum:
     xs, zs, cs = [np.array([0])], [np.array([0])], [np.array([complex(core_energy)])]
     p, q = np.nonzero(h)
     if p.size:
@@ -178,8 +221,8 @@ def jordan_wigner(h: np.ndarray, g: np.ndarray, core_energy: float, n: int,
 def molecular_system(ints: IntegralSet, ordering: str = "interleaved"):
     """MolecularSystem from integrals (mirrors MolecularSystem.from_integrals, system.py:33-37)."""
     from .system import IntegralInfo, MolecularSystem
-    h, g = spin_orbital_tables(ints, ordering)
-    ham = jordan_wigner(h, g, ints.core_energy, 2 * ints.norb)
-    hf = hartree_fock_configuration(ints.nelec, 2 * ints.norb, ordering, ints.ms2)
+    sq = to_spin_orbital(ints, ordering)
+    ham = jordan_wigner(sq)
+    hf = hartree_fock_reference(ints.nelec, sq.n_spin_orbitals, ordering, ints.ms2)
     return MolecularSystem(integrals=IntegralInfo(ints.norb, ints.nelec, ints.ms2),
-                           ordering=ordering, hamiltonian=ham, hf=hf)
+                           ordering=ordering, hamiltonian=ham, hf=hf, sq=sq)

@@ -24,7 +24,11 @@ import numpy as np
 from . import _native as N
 from .cibasis import CiBasis, Configuration
 from .pauli import PauliSum
-from .sparse import CsrMatrix, SparseVector, dot, spmspv
+from .sparse import CsrMatrix, SparseVector, dot, norm, spmspv  # noqa: F401 (norm: svengine namespace)
+
+# the reference declares this chunk size but never reads it (svengine.py:29);
+# kept for namespace parity -- the matrix-free operator needs no assembly chunks
+ASSEMBLY_CHUNK_ENTRIES = 4_000_000
 
 NORM_DRIFT_TOL = 1e-9
 SECTOR_LEAK_TOL = 1e-10

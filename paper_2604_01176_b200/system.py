@@ -38,6 +38,24 @@ class IntegralInfo:
         return (self.nelec - self.ms2) // 2
 
 
+def bundled_fcidump(name: str) -> Path:
+    """Path of a bundled FCIDUMP (reference `system.py:15-22`).  This package
+    ships the Pauli sums built from them (`bundled_hamiltonian`); the FCIDUMP
+    text is looked up in `data/` and then in an importable `svmps`."""
+    path = DATA / f"{name.lower()}.fcidump"
+    if path.exists():
+        return path
+    try:
+        from importlib import resources
+        ref = resources.files("svmps").joinpath("data", f"{name.lower()}.fcidump")
+        with resources.as_file(ref) as concrete:
+            if concrete.exists():
+                return Path(concrete)
+    except (ImportError, ModuleNotFoundError, TypeError):
+        pass
+    raise FileNotFoundError(f"no bundled FCIDUMP named {name!r}")
+
+
 def bundled_hamiltonian(name: str) -> Path:
     path = DATA / f"ham_{name.lower()}.npz"
     if not path.exists():
@@ -51,7 +69,14 @@ class MolecularSystem:
     ordering: str
     hamiltonian: PauliSum
     hf: Configuration
+    sq: object = field(default=None, repr=False)   # chem.SecondQuantizedHamiltonian when built from integrals
     _basis: CiBasis | None = field(default=None, repr=False)
+
+    @classmethod
+    def from_integrals(cls, ints, ordering: str = "interleaved") -> "MolecularSystem":
+        """Integrals -> spin orbitals -> Jordan-Wigner (reference `system.py:33-37`)."""
+        from .chem import molecular_system
+        return molecular_system(ints, ordering)
 
     @classmethod
     def from_pauli(cls, h: PauliSum, nelec: int, ms2: int = 0,
