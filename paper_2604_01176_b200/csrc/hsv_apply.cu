@@ -121,9 +121,17 @@ __global__ void k_csr_rows(const uint32_t* __restrict__ Sa, const uint32_t* __re
 // IEEE rounding is symmetric under negation) and h a per-group perfect
 // multiply-shift hash of the in-sector patterns of b on x.  Other groups
 // (singles carrying number-operator Z's) run the sequential term loop.
-template <typename W, int SH, int R, int MINB>
+template <typename W, int SH, int R, int MINB, bool RS>
 __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
   const int lane = threadIdx.x & 31;
+  // RS: the pass-1 beta rank table Rb0 (2^norb words) is copied to shared
+  // memory once per CTA, so the per-(row, group) rank lookup is an LDS with a
+  // 32-bit address instead of a 64-bit-addressed LDG
+  extern __shared__ uint32_t rb0_sh[];
+  if (RS) {
+    for (uint32_t i = threadIdx.x; i < (uint32_t)a.rb0_n; i += blockDim.x) rb0_sh[i] = __ldg(a.Rb0 + i);
+    __syncthreads();
+  }
   // 32-bit indices throughout (dim < 2^32 is checked at launch): fewer
   // registers and integer instructions than 64-bit row arithmetic
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -205,7 +213,7 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
             const double A = __ldg(a.tabs + h);
             const int sgn = popc(s[k] & cur.z0) << 31;
             const double amp = __hiloint2double(__double2hiint(A) ^ sgn, __double2loint(A));
-            const uint32_t rk = __ldg(a.Rb0 + (uint32_t)(sb[k] ^ xb));
+            const uint32_t rk = RS ? rb0_sh[sb[k] ^ xb] : __ldg(a.Rb0 + (uint32_t)(sb[k] ^ xb));
             const double2 p = a.psi[rowoff + rk];
             acc[k].x = fma(amp, p.x, acc[k].x);
             acc[k].y = fma(amp, p.y, acc[k].y);
@@ -347,13 +355,17 @@ void use_split_table(const hsv_op_s* op, int St, ApplyArgs& a) {
   a.split_bk = op->d_splits + T.cut_off;
 }
 
-template <typename W, int SH, int R, int MINB>
+template <typename W, int SH, int R, int MINB, bool RS = false>
 static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_warps_out) {
   ApplyArgs a = a0;
   a.upr = (int)((a.Nb + 32 * R - 1) / (32 * R));
   const int64_t units1 = (a.a_hi - a.a_lo) * a.upr;
+  const size_t smem = RS ? (size_t)a.rb0_n * sizeof(uint32_t) : 0;
+  if (smem > 48 * 1024)
+    HSV_TRY_CUDA(cudaFuncSetAttribute(k_apply<W, SH, R, MINB, RS>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<W, SH, R, MINB>, 256, 0));
+  HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<W, SH, R, MINB, RS>, 256, smem));
   occ = std::max(occ, 1);
   const int64_t max_warps = (int64_t)ctx().num_sms * occ * 8;
   // Split the bucket range of each row unit.  Split-major unit order keeps the
@@ -403,7 +415,7 @@ static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_wa
   }
   {
     ProfScope prof("apply");
-    k_apply<W, SH, R, MINB><<<(unsigned)grid, 256, 0, stream()>>>(a);
+    k_apply<W, SH, R, MINB, RS><<<(unsigned)grid, 256, smem, stream()>>>(a);
     if (ypart)
       launch_combine_splits(ypart, S, rows, a.out, a.a_lo * a.Nb, a.prune, a.peer_rows,
                             a.n_peer_rows);
@@ -468,9 +480,15 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
     const bool dyn = tuning().apply_interleave < 0 || tuning().apply_interleave == 2;
     R = (dyn ? 32 * units8 >= warps8 : 4 * units8 >= 3 * warps8) ? 8 : units4 >= warps4 ? 4 : 2;
   }
+  // Rb0 in shared memory (opt-in; 2^norb words, H12 16 KB, H14 64 KB): measured
+  // slower, H12 2.415 vs 2.394 ms, H14 58.8 vs 57.3 ms -- K1 is issue-bound and
+  // the LDS saves no issue slot over the L1-resident LDG
+  const bool rs = !s->wide && tuning().rb0_smem == 1 && s->norb <= 15;
+  a.rb0_n = rs ? (1 << s->norb) : 0;
 #define HSV_APPLY_CASES(W, SH)                                              \
   if (R == 1) return launch_apply_t<W, SH, 1, 6>(op, a, n_warps);              \
   if (R == 4 && M == 2) return launch_apply_t<W, SH, 4, 2>(op, a, n_warps);    \
+  if (R == 8 && rs) return launch_apply_t<W, SH, 8, 2, true>(op, a, n_warps);  \
   if (R == 8) return launch_apply_t<W, SH, 8, 2>(op, a, n_warps);              \
   if (R == 4) return launch_apply_t<W, SH, 4, 3>(op, a, n_warps);              \
   if (M == 3) return launch_apply_t<W, SH, 2, 3>(op, a, n_warps);              \

@@ -17,6 +17,8 @@ struct Tuning {
   int push_keys = 32;     // auto: push while nnz(psi) * (1 + groups) <= push_keys * rows - 2^20
   int sweep = 1;          // adjoint/forward sweeps: 1 one cooperative launch, 0 launch per op
   int sweep_grid = 0;     // sweep blocks: 0 = min(co-resident, work items)
+  int rb0_smem = 0;       // K1 (R=8) pass-1 Rb0 table in shared memory: 1 on (norb <= 15),
+                          // 0/-1 off (default: measured 1-3% slower at H12/H14)
   int staged = 0;         // K1s (TMA-staged partner rows) where the sector fits: 1 on, 0 off.
                           // Off by default: it cuts K1's global load sectors 8.4x at H12
                           // but not its time (K1 is issue-bound; 3.04 vs 3.07 ms)
@@ -47,6 +49,7 @@ struct ApplyArgs {
   double2* out;      // nullptr: energy only
   double* epart;     // [warps][2] energy partials or nullptr
   int64_t Nb;
+  int rb0_n;               // Rb0 words staged in shared memory by K1 (0: read from global)
   int64_t a_lo, a_hi;
   int64_t units;
   int upr;

@@ -94,3 +94,22 @@ def test_row_shards_reproduce_full_rows(hsv, N):
         N.call("hsv_synchronize")
         y = out.torch_view().cpu().numpy()
         assert np.abs(y - full).max() <= 1e-13 * scale, parts
+
+
+@pytest.mark.parametrize("name", ["h8", "h10", "h12"])
+def test_rb0_shared_memory_is_bitwise_equal(hsv, N, name):
+    """K1 with the pass-1 rank table Rb0 staged in shared memory (tuning
+    rb0_smem = 1, opt-in) reads the same ranks as the global-memory
+    lookup: rows and energy bitwise equal, with and without bucket splits."""
+    sysm = hsv.MolecularSystem.bundled(name)
+    op = hsv.assemble_subspace_hamiltonian(sysm.hamiltonian, sysm.basis)
+    st = dense_state(hsv, sysm)
+    try:
+        for split in (1, 8):
+            N.call("hsv_set_tuning", b"rb0_smem", 0)
+            y0, e0 = rows_of(N, op, st, split, 8)
+            N.call("hsv_set_tuning", b"rb0_smem", 1)
+            y1, e1 = rows_of(N, op, st, split, 8)
+            assert np.array_equal(y0, y1) and e0 == e1, (name, split)
+    finally:
+        N.call("hsv_set_tuning", b"rb0_smem", 0)

@@ -37,6 +37,8 @@ def main():
     ap.add_argument("--shard-index", nargs="+", type=int, default=[0],
                     help="which shard of the --shard split to time (default the rank-0 one)")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--tune", nargs="+", default=[""],
+                    help="extra hsv_set_tuning settings per run, e.g. rb0_smem=0 (A/B axis)")
     ap.add_argument("--lib", default=None, help="alternative libhsv build (A/B runs)")
     args = ap.parse_args()
     if args.lib:
@@ -55,10 +57,14 @@ def main():
         info = op.info()
         na = basis._sector.n_alpha_strings
         d_out = None
-        for r, sr, mb, sp, sh, si in [(r, sr, mb, sp, sh, si) for r in args.apply_r
-                                      for sr in args.screen_rows for mb in args.minb
-                                      for sp in args.split for sh in args.shard
-                                      for si in args.shard_index if si < sh]:
+        for r, sr, mb, sp, sh, si, tu in [(r, sr, mb, sp, sh, si, tu) for r in args.apply_r
+                                          for sr in args.screen_rows for mb in args.minb
+                                          for sp in args.split for sh in args.shard
+                                          for si in args.shard_index if si < sh
+                                          for tu in args.tune]:
+            for kv in filter(None, tu.split(",")):
+                k, v = kv.split("=")
+                N.call("hsv_set_tuning", k.encode(), int(v))
             N.call("hsv_set_tuning", b"apply_r", r)
             N.call("hsv_set_tuning", b"apply_minb", mb)
             N.call("hsv_set_tuning", b"screen_rows", sr)
@@ -90,7 +96,7 @@ def main():
             bytes_apply = (16.0 * nnz + 24.0 * dim) * (a_hi - a_lo) / na
             print(json.dumps({
                 "system": name, "dim": dim, "apply_r": r, "minb": mb, "screen_rows": sr,
-                "split": sp, "shard": sh, "shard_index": si, "apply_ms": ta, "screen_ms": ts,
+                "split": sp, "tune": tu, "shard": sh, "shard_index": si, "apply_ms": ta, "screen_ms": ts,
                 "apply_GBs_alg": bytes_apply / ta / 1e6, "energy": e,
                 "gmax": None if g is None else float(np.max(np.abs(g))), "nnz": nnz, **info}),
                 flush=True)
