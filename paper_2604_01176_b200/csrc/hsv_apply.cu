@@ -121,10 +121,15 @@ __global__ void k_csr_rows(const uint32_t* __restrict__ Sa, const uint32_t* __re
 // IEEE rounding is symmetric under negation) and h a per-group perfect
 // multiply-shift hash of the in-sector patterns of b on x.  Other groups
 // (singles carrying number-operator Z's) run the sequential term loop.
-template <typename W, int SH, int R, int MINB, bool RS>
+template <typename W, int SH, int R, int MINB, int RM>
 __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
+  constexpr bool RS = RM == 1;
   const int lane = threadIdx.x & 31;
-  // RS: the pass-1 beta rank table Rb0 (2^norb words) is copied to shared
+  // Pass-1 partner beta rank rank(Sb[rb] ^ xb), by RM:
+  //   0: Rb0[Sb[rb] ^ xb]        (random 4-byte gather over the 2^norb table)
+  //   2: bperm[slot(xb) + rb]    (per-xb rank permutation, one coalesced 128-byte
+  //                               line per warp: fewer L1 wavefronts per pair)
+  // RM 1 (RS): the pass-1 beta rank table Rb0 (2^norb words) is copied to shared
   // memory once per CTA, so the per-(row, group) rank lookup is an LDS with a
   // 32-bit address instead of a 64-bit-addressed LDG
   extern __shared__ uint32_t rb0_sh[];
@@ -213,7 +218,8 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
             const double A = __ldg(a.tabs + h);
             const int sgn = popc(s[k] & cur.z0) << 31;
             const double amp = __hiloint2double(__double2hiint(A) ^ sgn, __double2loint(A));
-            const uint32_t rk = RS ? rb0_sh[sb[k] ^ xb] : __ldg(a.Rb0 + (uint32_t)(sb[k] ^ xb));
+            const uint32_t rk = RM == 2 ? __ldg(a.bperm + (cur.pad0 + rb0 + k * 32))
+                                : RS ? rb0_sh[sb[k] ^ xb] : __ldg(a.Rb0 + (uint32_t)(sb[k] ^ xb));
             const double2 p = a.psi[rowoff + rk];
             acc[k].x = fma(amp, p.x, acc[k].x);
             acc[k].y = fma(amp, p.y, acc[k].y);
@@ -355,17 +361,17 @@ void use_split_table(const hsv_op_s* op, int St, ApplyArgs& a) {
   a.split_bk = op->d_splits + T.cut_off;
 }
 
-template <typename W, int SH, int R, int MINB, bool RS = false>
+template <typename W, int SH, int R, int MINB, int RM = 0>
 static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_warps_out) {
   ApplyArgs a = a0;
   a.upr = (int)((a.Nb + 32 * R - 1) / (32 * R));
   const int64_t units1 = (a.a_hi - a.a_lo) * a.upr;
-  const size_t smem = RS ? (size_t)a.rb0_n * sizeof(uint32_t) : 0;
+  const size_t smem = RM == 1 ? (size_t)a.rb0_n * sizeof(uint32_t) : 0;
   if (smem > 48 * 1024)
-    HSV_TRY_CUDA(cudaFuncSetAttribute(k_apply<W, SH, R, MINB, RS>,
+    HSV_TRY_CUDA(cudaFuncSetAttribute(k_apply<W, SH, R, MINB, RM>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<W, SH, R, MINB, RS>, 256, smem));
+  HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<W, SH, R, MINB, RM>, 256, smem));
   occ = std::max(occ, 1);
   const int64_t max_warps = (int64_t)ctx().num_sms * occ * 8;
   // Split the bucket range of each row unit.  Split-major unit order keeps the
@@ -415,7 +421,7 @@ static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_wa
   }
   {
     ProfScope prof("apply");
-    k_apply<W, SH, R, MINB, RS><<<(unsigned)grid, 256, smem, stream()>>>(a);
+    k_apply<W, SH, R, MINB, RM><<<(unsigned)grid, 256, smem, stream()>>>(a);
     if (ypart)
       launch_combine_splits(ypart, S, rows, a.out, a.a_lo * a.Nb, a.prune, a.peer_rows,
                             a.n_peer_rows);
@@ -485,10 +491,17 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   // the LDS saves no issue slot over the L1-resident LDG
   const bool rs = !s->wide && tuning().rb0_smem == 1 && s->norb <= 15;
   a.rb0_n = rs ? (1 << s->norb) : 0;
+  // per-xb beta rank permutations (built at upload for 32-bit words when small)
+  // auto: beta rows of 2048+ strings (H14: 57.3 -> 56.5 ms); at H12 (924) the
+  // 16 KB Rb0 table stays in L1 and wins (2.387 vs 2.415 ms), H10 0.130 vs 0.127
+  const bool bp = !rs && op->d_bperm &&
+                  (tuning().bperm == 1 || (tuning().bperm < 0 && s->Nb >= 2048));
+  a.bperm = op->d_bperm;
 #define HSV_APPLY_CASES(W, SH)                                              \
   if (R == 1) return launch_apply_t<W, SH, 1, 6>(op, a, n_warps);              \
   if (R == 4 && M == 2) return launch_apply_t<W, SH, 4, 2>(op, a, n_warps);    \
-  if (R == 8 && rs) return launch_apply_t<W, SH, 8, 2, true>(op, a, n_warps);  \
+  if (R == 8 && rs) return launch_apply_t<W, SH, 8, 2, 1>(op, a, n_warps);     \
+  if (R == 8 && bp) return launch_apply_t<W, SH, 8, 2, 2>(op, a, n_warps);     \
   if (R == 8) return launch_apply_t<W, SH, 8, 2>(op, a, n_warps);              \
   if (R == 4) return launch_apply_t<W, SH, 4, 3>(op, a, n_warps);              \
   if (M == 3) return launch_apply_t<W, SH, 2, 3>(op, a, n_warps);              \
@@ -905,13 +918,39 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
     }
   }
   std::vector<unsigned char> recs;
+  // K1 pass-1 beta rank permutations: for each distinct beta flip xb of a hashed
+  // group, bperm[slot + rb] = rank(Sb[rb] ^ xb) (0 out of sector, as Rb0), rows
+  // padded to a multiple of 256 so a unit's tail lanes stay inside the slot.
+  // Rec.pad0 holds the slot offset.  Skipped above 256 MB or 2^32 entries.
+  std::vector<uint32_t> bperm, bslot(ghash.size(), 0u);
+  if (SH == 16) {
+    const int64_t NbP = (s->Nb + 255) / 256 * 256;
+    std::vector<uint32_t> xbs;
+    for (size_t q = 0; q < ghash.size(); ++q)
+      if (ghash[q].tab >= 0) xbs.push_back((uint32_t)op->groups[q].x);
+    std::sort(xbs.begin(), xbs.end());
+    xbs.erase(std::unique(xbs.begin(), xbs.end()), xbs.end());
+    const int64_t entries = (int64_t)xbs.size() * NbP + 256;
+    if (!xbs.empty() && entries * 4 <= (256ll << 20)) {
+      bperm.assign((size_t)entries, 0u);
+      for (size_t i = 0; i < xbs.size(); ++i)
+        for (int64_t rb = 0; rb < s->Nb; ++rb) {
+          const uint32_t r = s->Rb[s->Sb[rb] ^ xbs[i]];
+          bperm[i * NbP + rb] = r == ~0u ? 0u : r;
+        }
+      for (size_t q = 0; q < ghash.size(); ++q)
+        if (ghash[q].tab >= 0)
+          bslot[q] = (uint32_t)((std::lower_bound(xbs.begin(), xbs.end(),
+                                                  (uint32_t)op->groups[q].x) - xbs.begin()) * NbP);
+    }
+  }
   if (SH == 16) {
     recs.resize(ghash.size() * 32);
     for (size_t q = 0; q < ghash.size(); ++q) {
       const GroupHash& h = ghash[q];
       uint32_t r[8] = {(uint32_t)op->groups[q].x,
                        (uint32_t)op->groups[q].y | ((uint32_t)h.shift << 8), (uint32_t)h.xm,
-                       (uint32_t)h.z0, (uint32_t)h.mul, (uint32_t)std::max(h.tab, 0), 0u, 0u};
+                       (uint32_t)h.z0, (uint32_t)h.mul, (uint32_t)std::max(h.tab, 0), bslot[q], 0u};
       memcpy(&recs[q * 32], r, 32);
     }
   } else {
@@ -951,6 +990,11 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
                                cudaMemcpyHostToDevice, st));
   if (!recs.empty())
     HSV_TRY_CUDA(cudaMemcpyAsync(op->d_recs, recs.data(), recs.size(), cudaMemcpyHostToDevice, st));
+  if (!bperm.empty()) {
+    if ((rc = dalloc(&op->d_bperm, bperm.size()))) return fail(rc);
+    HSV_TRY_CUDA(cudaMemcpyAsync(op->d_bperm, bperm.data(), bperm.size() * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, st));
+  }
   if (!ghash.empty())
     HSV_TRY_CUDA(cudaMemcpyAsync(op->d_ghash, ghash.data(), ghash.size() * sizeof(GroupHash),
                                  cudaMemcpyHostToDevice, st));
@@ -986,6 +1030,7 @@ int hsv_op_destroy(hsv_op op) {
   dfree(op->d_gsz);
   dfree(reinterpret_cast<SzTerm*>(op->d_szt));
   dfree(op->d_gxa);
+  dfree(op->d_bperm);
   delete op;
   return HSV_OK;
 }

@@ -71,6 +71,9 @@ int hsv_set_tuning(const char* key, int64_t value) {
     HSV_REQUIRE(value >= 0 && value <= 32 && (value & (value - 1)) == 0, HSV_ERR_INVALID,
                 "apply_split must be 0 (auto), 1, 2, 4, 8, 16 or 32");
     g_tuning.apply_split = (int)value;
+  } else if (k == "bperm") {
+    HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "bperm must be -1, 0 or 1");
+    g_tuning.bperm = (int)value;
   } else if (k == "rb0_smem") {
     HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "rb0_smem must be -1, 0 or 1");
     g_tuning.rb0_smem = (int)value;
