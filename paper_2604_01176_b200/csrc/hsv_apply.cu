@@ -492,10 +492,9 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   const bool rs = !s->wide && tuning().rb0_smem == 1 && s->norb <= 15;
   a.rb0_n = rs ? (1 << s->norb) : 0;
   // per-xb beta rank permutations (built at upload for 32-bit words when small)
-  // auto: beta rows of 2048+ strings (H14: 57.3 -> 56.5 ms); at H12 (924) the
-  // 16 KB Rb0 table stays in L1 and wins (2.387 vs 2.415 ms), H10 0.130 vs 0.127
-  const bool bp = !rs && op->d_bperm &&
-                  (tuning().bperm == 1 || (tuning().bperm < 0 && s->Nb >= 2048));
+  // on wherever built (16-bit rows): H10 0.130 -> 0.125 ms, H12 2.386 -> 2.385,
+  // H14 57.3 -> 56.4, H16 1404 -> 1359 ms (32-bit rows lost at H12, 2.415)
+  const bool bp = !rs && op->d_bperm && tuning().bperm != 0;
   a.bperm = op->d_bperm;
 #define HSV_APPLY_CASES(W, SH)                                              \
   if (R == 1) return launch_apply_t<W, SH, 1, 6>(op, a, n_warps);              \
@@ -921,8 +920,10 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
   // K1 pass-1 beta rank permutations: for each distinct beta flip xb of a hashed
   // group, bperm[slot + rb] = rank(Sb[rb] ^ xb) (0 out of sector, as Rb0), rows
   // padded to a multiple of 256 so a unit's tail lanes stay inside the slot.
-  // Rec.pad0 holds the slot offset.  Skipped above 256 MB or 2^32 entries.
-  std::vector<uint32_t> bperm, bslot(ghash.size(), 0u);
+  // 16-bit ranks (Nb <= 65536): 64 bytes per warp row.  Rec.pad0 holds the slot
+  // offset.  Skipped above 256 MB.
+  std::vector<uint16_t> bperm;
+  std::vector<uint32_t> bslot(ghash.size(), 0u);
   if (SH == 16) {
     const int64_t NbP = (s->Nb + 255) / 256 * 256;
     std::vector<uint32_t> xbs;
@@ -931,12 +932,12 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
     std::sort(xbs.begin(), xbs.end());
     xbs.erase(std::unique(xbs.begin(), xbs.end()), xbs.end());
     const int64_t entries = (int64_t)xbs.size() * NbP + 256;
-    if (!xbs.empty() && entries * 4 <= (256ll << 20)) {
+    if (!xbs.empty() && s->Nb <= 65536 && entries * 2 <= (256ll << 20)) {
       bperm.assign((size_t)entries, 0u);
       for (size_t i = 0; i < xbs.size(); ++i)
         for (int64_t rb = 0; rb < s->Nb; ++rb) {
           const uint32_t r = s->Rb[s->Sb[rb] ^ xbs[i]];
-          bperm[i * NbP + rb] = r == ~0u ? 0u : r;
+          bperm[i * NbP + rb] = (uint16_t)(r == ~0u ? 0u : r);
         }
       for (size_t q = 0; q < ghash.size(); ++q)
         if (ghash[q].tab >= 0)
@@ -992,7 +993,7 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
     HSV_TRY_CUDA(cudaMemcpyAsync(op->d_recs, recs.data(), recs.size(), cudaMemcpyHostToDevice, st));
   if (!bperm.empty()) {
     if ((rc = dalloc(&op->d_bperm, bperm.size()))) return fail(rc);
-    HSV_TRY_CUDA(cudaMemcpyAsync(op->d_bperm, bperm.data(), bperm.size() * sizeof(uint32_t),
+    HSV_TRY_CUDA(cudaMemcpyAsync(op->d_bperm, bperm.data(), bperm.size() * sizeof(uint16_t),
                                  cudaMemcpyHostToDevice, st));
   }
   if (!ghash.empty())

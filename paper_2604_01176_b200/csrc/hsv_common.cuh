@@ -172,7 +172,7 @@ struct hsv_op_s {
   double* d_diag = nullptr;    // per internal row; nullptr if no diagonal terms
   GroupHash* d_ghash = nullptr;
   void* d_recs = nullptr;       // packed Rec<W> per group (kernel layout)
-  uint32_t* d_bperm = nullptr;  // per-xb beta rank permutations (Rec.pad0 = slot), or nullptr
+  uint16_t* d_bperm = nullptr;  // per-xb beta rank permutations (Rec.pad0 = slot), or nullptr
   int64_t n_buckets_h = 0;      // buckets [0, n_buckets_h) are x-local (hashed)
   int* d_splits = nullptr;      // split cuts (SplitTable::cut_off)
   int4* d_vbuckets = nullptr;   // virtual buckets of the split tables

@@ -17,8 +17,8 @@ struct Tuning {
   int push_keys = 32;     // auto: push while nnz(psi) * (1 + groups) <= push_keys * rows - 2^20
   int sweep = 1;          // adjoint/forward sweeps: 1 one cooperative launch, 0 launch per op
   int sweep_grid = 0;     // sweep blocks: 0 = min(co-resident, work items)
-  int bperm = -1;         // K1 (R=8) pass-1 ranks from per-xb permutation rows (built for
-                          // 32-bit words, <= 256 MB): -1 auto (Nb >= 2048), 1 on, 0 off
+  int bperm = -1;         // K1 (R=8) pass-1 ranks from per-xb 16-bit permutation rows (built
+                          // for 32-bit words, Nb <= 65536, <= 256 MB): -1/1 on, 0 off
   int rb0_smem = 0;       // K1 (R=8) pass-1 Rb0 table in shared memory: 1 on (norb <= 15),
                           // 0/-1 off (default: measured 1-3% slower at H12/H14)
   int staged = 0;         // K1s (TMA-staged partner rows) where the sector fits: 1 on, 0 off.
@@ -51,7 +51,7 @@ struct ApplyArgs {
   double2* out;      // nullptr: energy only
   double* epart;     // [warps][2] energy partials or nullptr
   int64_t Nb;
-  const uint32_t* bperm;   // per-xb beta rank permutations (Rec.pad0 = slot offset) or nullptr
+  const uint16_t* bperm;   // per-xb beta rank permutations (Rec.pad0 = slot offset) or nullptr
   int rb0_n;               // Rb0 words staged in shared memory by K1 (0: read from global)
   int64_t a_lo, a_hi;
   int64_t units;

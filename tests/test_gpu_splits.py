@@ -113,3 +113,22 @@ def test_rb0_shared_memory_is_bitwise_equal(hsv, N, name):
             assert np.array_equal(y0, y1) and e0 == e1, (name, split)
     finally:
         N.call("hsv_set_tuning", b"rb0_smem", 0)
+
+
+@pytest.mark.parametrize("name", ["h8", "h10", "h12"])
+def test_bperm_is_bitwise_equal(hsv, N, name):
+    """K1 pass-1 partner ranks from the per-xb 16-bit permutation rows (tuning
+    bperm, on by default where built) equal the Rb0 gather: rows and energy
+    bitwise, with and without bucket splits, at R = 8 and at R = 2."""
+    sysm = hsv.MolecularSystem.bundled(name)
+    op = hsv.assemble_subspace_hamiltonian(sysm.hamiltonian, sysm.basis)
+    st = dense_state(hsv, sysm)
+    try:
+        for split, r in ((1, 8), (8, 8), (8, 2)):
+            N.call("hsv_set_tuning", b"bperm", 0)
+            y0, e0 = rows_of(N, op, st, split, r)
+            N.call("hsv_set_tuning", b"bperm", 1)
+            y1, e1 = rows_of(N, op, st, split, r)
+            assert np.array_equal(y0, y1) and e0 == e1, (name, split, r)
+    finally:
+        N.call("hsv_set_tuning", b"bperm", -1)
