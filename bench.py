@@ -229,6 +229,9 @@ def run_hsv(args):
             os.dup2(saved, 1)
             os.close(saved)
     N.init(local)
+    for kv in args.tune:   # A/B runs of library tuning keys (hsv_set_tuning)
+        k, v = kv.split("=")
+        N.call("hsv_set_tuning", k.encode(), int(v))
     # a real (non-legacy) stream shared by torch events, NCCL and libhsv launches
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -487,6 +490,8 @@ def main():
     ap.add_argument("--adapt-iters", type=int, default=16)
     ap.add_argument("--config", default=CONFIG, choices=["h8", "h10", "h12", "h14", "h16"],
                     help="system (the BASELINE metric is quoted on h12; others for scaling runs)")
+    ap.add_argument("--tune", nargs="*", default=[], metavar="KEY=V",
+                    help="library tuning overrides (hsv_set_tuning), for A/B runs only")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "hsv":
         args.warmup = 3
