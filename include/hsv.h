@@ -252,7 +252,9 @@ HSV_API int hsv_eg_forward_peer_async(hsv_op op, uint64_t hf_key, const uint64_t
  * "apply_interleave" (-1 auto = 2 dynamic, 0 contiguous, 1 interleaved),
  * "screen_rows", "push" (-1 auto, 0 pull only, 1 push whenever it fits),
  * "push_keys" (push budget factor), "sweep" (1 fused cooperative sweeps, 0 one
- * launch per rotation), "sweep_grid" (0 auto), "staged" (1: TMA-staged K1s) ---- */
+ * launch per rotation), "sweep_grid" (0 auto), "staged" (1: TMA-staged K1s),
+ * "bperm" (K1 partner beta ranks from per-xb 16-bit rows: -1/1 on, 0 Rb0 gather),
+ * "rb0_smem" (1: Rb0 staged in shared memory, opt-in) ---- */
 HSV_API int hsv_set_tuning(const char* key, int64_t value);
 
 /* ---- live kernel timing (CUDA events on the launch stream) ---- */
