@@ -75,6 +75,11 @@ HSV_API int hsv_set_stream(void* cuda_stream);
 HSV_API void* hsv_get_stream(void);
 /* Number of CUDA kernels this library launched since the last reset. */
 HSV_API int64_t hsv_launch_count(int reset);
+/* Device work counters of the ADAPT evaluation kernels (8 slots): [0] rotation
+ * pairs processed by forward sweeps, [1] by adjoint sweeps, [2] rows computed by
+ * the support-restricted H application (K1r).  Synchronizes when out != NULL;
+ * reset != 0 zeroes them (stream-ordered). */
+HSV_API int hsv_stats(int64_t* out, int reset);
 HSV_API int hsv_synchronize(void);
 
 /* ---- sector: replaces CiBasis / enumerate_basis (cibasis.py:98-181) ---- */

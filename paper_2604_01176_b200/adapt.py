@@ -283,12 +283,14 @@ class RunResult:
 
 def run_adapt(config: AdaptConfig, system, *, pool: OperatorPool | None = None,
               reference_energy: float | None = None, csv_path=None, trunc_csv_path=None,
-              progress=None, engine=None, replay=None) -> RunResult:
+              progress=None, engine=None, replay=None, initial=None) -> RunResult:
     """screen -> select -> append -> optimize -> record (adapt.py:570-664).
 
     `replay` (optional list of pool indices) forces the operator sequence of a
     reference run, for parity checks where exact gradient ties make the free
-    selection non-unique (hard part 2).
+    selection non-unique (hard part 2).  `initial`
+    (optional (ops, thetas)) resumes a run from an ansatz of depth k: the loop
+    starts at iteration k with that state (the deep-ADAPT benchmark leg).
     """
     config.validate()
     engine = engine or make_engine(system, config)
@@ -319,12 +321,19 @@ def run_adapt(config: AdaptConfig, system, *, pool: OperatorPool | None = None,
             progress(rec)
 
     try:
-        state = engine.initial_state()
+        if initial is not None:
+            ansatz = list(initial[0])
+            thetas = np.array(initial[1], dtype=np.float64)
+            state = engine.rebuild(ansatz, thetas)
+            selected = ansatz[-1].label() if ansatz else None
+            it = len(ansatz)
+        else:
+            state = engine.initial_state()
+            selected = None
+            it = 0
         energy = engine.energy(state)
         n_evals += 1
         grads = engine.screen(state, pool)
-        selected = None
-        it = 0
         while True:
             emit(RunRecord(it, selected, float(np.max(np.abs(grads))), float(energy),
                            None if reference_energy is None else abs(energy - reference_energy),

@@ -11,6 +11,8 @@
 #include <cstring>
 #include <numeric>
 
+#include <cub/cub.cuh>
+
 #include "hsv_common.cuh"
 #include "hsv_kernels.cuh"
 
@@ -121,9 +123,10 @@ __global__ void k_csr_rows(const uint32_t* __restrict__ Sa, const uint32_t* __re
 // IEEE rounding is symmetric under negation) and h a per-group perfect
 // multiply-shift hash of the in-sector patterns of b on x.  Other groups
 // (singles carrying number-operator Z's) run the sequential term loop.
-template <typename W, int SH, int R, int MINB, int RM>
+template <typename W, int SH, int R, int MINB, int RM, int LM>
 __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
   constexpr bool RS = RM == 1;
+  static_assert(!(LM && RM == 2), "row-list mode reads partner ranks from Rb0");
   const int lane = threadIdx.x & 31;
   // Pass-1 partner beta rank rank(Sb[rb] ^ xb), by RM:
   //   0: Rb0[Sb[rb] ^ xb]        (random 4-byte gather over the 2^norb table)
@@ -141,7 +144,9 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
   // registers and integer instructions than 64-bit row arithmetic
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t tw = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t units = (uint32_t)a.units, Nb = (uint32_t)a.Nb;
+  // LM (K1r): the unit count comes from the device-built list (no host sync)
+  const uint32_t units = LM ? __ldg(a.d_units) * (uint32_t)a.nsplit : (uint32_t)a.units;
+  const uint32_t Nb = (uint32_t)a.Nb;
   // energy partials live in shared memory, not in registers across the group loop
   __shared__ double esh[8][2];
   if (lane == 0) { esh[threadIdx.x >> 5][0] = 0.0; esh[threadIdx.x >> 5][1] = 0.0; }
@@ -172,19 +177,30 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
     const uint32_t u = uw - (uint32_t)sp * units1;
     const int bk0 = a.split_bk ? __ldg(a.split_bk + sp) : 0;
     const int bk1 = a.split_bk ? __ldg(a.split_bk + sp + 1) : a.n_buckets;
-    const uint32_t ur = u / (uint32_t)a.upr;
-    const uint32_t ra = (uint32_t)a.a_lo + ur;
-    const uint32_t rb0 = (u - ur * (uint32_t)a.upr) * (32 * R) + lane;
+    uint32_t ra, rb0, lcnt = 0u;
+    const uint32_t* lrow = nullptr;
+    if (LM) {   // K1r: the lane's rows are list entries rb0, rb0 + 32, ... of alpha row ra
+      const uint2 ut = __ldg(a.utab + u);
+      ra = (uint32_t)a.a_lo + ut.x;
+      rb0 = ut.y * (32 * R) + lane;
+      lcnt = __ldg(a.rcnt + ut.x);
+      lrow = a.rlist + (size_t)ut.x * Nb;
+    } else {
+      const uint32_t ur = u / (uint32_t)a.upr;
+      ra = (uint32_t)a.a_lo + ur;
+      rb0 = (u - ur * (uint32_t)a.upr) * (32 * R) + lane;
+    }
     const uint32_t sa = __ldg(a.Sa + ra);
     const uint32_t rowbase = ra * Nb;
     W s[R];
     uint32_t sb[R];
     double2 acc[R];
-    unsigned live = 0u;
+    unsigned live = 0u, inrm = 0u;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      const uint32_t rb = rb0 + k * 32;
+      const uint32_t rb = LM ? (rb0 + k * 32 < lcnt ? __ldg(lrow + rb0 + k * 32) : Nb) : rb0 + k * 32;
       const bool inr = rb < Nb;
+      if (LM) inrm |= inr ? (1u << k) : 0u;
       sb[k] = inr ? __ldg(a.Sb + rb) : 0u;
       s[k] = (W)sa | ((W)sb[k] << SH);
       const double2 pv = inr ? a.psi[rowbase + rb] : make_double2(0.0, 0.0);
@@ -286,8 +302,8 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) {
-      const uint32_t rb = rb0 + k * 32;
-      if (rb >= Nb) continue;
+      if (LM ? !((inrm >> k) & 1u) : rb0 + k * 32 >= Nb) continue;
+      const uint32_t rb = LM ? __ldg(a.Rb + sb[k]) : rb0 + k * 32;
       if (a.out) {
         if (a.nsplit > 1) {   // partial row, combined in split order by k_combine_splits
           a.ypart[(int64_t)sp * a.part_stride + (rowbase + rb - (uint32_t)a.a_lo * Nb)] = acc[k];
@@ -302,8 +318,8 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
       double er = 0.0, ei = 0.0;
 #pragma unroll
       for (int k = 0; k < R; ++k) {
-        const uint32_t rb = rb0 + k * 32;
-        if (rb < Nb && ((live >> k) & 1u)) {
+        if ((LM ? (inrm >> k) & 1u : rb0 + k * 32 < Nb) && ((live >> k) & 1u)) {
+          const uint32_t rb = LM ? __ldg(a.Rb + sb[k]) : rb0 + k * 32;
           const double2 pv = a.psi[rowbase + rb];
           er += pv.x * acc[k].x + pv.y * acc[k].y;
           ei += pv.x * acc[k].y - pv.y * acc[k].x;
@@ -348,6 +364,33 @@ void launch_combine_splits(const double2* part, int S, int64_t rows, double2* ou
                                                                            prune, peers, n_peers);
 }
 
+// K1r: rows marked in smap get the sum of their split partials (split order,
+// as k_combine_splits), every other row an exact zero.
+__global__ void k_combine_splits_map(const double2* __restrict__ part, int S, int64_t rows,
+                                     double2* __restrict__ out, int64_t off,
+                                     const uint8_t* __restrict__ smap, double2* const* peers,
+                                     int n_peers) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= rows) return;
+  double2 y = make_double2(0.0, 0.0);
+  if (smap[off + i]) {
+    y = part[i];
+    for (int s = 1; s < S; ++s) {
+      const double2 p = part[s * rows + i];
+      y.x += p.x;
+      y.y += p.y;
+    }
+  }
+  put_row(out, peers, n_peers, off + i, y);
+}
+
+static void launch_combine_splits_map(const double2* part, int S, int64_t rows, double2* out,
+                                      int64_t off, const uint8_t* smap, double2* const* peers,
+                                      int n_peers) {
+  k_combine_splits_map<<<(unsigned)((rows + 255) / 256), 256, 0, stream()>>>(
+      part, S, rows, out, off, smap, peers, n_peers);
+}
+
 // Point a launch at the split table for S parts (virtual buckets + cuts).
 void use_split_table(const hsv_op_s* op, int St, ApplyArgs& a) {
   if (St <= 1) {
@@ -361,17 +404,22 @@ void use_split_table(const hsv_op_s* op, int St, ApplyArgs& a) {
   a.split_bk = op->d_splits + T.cut_off;
 }
 
-template <typename W, int SH, int R, int MINB, int RM = 0>
-static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_warps_out) {
+template <typename W, int SH, int R, int MINB, int RM = 0, int LM = 0>
+static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_warps_out,
+                          const uint8_t* smap = nullptr, int64_t list_units = 0) {
   ApplyArgs a = a0;
   a.upr = (int)((a.Nb + 32 * R - 1) / (32 * R));
-  const int64_t units1 = (a.a_hi - a.a_lo) * a.upr;
+  // units of the full row range: the split count S below depends on it only, so
+  // the row-list launch (LM) picks the same S as the full one and its rows are
+  // bit-identical to the full kernel's
+  const int64_t units1_full = (a.a_hi - a.a_lo) * a.upr;
+  const int64_t units1 = LM ? list_units : units1_full;
   const size_t smem = RM == 1 ? (size_t)a.rb0_n * sizeof(uint32_t) : 0;
   if (smem > 48 * 1024)
-    HSV_TRY_CUDA(cudaFuncSetAttribute(k_apply<W, SH, R, MINB, RM>,
+    HSV_TRY_CUDA(cudaFuncSetAttribute(k_apply<W, SH, R, MINB, RM, LM>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<W, SH, R, MINB, RM>, 256, smem));
+  HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<W, SH, R, MINB, RM, LM>, 256, smem));
   occ = std::max(occ, 1);
   const int64_t max_warps = (int64_t)ctx().num_sms * occ * 8;
   // Split the bucket range of each row unit.  Split-major unit order keeps the
@@ -384,16 +432,18 @@ static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_wa
   int S = tuning().apply_split;
   if (S <= 0) {
     S = 8;
-    while (S < 32 && units1 * S < 8 * max_warps) S *= 2;
+    while (S < 32 && units1_full * S < 8 * max_warps) S *= 2;
     const int64_t rows_all = (a.a_hi - a.a_lo) * a.Nb;
     while (S > 1 && a.out && S * rows_all * (int64_t)sizeof(double2) > (32ll << 30)) S /= 2;
   }
   if (!a0.split_bk) S = 1;
+  // K1r with peer stores: the combine pass must write (zero) every row to the peers
+  if (LM && S == 1 && a.n_peer_rows > 0 && a0.split_bk) S = 2;
   a.nsplit = S;
   use_split_table(op, S, a);
   // interleaved unless forced off (measured best at H12 and H14)
   const int il = tuning().apply_interleave;   // -1 auto (= 2), 0 contiguous, 1 interleaved, 2 dynamic
-  a.interleave = il < 0 ? 2 : il;
+  a.interleave = LM || il < 0 ? 2 : il;       // the list mode's unit count is on the device
   a.units = units1 * S;
   int64_t grid = max_warps / 8;
   const int64_t need = (a.units + 7) / 8;
@@ -408,6 +458,8 @@ static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_wa
     a.ucounter = ucounter;
     if (a.epart) {
       HSV_TRY(dalloc(&upart, 2 * a.units));
+      if (LM)   // units past the device count leave their partials untouched
+        HSV_TRY_CUDA(cudaMemsetAsync(upart, 0, 2 * a.units * sizeof(double), stream()));
       a.upart = upart;
     }
     if (n_warps_out) *n_warps_out = 1;   // the unit partials are reduced into epart[0..1] below
@@ -419,10 +471,15 @@ static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_wa
     a.ypart = ypart;
     a.part_stride = rows;
   }
+  if (LM && a.out && !ypart)   // rows outside the list are exact zeros
+    HSV_TRY_CUDA(cudaMemsetAsync(a.out + a.a_lo * a.Nb, 0, rows * sizeof(double2), stream()));
   {
-    ProfScope prof("apply");
-    k_apply<W, SH, R, MINB, RM><<<(unsigned)grid, 256, smem, stream()>>>(a);
-    if (ypart)
+    ProfScope prof(LM ? "apply_rows" : "apply");
+    k_apply<W, SH, R, MINB, RM, LM><<<(unsigned)grid, 256, smem, stream()>>>(a);
+    if (ypart && LM)
+      launch_combine_splits_map(ypart, S, rows, a.out, a.a_lo * a.Nb, smap, a.peer_rows,
+                                a.n_peer_rows);
+    else if (ypart)
       launch_combine_splits(ypart, S, rows, a.out, a.a_lo * a.Nb, a.prune, a.peer_rows,
                             a.n_peer_rows);
   }
@@ -510,6 +567,141 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   if (s->wide) { HSV_APPLY_CASES(uint64_t, 32) }
   HSV_APPLY_CASES(uint32_t, 16)
 #undef HSV_APPLY_CASES
+}
+
+// ------------------------------------------------------ K1r (row lists)
+// One block per alpha row: the marked beta ranks of the row in ascending order
+// (ballot + popc compaction), and their count.
+__global__ void k_rowlist(const uint8_t* __restrict__ smap, const double2* __restrict__ amp,
+                          int64_t a_lo, int64_t Nb, uint32_t* __restrict__ rlist,
+                          uint32_t* __restrict__ rcnt, unsigned long long* stats) {
+  __shared__ uint32_t wsum[8];
+  __shared__ uint32_t base;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t row0 = (a_lo + blockIdx.x) * Nb;
+  uint32_t* out = rlist + (int64_t)blockIdx.x * Nb;
+  if (threadIdx.x == 0) base = 0;
+  __syncthreads();
+  for (int64_t j0 = 0; j0 < Nb; j0 += 256) {
+    const int64_t j = j0 + threadIdx.x;
+    bool f = false;
+    if (j < Nb) {
+      if (smap) {
+        f = smap[row0 + j] != 0;
+      } else {
+        const double2 v = amp[row0 + j];
+        f = v.x != 0.0 || v.y != 0.0;
+      }
+    }
+    const unsigned b = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wsum[w] = __popc(b);
+    __syncthreads();
+    uint32_t off = base;
+    for (int q = 0; q < w; ++q) off += wsum[q];
+    if (f) out[off + __popc(b & ((1u << lane) - 1u))] = (uint32_t)j;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int q = 0; q < 8; ++q) t += wsum[q];
+      base += t;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    rcnt[blockIdx.x] = base;
+    if (stats && base) atomicAdd(stats + kStatRowsK1r, (unsigned long long)base);
+  }
+}
+
+// Single block: unit table (alpha row, chunk) in alpha-row order, and the count.
+__global__ void __launch_bounds__(1024) k_unit_table(const uint32_t* __restrict__ rcnt,
+                                                     int64_t n_rows, uint32_t rpu,
+                                                     uint2* __restrict__ utab,
+                                                     uint32_t* __restrict__ d_units) {
+  typedef cub::BlockScan<uint32_t, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ uint32_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t c0 = 0; c0 < n_rows; c0 += 1024) {
+    const int64_t i = c0 + threadIdx.x;
+    const uint32_t nu = i < n_rows ? (__ldg(rcnt + i) + rpu - 1) / rpu : 0u;
+    uint32_t ex, tot;
+    Scan(tmp).ExclusiveSum(nu, ex, tot);
+    const uint32_t off = carry + ex;
+    for (uint32_t q = 0; q < nu; ++q) utab[off + q] = make_uint2((uint32_t)i, q);
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *d_units = carry;
+}
+
+int RowList::build(const hsv_sector_s* s, const uint8_t* smap, const double2* amp, int64_t a_lo,
+                   int64_t a_hi, int rpu) {
+  const int64_t na = a_hi - a_lo;
+  max_units = na * ((s->Nb + rpu - 1) / rpu);
+  HSV_TRY(dalloc(&rlist, std::max<int64_t>(na * s->Nb, 1)));
+  HSV_TRY(dalloc(&rcnt, std::max<int64_t>(na, 1)));
+  HSV_TRY(dalloc(&utab, std::max<int64_t>(max_units, 1)));
+  HSV_TRY(dalloc(&d_units, 1));
+  if (na == 0) {
+    HSV_TRY_CUDA(cudaMemsetAsync(d_units, 0, sizeof(uint32_t), stream()));
+    return HSV_OK;
+  }
+  k_rowlist<<<(unsigned)na, 256, 0, stream()>>>(smap, amp, a_lo, s->Nb, rlist, rcnt,
+                                                 ctx().d_stats);
+  k_unit_table<<<1, 1024, 0, stream()>>>(rcnt, na, (uint32_t)rpu, utab, d_units);
+  count_launch(2);
+  HSV_CHECK_LAUNCH();
+  return HSV_OK;
+}
+
+void RowList::release() {
+  dfree(rlist);
+  dfree(rcnt);
+  dfree(utab);
+  dfree(d_units);
+  rlist = rcnt = d_units = nullptr;
+  utab = nullptr;
+}
+
+int launch_apply_rows(const hsv_op_s* op, const double2* psi, double2* out, int64_t a_lo,
+                      int64_t a_hi, const uint32_t* arow, const uint8_t* smap) {
+  const hsv_sector_s* s = op->sec;
+  HSV_REQUIRE(s->dim < ((int64_t)1 << 32), HSV_ERR_UNSUPPORTED,
+              "sector dimension %lld exceeds the 32-bit row index of the apply kernel",
+              (long long)s->dim);
+  ApplyArgs a{};
+  a.arow = arow;
+  a.split_bk = op->d_splits;
+  a.dim_bytes = s->dim * (int64_t)sizeof(double2);
+  a.Sa = s->d_Sa; a.Sb = s->d_Sb; a.Ra = s->d_Ra; a.Rb = s->d_Rb; a.Rb0 = s->d_Rb0;
+  a.buckets = op->d_buckets; a.n_buckets = (int)op->n_buckets;
+  a.groups = op->d_groups; a.terms = op->d_terms; a.diag = op->d_diag;
+  a.tabs = op->d_tabs; a.recs = op->d_recs; a.n_buckets_h = (int)op->n_buckets_h;
+  a.gsz = op->d_gsz; a.szt = op->d_szt; a.gxa = op->d_gxa; a.g_hashed = (int)op->g_hashed;
+  a.peer_rows = ctx().peer_rows;
+  a.n_peer_rows = ctx().n_peer_rows;
+  a.psi = psi; a.out = out; a.epart = nullptr;
+  a.Nb = s->Nb; a.a_lo = a_lo; a.a_hi = a_hi; a.prune = 0.0; a.energy_only = 0;
+  // rows per lane: 8 while the full row range gives a 256-row unit to every
+  // resident warp (the full kernel's rule), else 4
+  const int64_t units8 = (a_hi - a_lo) * ((s->Nb + 255) / 256);
+  const int R = 32 * units8 >= (int64_t)ctx().num_sms * 2 * 8 ? 8 : 4;
+  RowList rl;
+  int rc = rl.build(s, smap, nullptr, a_lo, a_hi, 32 * R);
+  if (rc == HSV_OK) {
+    a.rlist = rl.rlist; a.rcnt = rl.rcnt; a.utab = rl.utab; a.d_units = rl.d_units;
+    if (s->wide)
+      rc = R == 8 ? launch_apply_t<uint64_t, 32, 8, 2, 0, 1>(op, a, nullptr, smap, rl.max_units)
+                  : launch_apply_t<uint64_t, 32, 4, 3, 0, 1>(op, a, nullptr, smap, rl.max_units);
+    else
+      rc = R == 8 ? launch_apply_t<uint32_t, 16, 8, 2, 0, 1>(op, a, nullptr, smap, rl.max_units)
+                  : launch_apply_t<uint32_t, 16, 4, 3, 0, 1>(op, a, nullptr, smap, rl.max_units);
+  }
+  rl.release();
+  return rc;
 }
 
 // Host: does group [t0, t1) admit amp(b) = (-1)^popc(b&z0) * A[h(b & x)]?  If
@@ -1128,6 +1320,7 @@ int hsv_apply_h(hsv_op op, hsv_state in, hsv_state out, double prune) {
                        in->d_arow, &in->dense_hint));
   out->norm2_valid = false;
   out->arow_valid = false;
+  out->smap_valid = false;
   out->dense_hint = false;
   return stream_sync();
 }
@@ -1143,6 +1336,7 @@ int hsv_apply_h_rows_async(hsv_op op, hsv_state in, hsv_state out, int64_t a_lo,
                        in->d_arow, &in->dense_hint));
   out->norm2_valid = false;
   out->arow_valid = false;
+  out->smap_valid = false;
   out->dense_hint = false;
   return HSV_OK;
 }

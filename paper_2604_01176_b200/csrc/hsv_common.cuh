@@ -66,7 +66,11 @@ struct Context {
   // every output row into these peer buffers (NVLink), see ApplyArgs::peer_rows
   double2* const* peer_rows = nullptr;
   int n_peer_rows = 0;
+  // device work counters (hsv_stats): exact units processed by the ADAPT
+  // evaluation kernels, for the bench's algorithmic-byte accounting
+  unsigned long long* d_stats = nullptr;
 };
+enum StatKey { kStatPairsFwd = 0, kStatPairsAdj = 1, kStatRowsK1r = 2, kStatCount = 8 };
 Context& ctx();
 int ensure_init();
 inline cudaStream_t stream() { return ctx().stream; }
@@ -235,6 +239,13 @@ struct hsv_state_s {
   // forward call does not wait for the device.
   int* d_pend_err = nullptr;
   double* d_pend_val = nullptr;
+  // Structural support of an ansatz state (1 byte per row, allocated on first
+  // use): row b is marked when some rotation of the forward sweep that built
+  // psi can have moved amplitude into it (hsv_eg_forward_async).  Superset of
+  // the nonzeros, independent of exact cancellations; the support-restricted
+  // K1 computes w = H psi on these rows only (hsv_apply.cu, K1r).
+  uint8_t* d_smap = nullptr;
+  bool smap_valid = false;
 };
 
 namespace hsv {

@@ -209,6 +209,23 @@ int hsv_init(int device) {
   HSV_TRY_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
   uint64_t thr = UINT64_MAX;
   HSV_TRY_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  if (!g_ctx.d_stats) {
+    HSV_TRY_CUDA(cudaMalloc(&g_ctx.d_stats, kStatCount * sizeof(unsigned long long)));
+    HSV_TRY_CUDA(cudaMemset(g_ctx.d_stats, 0, kStatCount * sizeof(unsigned long long)));
+  }
+  return HSV_OK;
+}
+
+int hsv_stats(int64_t* out, int reset) {
+  HSV_TRY(ensure_init());
+  if (out) {
+    HSV_TRY(stream_sync());
+    HSV_TRY_CUDA(cudaMemcpy(out, g_ctx.d_stats, kStatCount * sizeof(int64_t),
+                            cudaMemcpyDeviceToHost));
+  }
+  if (reset)
+    HSV_TRY_CUDA(cudaMemsetAsync(g_ctx.d_stats, 0, kStatCount * sizeof(unsigned long long),
+                                 stream()));
   return HSV_OK;
 }
 

@@ -15,12 +15,15 @@ struct Tuning {
   int apply_interleave = -1;  // K1 unit schedule: -1 auto (= 2), 0 contiguous, 1 interleaved, 2 dynamic
   int push = -1;          // sparse-psi push path: -1 auto, 0 off, 1 whenever it fits in memory
   int push_keys = 32;     // auto: push while nnz(psi) * (1 + groups) <= push_keys * rows - 2^20
-  int sweep = 1;          // adjoint/forward sweeps: 1 one cooperative launch, 0 launch per op
+  int sweep = 2;          // adjoint/forward sweeps: 2 batched (orbits of kBatch rotations per
+                          // grid barrier, hsv_sweep.cu), 1 one barrier per rotation, 0 launch per op
   int sweep_grid = 0;     // sweep blocks: 0 = min(co-resident, work items)
   int bperm = -1;         // K1 (R=8) pass-1 ranks from per-xb 16-bit permutation rows (built
                           // for 32-bit words, Nb <= 65536, <= 256 MB): -1/1 on, 0 off
   int rb0_smem = 0;       // K1 (R=8) pass-1 Rb0 table in shared memory: 1 on (norb <= 15),
                           // 0/-1 off (default: measured 1-3% slower at H12/H14)
+  int restrict_rows = -1; // K1r in the adjoint evaluation (w = H psi on the structural
+                          // support of psi only): -1/1 on, 0 off (full K1 / push)
   int staged = 0;         // K1s (TMA-staged partner rows) where the sector fits: 1 on, 0 off.
                           // Off by default: it cuts K1's global load sectors 8.4x at H12
                           // but not its time (K1 is issue-bound; 3.04 vs 3.07 ms)
@@ -68,6 +71,26 @@ struct ApplyArgs {
   double* upart;              // dynamic schedule: [units][2] energy partials
   double2* const* peer_rows;  // device array: other ranks' w buffers (NVLink), or nullptr
   int n_peer_rows;
+  // K1r (row-list mode): rows of alpha row ra are rlist[(ra - a_lo) * Nb + i],
+  // i < rcnt[ra - a_lo]; work unit u covers list chunk utab[u].y of alpha row
+  // a_lo + utab[u].x; *d_units list units (device count, no host sync)
+  const uint32_t* rlist;
+  const uint32_t* rcnt;
+  const uint2* utab;
+  const uint32_t* d_units;
+};
+
+// K1r: row lists of the rows marked in smap (or, smap == nullptr, of the
+// nonzero rows of amp) for alpha rows [a_lo, a_hi), and the unit table.
+struct RowList {
+  uint32_t* rlist = nullptr;
+  uint32_t* rcnt = nullptr;
+  uint2* utab = nullptr;
+  uint32_t* d_units = nullptr;
+  int64_t max_units = 0;
+  int build(const hsv_sector_s* s, const uint8_t* smap, const double2* amp, int64_t a_lo,
+            int64_t a_hi, int rows_per_unit);
+  void release();
 };
 
 // Final value of output row `row`: local store plus the same store into every
@@ -134,6 +157,10 @@ void launch_combine_splits(const double2* part, int S, int64_t rows, double2* ou
 int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* epart,
                  int64_t a_lo, int64_t a_hi, double prune, int energy_only, int64_t* n_warps,
                  const uint32_t* arow = nullptr, bool* dense_hint = nullptr);
+// K1r: out = H psi on the rows marked in smap (exactly the K1 values there),
+// 0 on every other row of [a_lo, a_hi); no energy partials.
+int launch_apply_rows(const hsv_op_s* op, const double2* psi, double2* out, int64_t a_lo,
+                      int64_t a_hi, const uint32_t* arow, const uint8_t* smap);
 
 // Compressed QEB masks of one excitation operator.
 struct OpMasks {
@@ -149,6 +176,13 @@ struct PairLists {
   int64_t ca = 0, cb = 0;
 };
 int build_pair_lists_async(const hsv_sector_s* s, const OpMasks& m, PairLists& pl);
+
+// K3b/K5b batched sweeps (hsv_sweep.cu): mode 0 forward, 1 adjoint.
+int launch_bsweep(const hsv_sector_s* sec, int mode, const std::vector<OpMasks>& ops,
+                  const double* cs, const double* sn, double2* psi, double2* lam, uint8_t* smap,
+                  double* norm2, double* d_grads, int* err, double* err_val);
+int smap_arow_async(const hsv_sector_s* sec, const uint8_t* smap, uint32_t* flags);
+void release_sweep_plans();
 
 int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
                   const hsv_pool_s* pool, int64_t a_lo, int64_t a_hi, double* d_grads,

@@ -77,11 +77,14 @@ int hsv_set_tuning(const char* key, int64_t value) {
   } else if (k == "rb0_smem") {
     HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "rb0_smem must be -1, 0 or 1");
     g_tuning.rb0_smem = (int)value;
+  } else if (k == "restrict_rows") {
+    HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "restrict_rows must be -1, 0 or 1");
+    g_tuning.restrict_rows = (int)value;
   } else if (k == "push") {
     HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "push must be -1, 0 or 1");
     g_tuning.push = (int)value;
   } else if (k == "sweep") {
-    HSV_REQUIRE(value == 0 || value == 1, HSV_ERR_INVALID, "sweep must be 0 or 1");
+    HSV_REQUIRE(value >= 0 && value <= 2, HSV_ERR_INVALID, "sweep must be 0, 1 or 2");
     g_tuning.sweep = (int)value;
   } else if (k == "staged") {
     HSV_REQUIRE(value == 0 || value == 1, HSV_ERR_INVALID, "staged must be 0 or 1");

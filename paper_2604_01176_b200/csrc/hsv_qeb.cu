@@ -326,6 +326,7 @@ struct SweepArgs {
   double* grads;         // kAdjoint: gradient of op i at grads[i]
   int* err;
   double* err_val;
+  uint8_t* smap;         // kRotate: structural support map (see hsv_state_s), or nullptr
 };
 
 // Grid-wide barrier of the cooperative launch (measured 1.2 us at 2 blocks/SM,
@@ -420,6 +421,9 @@ __global__ void __launch_bounds__(256) k_sweep(const SweepArgs a) {
           givens(vb, vp, o.c, o.s, nb, np);
           a.psi[ib] = nb;
           a.psi[ip] = np;
+          if (a.smap) {   // structural support: either side marked -> both marked
+            if (a.smap[ib] | a.smap[ip]) { a.smap[ib] = 1; a.smap[ip] = 1; }
+          }
           v[0] = vb.x * vb.x + vb.y * vb.y + vp.x * vp.x + vp.y * vp.y;
           v[1] = nb.x * nb.x + nb.y * nb.y + np.x * np.x + np.y * np.y;
         } else {
@@ -505,7 +509,7 @@ __global__ void __launch_bounds__(256) k_sweep(const SweepArgs a) {
 template <int MODE>
 static int launch_sweep(const hsv_sector_s* sec, const std::vector<SweepOp>& ops_in, double2* psi,
                         uint32_t* fpsi, double2* lam, uint32_t* flam, double* norm2,
-                        double* d_grads, PairScratch& sc) {
+                        double* d_grads, PairScratch& sc, uint8_t* smap = nullptr) {
   if (ops_in.empty()) return HSV_OK;
   constexpr int NV = MODE == kAdjoint ? 3 : 2;
   static thread_local std::vector<SweepOp> ops;
@@ -538,6 +542,7 @@ static int launch_sweep(const hsv_sector_s* sec, const std::vector<SweepOp>& ops
   a.psi = psi; a.lam = lam; a.fpsi = fpsi; a.flam = flam;
   a.part = part; a.part_stride = max_items * NV; a.chunk = (int)chunk; a.red = red;
   a.norm2 = norm2; a.grads = d_grads; a.err = sc.err; a.err_val = sc.err_val;
+  a.smap = smap;
   static int occ[3] = {0, 0, 0};
   if (!occ[MODE]) {
     HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ[MODE], k_sweep<MODE>, 256, 0));
@@ -614,6 +619,7 @@ int hsv_apply_qeb(hsv_state in, hsv_state out, uint64_t occ, uint64_t virt, doub
   dfree(pl.la); dfree(pl.lb);
   sc.release();
   out->norm2_valid = true;
+  out->smap_valid = false;
   out->dense_hint = false;
   return rc;
 }
@@ -632,6 +638,7 @@ int hsv_apply_generator(hsv_state in, hsv_state out, uint64_t occ, uint64_t virt
   dfree(pl.la); dfree(pl.lb);
   out->norm2_valid = false;
   out->arow_valid = false;
+  out->smap_valid = false;
   out->dense_hint = false;
   return stream_sync();
 }
@@ -650,7 +657,7 @@ static int check_eg_args(hsv_op op, const uint64_t* occ, const uint64_t* virt, c
 // in `sc` for the caller's sc.check().
 static int forward_psi(const hsv_sector_s* sec, uint64_t hf_key, const uint64_t* occ,
                        const uint64_t* virt, const double* cs, const double* sn, int64_t k,
-                       hsv_state psi, PairScratch& sc, PairLists& pl) {
+                       hsv_state psi, PairScratch& sc, PairLists& pl, bool want_smap = false) {
   const uint32_t sa = sec->compress_a(hf_key), sb = sec->compress_b(hf_key);
   HSV_REQUIRE((sec->n_qubits >= 64 || (hf_key >> sec->n_qubits) == 0) && sec->Ra[sa] != ~0u &&
                   sec->Rb[sb] != ~0u,
@@ -671,13 +678,40 @@ static int forward_psi(const hsv_sector_s* sec, uint64_t hf_key, const uint64_t*
                                stream()));
   HSV_TRY_CUDA(cudaMemcpyAsync(psi->d_arow + sec->Ra[sa], &one_flag, sizeof(uint32_t),
                                cudaMemcpyHostToDevice, stream()));
+  if (tuning().sweep == 2) {   // batched sweep (hsv_sweep.cu); keeps the support map
+    if (!psi->d_smap) HSV_TRY(dalloc(&psi->d_smap, sec->dim));
+    static thread_local uint8_t one_b;
+    one_b = 1;
+    HSV_TRY_CUDA(cudaMemsetAsync(psi->d_smap, 0, sec->dim, stream()));
+    HSV_TRY_CUDA(cudaMemcpyAsync(psi->d_smap + hidx, &one_b, 1, cudaMemcpyHostToDevice, stream()));
+    static thread_local std::vector<OpMasks> ops;
+    ops.clear();
+    for (int64_t i = 0; i < k; ++i) ops.push_back(compress_op(sec, occ[i], virt[i]));
+    HSV_TRY(launch_bsweep(sec, 0, ops, cs, sn, psi->d_amp, nullptr, psi->d_smap, psi->d_norm2,
+                          nullptr, sc.err, sc.err_val));
+    HSV_TRY(smap_arow_async(sec, psi->d_smap, psi->d_arow));
+    psi->norm2_valid = psi->arow_valid = psi->smap_valid = true;
+    psi->dense_hint = false;
+    (void)want_smap;
+    return HSV_OK;
+  }
+  // structural support map: HF row only, grown by every rotation of the sweep
+  uint8_t* smap = nullptr;
+  if (want_smap && tuning().sweep) {
+    if (!psi->d_smap) HSV_TRY(dalloc(&psi->d_smap, sec->dim));
+    smap = psi->d_smap;
+    static thread_local uint8_t one_b;
+    one_b = 1;
+    HSV_TRY_CUDA(cudaMemsetAsync(smap, 0, sec->dim, stream()));
+    HSV_TRY_CUDA(cudaMemcpyAsync(smap + hidx, &one_b, 1, cudaMemcpyHostToDevice, stream()));
+  }
   if (tuning().sweep) {
     static thread_local std::vector<SweepOp> ops;
     ops.clear();
     for (int64_t i = 0; i < k; ++i)
       if (!(cs[i] == 1.0 && sn[i] == 0.0)) ops.push_back(sweep_op(sec, occ[i], virt[i], cs[i], sn[i]));
     HSV_TRY(launch_sweep<kRotate>(sec, ops, psi->d_amp, psi->d_arow, nullptr, nullptr,
-                                  psi->d_norm2, nullptr, sc));
+                                  psi->d_norm2, nullptr, sc, smap));
   } else {
     for (int64_t i = 0; i < k; ++i) {
       if (cs[i] == 1.0 && sn[i] == 0.0) continue;
@@ -690,6 +724,7 @@ static int forward_psi(const hsv_sector_s* sec, uint64_t hf_key, const uint64_t*
     }
   }
   psi->norm2_valid = psi->arow_valid = true;
+  psi->smap_valid = smap != nullptr;
   psi->dense_hint = false;
   return HSV_OK;
 }
@@ -724,10 +759,16 @@ int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const 
   PairScratch sc;
   HSV_TRY(sc.init(sec, 2));
   PairLists pl;
-  HSV_TRY(forward_psi(sec, hf_key, occ, virt, cs, sn, k, psi, sc, pl));
+  // K1r: the adjoint sweep reads w = H psi only on the structural support of
+  // psi (rotation pairs never straddle it), so w is computed there
+  const bool rows_only = tuning().restrict_rows != 0 && tuning().sweep;
+  HSV_TRY(forward_psi(sec, hf_key, occ, virt, cs, sn, k, psi, sc, pl, rows_only));
   int64_t used = 0;
-  HSV_TRY(launch_apply(op, psi->d_amp, w->d_amp, nullptr, a_lo, a_hi, 0.0, 0, &used, psi->d_arow,
-                       &psi->dense_hint));
+  if (rows_only && psi->smap_valid)
+    HSV_TRY(launch_apply_rows(op, psi->d_amp, w->d_amp, a_lo, a_hi, psi->d_arow, psi->d_smap));
+  else
+    HSV_TRY(launch_apply(op, psi->d_amp, w->d_amp, nullptr, a_lo, a_hi, 0.0, 0, &used,
+                         psi->d_arow, &psi->dense_hint));
   w->norm2_valid = w->arow_valid = false;
   w->dense_hint = false;
   // drift errors are read by hsv_eg_backward (no host sync here); an unread
@@ -777,20 +818,29 @@ int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
   double* d_grad = nullptr;
   HSV_TRY(dalloc(&d_grad, k + 2));
   HSV_TRY(state_dot_async(psi, w, d_grad + k));
-  HSV_TRY(state_arow_async(psi));
-  HSV_TRY(state_arow_async(w));
+  if (tuning().sweep != 2) {   // flags of the one-barrier-per-rotation sweeps
+    HSV_TRY(state_arow_async(psi));
+    HSV_TRY(state_arow_async(w));
+  }
   if (k > 0) HSV_TRY(state_norm2_async(w));   // <lam|lam> for the drift checks
   PairScratch sc;
   HSV_TRY(sc.init(sec, 3));
   PairLists pl;
-  if (tuning().sweep) {
+  if (tuning().sweep == 2) {
+    static thread_local std::vector<OpMasks> bops;
+    bops.clear();
+    for (int64_t i = 0; i < k; ++i) bops.push_back(compress_op(sec, occ[i], virt[i]));
+    HSV_TRY(launch_bsweep(sec, 1, bops, cs, sn, psi->d_amp, w->d_amp,
+                          psi->smap_valid ? psi->d_smap : nullptr, w->d_norm2, d_grad, sc.err,
+                          sc.err_val));
+  } else if (tuning().sweep) {
     static thread_local std::vector<SweepOp> ops;
     ops.clear();
     for (int64_t i = 0; i < k; ++i) ops.push_back(sweep_op(sec, occ[i], virt[i], cs[i], sn[i]));
     HSV_TRY(launch_sweep<kAdjoint>(sec, ops, psi->d_amp, psi->d_arow, w->d_amp, w->d_arow,
                                    w->d_norm2, d_grad, sc));
   }
-  for (int64_t i = tuning().sweep ? -1 : k - 1; i >= 0; --i) {
+  for (int64_t i = tuning().sweep ? -1 : k - 1; i >= 0; --i) {   // per-op launches
     HSV_TRY(build_pair_lists_async(sec, compress_op(sec, occ[i], virt[i]), pl));
     if (pl.ca == 0 || pl.cb == 0) {
       HSV_TRY_CUDA(cudaMemsetAsync(d_grad + i, 0, sizeof(double), stream()));
@@ -812,6 +862,9 @@ int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
   sc.release();
   dfree(d_grad);
   psi->norm2_valid = false;
+  psi->arow_valid = psi->arow_valid && tuning().sweep != 2;   // batched sweep keeps no flags
+  w->arow_valid = w->arow_valid && tuning().sweep != 2;
+  psi->smap_valid = w->smap_valid = false;
   psi->dense_hint = w->dense_hint = false;
   HSV_TRY(stream_sync());
   for (int64_t i = 0; i < k; ++i) grads[i] = h[i];

@@ -31,6 +31,7 @@ int state_fill_zero_async(hsv_state st) {
   HSV_TRY_CUDA(cudaMemsetAsync(st->d_arow, 0, st->sec->Na * sizeof(uint32_t), stream()));
   st->norm2_valid = true;
   st->arow_valid = true;
+  st->smap_valid = false;
   st->dense_hint = false;
   return HSV_OK;
 }
@@ -269,6 +270,7 @@ int hsv_state_destroy(hsv_state st) {
   dfree(st->d_arow);
   dfree(st->d_pend_err);
   dfree(st->d_pend_val);
+  dfree(st->d_smap);
   delete st;
   return HSV_OK;
 }
@@ -285,6 +287,7 @@ int hsv_state_copy(hsv_state dst, hsv_state src) {
                                cudaMemcpyDeviceToDevice, stream()));
   dst->norm2_valid = src->norm2_valid;
   dst->arow_valid = src->arow_valid;
+  dst->smap_valid = false;
   dst->dense_hint = src->dense_hint;
   return stream_sync();
 }
@@ -314,6 +317,7 @@ int hsv_state_set_basis(hsv_state st, uint64_t key, double re, double im) {
   HSV_TRY_CUDA(cudaMemcpyAsync(st->d_norm2, &n2, sizeof(double), cudaMemcpyHostToDevice,
                                stream()));
   st->arow_valid = false;
+  st->smap_valid = false;
   st->dense_hint = false;
   return stream_sync();
 }
@@ -348,6 +352,7 @@ int hsv_state_set_sparse(hsv_state st, const int64_t* pos, const double* re, con
     dfree(d_bad);
   }
   st->arow_valid = false;
+  st->smap_valid = false;
   // more than dim/8 entries is always past the push path's budget: skip its probe
   st->dense_hint = n > st->sec->dim / 8;
   HSV_TRY(state_norm2_async(st));
@@ -374,6 +379,7 @@ int hsv_state_set_dense(hsv_state st, const double* re, const double* im) {
   dfree(d_re);
   dfree(d_im);
   st->arow_valid = false;
+  st->smap_valid = false;
   st->dense_hint = true;
   HSV_TRY(state_norm2_async(st));
   HSV_TRY(stream_sync());   // host buffers may be reused on return
@@ -409,6 +415,7 @@ int hsv_state_set_keys(hsv_state st, const uint64_t* keys, const double* re, con
     dfree(d_i);
   }
   st->arow_valid = false;
+  st->smap_valid = false;
   st->dense_hint = n > st->sec->dim / 8;
   HSV_TRY(state_norm2_async(st));
   return stream_sync();
@@ -543,6 +550,7 @@ int hsv_state_axpy(double ar, double ai, hsv_state x, hsv_state y) {
   HSV_CHECK_LAUNCH();
   y->norm2_valid = false;
   y->arow_valid = false;
+  y->smap_valid = false;
   y->dense_hint = false;
   return stream_sync();
 }
@@ -555,6 +563,7 @@ int hsv_state_scale(hsv_state st, double ar, double ai) {
   HSV_CHECK_LAUNCH();
   st->norm2_valid = false;
   st->arow_valid = false;
+  st->smap_valid = false;
   st->dense_hint = false;
   return stream_sync();
 }
@@ -565,6 +574,7 @@ int hsv_state_device_ptr(hsv_state st, void** ptr, int64_t* n) {
   if (n) *n = st->sec->dim;
   st->norm2_valid = false;   // caller may write through the pointer
   st->arow_valid = false;
+  st->smap_valid = false;
   st->dense_hint = false;
   return HSV_OK;
 }

@@ -16,8 +16,12 @@ def hsv():
 @pytest.fixture()
 def N():
     from paper_2604_01176_b200 import _native as N
+    # the per-op path computes w = H psi on every row: compare against the
+    # sweep with the full K1 too (K1r is checked in test_gpu_restrict.py)
+    N.call("hsv_set_tuning", b"restrict_rows", 0)
     yield N
-    N.call("hsv_set_tuning", b"sweep", 1)
+    N.call("hsv_set_tuning", b"sweep", 2)
+    N.call("hsv_set_tuning", b"restrict_rows", -1)
 
 
 def eg(N, eng, ops, th, sweep):
@@ -25,9 +29,14 @@ def eg(N, eng, ops, th, sweep):
     return eng.energy_and_gradient(ops, th)
 
 
+@pytest.mark.parametrize("sweep", [1, 2])
 @pytest.mark.parametrize("name,k", [("h2", 3), ("h4", 12), ("h6", 30), ("h8", 40),
                                     ("h10", 25), ("h12", 20)])
-def test_sweep_bitwise_equals_per_op(hsv, N, name, k):
+def test_sweep_bitwise_equals_per_op(hsv, N, name, k, sweep):
+    """sweep 1 (one barrier per rotation) replays the per-op reductions: bitwise.
+    sweep 2 (orbit batches, hsv_sweep.cu) sums the gradient partials per orbit
+    instead of per pair block: the state and the energy are bitwise, the
+    gradients agree to rounding."""
     sysm = hsv.MolecularSystem.bundled(name)
     eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
     pool = hsv.build_qeb_pool(sysm.n_qubits, sysm.integrals.nelec)
@@ -37,10 +46,13 @@ def test_sweep_bitwise_equals_per_op(hsv, N, name, k):
         th = rng.uniform(-0.4, 0.4, size=k)
         th[::5] = 0.0                               # identity rotations are skipped forward
         ops = [pool.ops[i] for i in idx]
-        e1, g1 = eg(N, eng, ops, th, 1)
+        e1, g1 = eg(N, eng, ops, th, sweep)
         e0, g0 = eg(N, eng, ops, th, 0)
         assert e1 == e0
-        assert np.array_equal(g1, g0)
+        if sweep == 1:
+            assert np.array_equal(g1, g0)
+        else:
+            assert np.max(np.abs(g1 - g0)) <= 1e-13 * max(1.0, np.max(np.abs(g0)))
 
 
 def test_sweep_forward_state_and_two_phase(hsv, N):
@@ -56,7 +68,7 @@ def test_sweep_forward_state_and_two_phase(hsv, N):
     cs, sn = np.cos(th), np.sin(th)
     na = sysm.basis._sector.n_alpha_strings
     out = []
-    for sweep in (1, 0):
+    for sweep in (2, 1, 0):
         N.call("hsv_set_tuning", b"sweep", sweep)
         psi, w = DeviceState(sysm.basis), DeviceState(sysm.basis)
         N.call("hsv_eg_forward_async", eng.matrix.handle, int(sysm.hf.bits), N.ptr_u64(occ),
@@ -64,9 +76,10 @@ def test_sweep_forward_state_and_two_phase(hsv, N):
                w.handle)
         N.call("hsv_synchronize")
         out.append((psi.to_sparse(), w.to_sparse()))
-    (p1, w1), (p0, w0) = out
-    assert np.array_equal(p1.indices, p0.indices) and np.array_equal(p1.values, p0.values)
-    assert np.array_equal(w1.indices, w0.indices) and np.array_equal(w1.values, w0.values)
+    (p2, w2), (p1, w1), (p0, w0) = out
+    for p, w in ((p2, w2), (p1, w1)):
+        assert np.array_equal(p.indices, p0.indices) and np.array_equal(p.values, p0.values)
+        assert np.array_equal(w.indices, w0.indices) and np.array_equal(w.values, w0.values)
     ref = hsv.apply_ansatz(sysm.basis, sysm.hf, ops, th).vec
     assert np.array_equal(ref.indices, p1.indices) and np.array_equal(ref.values, p1.values)
 
@@ -82,7 +95,7 @@ def test_ansatz_state_equals_rotation_by_rotation(hsv, N, name, k):
     th = rng.uniform(-0.5, 0.5, size=k)
     th[::4] = 0.0
     ops = [pool.ops[i] for i in idx]
-    for sweep in (1, 0):
+    for sweep in (2, 1, 0):
         N.call("hsv_set_tuning", b"sweep", sweep)
         fused = hsv.apply_ansatz(sysm.basis, sysm.hf, ops, th).vec
         st = hsv.SvState.from_configuration(sysm.basis, sysm.hf)
@@ -95,7 +108,7 @@ def test_ansatz_state_equals_rotation_by_rotation(hsv, N, name, k):
     assert empty.nnz == 1
 
 
-@pytest.mark.parametrize("sweep", [1, 0])
+@pytest.mark.parametrize("sweep", [2, 1, 0])
 def test_forward_drift_reported_by_backward(hsv, N, sweep):
     """A non-unitary rotation (c^2 + s^2 != 1) in the forward sweep: the forward call
     returns without waiting for the device and the consuming backward call raises
