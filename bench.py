@@ -329,6 +329,8 @@ def run_hsv(args):
         clk.mark()
     N.call("hsv_prof_collect")
     N.call("hsv_prof_enable", 0)
+    if peer is not None:
+        peer.check()          # every exchange of the timed region completed (bounded waits)
     launches = int(N.lib().hsv_launch_count(1))
     ms = [a.elapsed_time(b) for a, b in ev]
     t_ms = float(sum(ms))

@@ -234,6 +234,11 @@ HSV_API int hsv_sum_rows_async(const double* d_in, int64_t n_rows, int64_t n_col
 HSV_API int hsv_peer_create(int world, int rank, int64_t bytes, hsv_peer* out, void* handle_out);
 HSV_API int hsv_peer_open(hsv_peer p, const void* handles);
 HSV_API int hsv_peer_destroy(hsv_peer p);
+/* Synchronize and report the exchanges since the last check: HSV_ERR_CUDA if a
+ * device-side wait timed out (HSV_PEER_TIMEOUT_S, default 60 s) or a peer rank
+ * aborted its side of an exchange because its own call failed.  The waits are
+ * bounded, so a dead or failed peer surfaces here instead of hanging the stream. */
+HSV_API int hsv_peer_check(hsv_peer p);
 HSV_API int hsv_peer_data(hsv_peer p, void** d_data, int64_t* bytes);
 HSV_API int hsv_peer_allgather_async(hsv_peer p, const void* d_src, int64_t n);
 /* All-gather + rank-order sum in ONE launch: the n float64 values at d_src go
@@ -261,6 +266,17 @@ HSV_API int hsv_eg_forward_peer_async(hsv_op op, uint64_t hf_key, const uint64_t
  * "bperm" (K1 partner beta ranks from per-xb 16-bit rows: -1/1 on, 0 Rb0 gather),
  * "rb0_smem" (1: Rb0 staged in shared memory, opt-in) ---- */
 HSV_API int hsv_set_tuning(const char* key, int64_t value);
+
+/* ---- Krylov basis blocks (FCI reference: thick-restart Lanczos, fci.py;
+ * replaces scipy eigsh in oracle.py:99-142) ---- */
+/* c_j = <q_j|w> (complex, c_out[2j], c_out[2j+1]; c_out may be NULL) for the m
+ * basis states in one launch; subtract != 0: then w -= sum_j c_j q_j (one pass).
+ * Fixed-order reductions (repeatable bit for bit).  Synchronizes. */
+HSV_API int hsv_krylov_project(const hsv_state* q, int64_t m, hsv_state w, int subtract,
+                               double* c_out);
+/* out = sum_j coeff[j] q_j (real coefficients; a Ritz vector).  Synchronizes. */
+HSV_API int hsv_krylov_combine(const hsv_state* q, int64_t m, const double* coeff,
+                               hsv_state out);
 
 /* ---- live kernel timing (CUDA events on the launch stream) ---- */
 HSV_API int hsv_prof_enable(int on);

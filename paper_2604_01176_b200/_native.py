@@ -94,12 +94,15 @@ _SIGNATURES = {
     "hsv_peer_create": (C.c_int, [C.c_int, C.c_int, i64, C.POINTER(vp), vp]),
     "hsv_peer_open": (C.c_int, [vp, vp]),
     "hsv_peer_destroy": (C.c_int, [vp]),
+    "hsv_peer_check": (C.c_int, [vp]),
     "hsv_peer_data": (C.c_int, [vp, C.POINTER(vp), C.POINTER(i64)]),
     "hsv_peer_allgather_async": (C.c_int, [vp, vp, i64]),
     "hsv_peer_allreduce_async": (C.c_int, [vp, vp, i64, vp]),
     "hsv_eg_forward_peer_async": (C.c_int, [vp, C.c_uint64, P_u64, P_u64, P_dbl, P_dbl, i64,
                                             i64, i64, vp, vp, vp]),
     "hsv_set_tuning": (C.c_int, [C.c_char_p, i64]),
+    "hsv_krylov_project": (C.c_int, [C.POINTER(vp), i64, vp, C.c_int, P_dbl]),
+    "hsv_krylov_combine": (C.c_int, [C.POINTER(vp), i64, P_dbl, vp]),
     "hsv_prof_enable": (C.c_int, [C.c_int]),
     "hsv_prof_collect": (C.c_int, []),
     "hsv_prof_get": (C.c_int, [C.c_char_p, P_dbl, P_i64]),

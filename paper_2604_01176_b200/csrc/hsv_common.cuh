@@ -219,6 +219,7 @@ struct hsv_peer_s {
   unsigned int* d_counter = nullptr;    // last-CTA detection in the put kernel
   uint64_t epoch = 0;
   bool opened = false;
+  int* d_err = nullptr;                 // 1: a wait timed out, 2: a peer aborted (hsv_peer_check)
 };
 
 struct hsv_state_s {
@@ -240,10 +241,11 @@ struct hsv_state_s {
   int* d_pend_err = nullptr;
   double* d_pend_val = nullptr;
   // Structural support of an ansatz state (1 byte per row, allocated on first
-  // use): row b is marked when some rotation of the forward sweep that built
-  // psi can have moved amplitude into it (hsv_eg_forward_async).  Superset of
-  // the nonzeros, independent of exact cancellations; the support-restricted
-  // K1 computes w = H psi on these rows only (hsv_apply.cu, K1r).
+  // use): the closure of the HF row under every rotation of the forward sweep
+  // that built psi, theta = 0 included (hsv_eg_forward_async).  A superset of
+  // the nonzeros, independent of exact cancellations, closed under each
+  // rotation; the adjoint sweep reads w = H psi only there, so the
+  // support-restricted K1 computes those rows only (hsv_apply.cu, K1r).
   uint8_t* d_smap = nullptr;
   bool smap_valid = false;
 };

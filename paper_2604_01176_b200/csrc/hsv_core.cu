@@ -6,6 +6,7 @@
 #include <mutex>
 
 #include "hsv_common.cuh"
+#include "hsv_kernels.cuh"
 
 namespace hsv {
 
@@ -361,6 +362,7 @@ int hsv_sector_create(int n_qubits, int n_alpha, int n_beta, int ordering, hsv_s
 
 int hsv_sector_destroy(hsv_sector s) {
   if (!s) return HSV_OK;
+  release_sweep_plans(s);   // cached sweep plans of this sector (hsv_sweep.cu)
   dfree(s->d_Sa); dfree(s->d_Sb); dfree(s->d_Ra); dfree(s->d_Rb); dfree(s->d_Rb0);
   dfree(s->d_perm); dfree(s->d_iperm); dfree(s->d_binom); dfree(s->d_spin);
   dfree(s->d_aslot); dfree(s->d_bslot);

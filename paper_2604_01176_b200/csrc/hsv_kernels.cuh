@@ -178,11 +178,13 @@ struct PairLists {
 int build_pair_lists_async(const hsv_sector_s* s, const OpMasks& m, PairLists& pl);
 
 // K3b/K5b batched sweeps (hsv_sweep.cu): mode 0 forward, 1 adjoint.
-int launch_bsweep(const hsv_sector_s* sec, int mode, const std::vector<OpMasks>& ops,
-                  const double* cs, const double* sn, double2* psi, double2* lam, uint8_t* smap,
-                  double* norm2, double* d_grads, int* err, double* err_val);
+int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
+                  const std::vector<OpMasks>& ops, const double* cs, const double* sn,
+                  double2* psi, double2* lam, uint8_t* smap_out, double* norm2, double* d_grads,
+                  int* err, double* err_val, bool* used);
 int smap_arow_async(const hsv_sector_s* sec, const uint8_t* smap, uint32_t* flags);
-void release_sweep_plans();
+// drop the cached sweep plan (of sector s only, when s != nullptr)
+void release_sweep_plans(const hsv_sector_s* s = nullptr);
 
 int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
                   const hsv_pool_s* pool, int64_t a_lo, int64_t a_hi, double* d_grads,

@@ -15,7 +15,9 @@
 //    every rank's buffer by the K1 epilogue itself (put_row), so the all-gather
 //    of w rides on NVLink while K1 is still computing other rows -- the
 //    compute + collective fusion of the multi-GPU adjoint sweep.
+#include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "hsv_common.cuh"
 #include "hsv_kernels.cuh"
@@ -32,6 +34,42 @@ __device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+constexpr uint64_t kAbortBit = 1ull << 63;   // flag value of a rank that gave up this exchange
+
+// Publish `epoch` (or, abort != 0, epoch | kAbortBit) to every rank's flag slot
+// of this rank, then wait -- bounded by timeout_ns -- until every rank has
+// published this epoch.  A timeout or a peer's abort sets *err (1 timeout,
+// 2 peer abort) and returns: the host reads it (hsv_peer_check) instead of the
+// stream hanging forever on a dead or failed peer.
+__device__ void publish_and_wait(char* const* bases, int world, int rank, int64_t flags_off,
+                                 uint64_t epoch, int abort, uint64_t timeout_ns, int* err,
+                                 unsigned sleep_ns) {
+  __threadfence_system();
+  const uint64_t mark = abort ? (epoch | kAbortBit) : epoch;
+  for (int r = 0; r < world; ++r)
+    st_release_sys(reinterpret_cast<uint64_t*>(bases[r] + flags_off) + rank, mark);
+  const uint64_t* mine = reinterpret_cast<const uint64_t*>(bases[rank] + flags_off);
+  const uint64_t t0 = globaltimer_ns();
+  for (int r = 0; r < world; ++r) {
+    while (true) {
+      const uint64_t v = ld_acquire_sys(mine + r);
+      if (v & kAbortBit) {
+        if ((v & ~kAbortBit) >= epoch) { atomicMax(err, 2); break; }
+      } else if (v >= epoch) {
+        break;
+      }
+      if (globaltimer_ns() - t0 > timeout_ns) { atomicMax(err, 1); return; }
+      __nanosleep(sleep_ns);
+    }
+  }
+  __threadfence_system();
+}
 
 // copy n bytes (multiple of 16) from src to bases[r] + off for every rank r
 __global__ void k_peer_put(const uint4* __restrict__ src, int64_t n16, char* const* bases,
@@ -45,15 +83,9 @@ __global__ void k_peer_put(const uint4* __restrict__ src, int64_t n16, char* con
 
 // publish this rank's arrival for `epoch` to every rank, then wait for all
 __global__ void k_peer_barrier(char* const* bases, int world, int rank, int64_t flags_off,
-                               uint64_t epoch) {
+                               uint64_t epoch, int abort, uint64_t timeout_ns, int* err) {
   if (threadIdx.x != 0) return;
-  __threadfence_system();
-  for (int r = 0; r < world; ++r)
-    st_release_sys(reinterpret_cast<uint64_t*>(bases[r] + flags_off) + rank, epoch);
-  const uint64_t* mine = reinterpret_cast<const uint64_t*>(bases[rank] + flags_off);
-  for (int r = 0; r < world; ++r)
-    while (ld_acquire_sys(mine + r) < epoch) __nanosleep(64);
-  __threadfence_system();
+  publish_and_wait(bases, world, rank, flags_off, epoch, abort, timeout_ns, err, 64);
 }
 
 // all-gather + barrier + rank-order sum in one CTA: puts, then thread 0 publishes
@@ -63,7 +95,8 @@ __global__ void __launch_bounds__(1024) k_peer_allreduce(const double* __restric
                                                          int64_t n, char* const* bases,
                                                          int world, int rank, int64_t half,
                                                          int64_t flags_off, uint64_t epoch,
-                                                         double* __restrict__ out) {
+                                                         double* __restrict__ out,
+                                                         uint64_t timeout_ns, int* err) {
   const int64_t n16 = n / 2;
   for (int64_t i = threadIdx.x; i < n16; i += blockDim.x) {
     const uint4 v = reinterpret_cast<const uint4*>(src)[i];
@@ -71,15 +104,8 @@ __global__ void __launch_bounds__(1024) k_peer_allreduce(const double* __restric
       reinterpret_cast<uint4*>(bases[r] + half + rank * n * (int64_t)sizeof(double))[i] = v;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();
-    for (int r = 0; r < world; ++r)
-      st_release_sys(reinterpret_cast<uint64_t*>(bases[r] + flags_off) + rank, epoch);
-    const uint64_t* mine = reinterpret_cast<const uint64_t*>(bases[rank] + flags_off);
-    for (int r = 0; r < world; ++r)
-      while (ld_acquire_sys(mine + r) < epoch) __nanosleep(32);
-    __threadfence_system();
-  }
+  if (threadIdx.x == 0)
+    publish_and_wait(bases, world, rank, flags_off, epoch, 0, timeout_ns, err, 32);
   __syncthreads();
   const double* data = reinterpret_cast<const double*>(bases[rank] + half);
   for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
@@ -89,8 +115,15 @@ __global__ void __launch_bounds__(1024) k_peer_allreduce(const double* __restric
   }
 }
 
-int peer_barrier(hsv_peer_s* p) {
-  k_peer_barrier<<<1, 32, 0, stream()>>>(p->d_bases, p->world, p->rank, p->flags_off, p->epoch);
+uint64_t peer_timeout_ns() {
+  const char* e = getenv("HSV_PEER_TIMEOUT_S");
+  const double s = e ? atof(e) : 60.0;
+  return (uint64_t)((s > 0 ? s : 60.0) * 1e9);
+}
+
+int peer_barrier(hsv_peer_s* p, int abort = 0) {
+  k_peer_barrier<<<1, 32, 0, stream()>>>(p->d_bases, p->world, p->rank, p->flags_off, p->epoch,
+                                         abort, peer_timeout_ns(), p->d_err);
   count_launch();
   HSV_CHECK_LAUNCH();
   return HSV_OK;
@@ -122,6 +155,14 @@ int hsv_peer_create(int world, int rank, int64_t bytes, hsv_peer* out, void* han
     return HSV_ERR_OOM;
   }
   cudaMemset(p->base + p->flags_off, 0, (size_t)world * sizeof(uint64_t));
+  if (cudaMalloc(&p->d_err, sizeof(int)) != cudaSuccess) {
+    cudaGetLastError();
+    cudaFree(p->base);
+    delete p;
+    set_error(HSV_ERR_OOM, "peer error flag allocation failed");
+    return HSV_ERR_OOM;
+  }
+  cudaMemset(p->d_err, 0, sizeof(int));
   cudaIpcMemHandle_t h;
   e = cudaIpcGetMemHandle(&h, p->base);
   if (e != cudaSuccess) {
@@ -165,7 +206,22 @@ int hsv_peer_destroy(hsv_peer p) {
     if (r != p->rank && p->bases[r]) cudaIpcCloseMemHandle(p->bases[r]);
   if (p->d_bases) cudaFree(p->d_bases);
   if (p->base) cudaFree(p->base);
+  if (p->d_err) cudaFree(p->d_err);
   delete p;
+  return HSV_OK;
+}
+
+int hsv_peer_check(hsv_peer p) {
+  HSV_REQUIRE(p, HSV_ERR_INVALID, "null peer");
+  int h = 0;
+  HSV_TRY(stream_sync());
+  HSV_TRY_CUDA(cudaMemcpy(&h, p->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h) HSV_TRY_CUDA(cudaMemset(p->d_err, 0, sizeof(int)));
+  HSV_REQUIRE(h != 1, HSV_ERR_CUDA,
+              "NVLink peer exchange timed out (a peer did not arrive within "
+              "HSV_PEER_TIMEOUT_S); its results are invalid");
+  HSV_REQUIRE(h != 2, HSV_ERR_CUDA,
+              "a peer rank aborted the NVLink exchange (its call failed); results are invalid");
   return HSV_OK;
 }
 
@@ -205,7 +261,7 @@ int hsv_peer_allreduce_async(hsv_peer p, const double* d_src, int64_t n, double*
     ProfScope prof("peer");
     k_peer_allreduce<<<1, 1024, 0, stream()>>>(d_src, n, p->d_bases, p->world, p->rank,
                                                (p->epoch & 1) * p->bytes, p->flags_off, p->epoch,
-                                               d_out);
+                                               d_out, peer_timeout_ns(), p->d_err);
     count_launch();
     HSV_CHECK_LAUNCH();
   }
@@ -234,7 +290,16 @@ int hsv_eg_forward_peer_async(hsv_op op, uint64_t hf_key, const uint64_t* occ,
   ctx().peer_rows = nullptr;
   ctx().n_peer_rows = 0;
   dfree(d_sinks);
-  if (rc) return rc;
+  if (rc) {
+    // still take part in this epoch's barrier, flagged as an abort, so the
+    // other ranks stop waiting and report the failure (hsv_peer_check)
+    const int saved = rc;
+    std::string msg(256, '\0');
+    hsv_last_error(&msg[0], msg.size());
+    peer_barrier(p, 1);
+    set_error(saved, "%s", msg.c_str());
+    return saved;
+  }
   {
     ProfScope prof("peer");
     HSV_TRY(peer_barrier(p));

@@ -299,13 +299,24 @@ static int push_t(const hsv_op_s* op, const ApplyArgs& a0, bool* done, int64_t* 
   // read the real count on the device -- one host sync instead of two.
   static int64_t last_nsrc = -1;
   uint64_t *keys = nullptr, *keys2 = nullptr;
+  void* tmp = nullptr;
   bool sized = false;
+  // an allocation the push path cannot get is not an error: free what it holds
+  // and let launch_apply run the pull kernel, which needs no scratch keys
+#define HSV_PUSH_ALLOC(ptr, n)                                                   \
+  do {                                                                           \
+    if (dalloc((ptr), (n)) != HSV_OK) {                                          \
+      dfree(keys); dfree(keys2); dfree(reinterpret_cast<char*>(tmp));            \
+      dfree(src); dfree(cnt);                                                    \
+      return HSV_OK;                                                             \
+    }                                                                            \
+  } while (0)
   if (last_nsrc >= 0) {
     const int64_t guess = std::min<int64_t>(cap_src, std::max<int64_t>(4 * last_nsrc, 64));
     p.n_src = guess;
     p.n_src_dev = cnt;
     p.cap_keys = (unsigned long long)(guess * per_src);
-    HSV_TRY(dalloc(&keys, guess * per_src));
+    HSV_PUSH_ALLOC(&keys, guess * per_src);
     p.keys = keys;
     HSV_TRY(launch_keys(true));
     HSV_TRY_CUDA(cudaMemcpyAsync(h, cnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -333,7 +344,7 @@ static int push_t(const hsv_op_s* op, const ApplyArgs& a0, bool* done, int64_t* 
     p.n_src = (int64_t)h[0];
     p.n_src_dev = nullptr;
     p.cap_keys = (unsigned long long)(p.n_src * per_src);
-    HSV_TRY(dalloc(&keys, std::max<int64_t>(1, p.n_src * per_src)));
+    HSV_PUSH_ALLOC(&keys, std::max<int64_t>(1, p.n_src * per_src));
     p.keys = keys;
     HSV_TRY_CUDA(cudaMemsetAsync(cnt + 1, 0, sizeof(unsigned long long), stream()));
     HSV_TRY(launch_keys(false));
@@ -342,7 +353,9 @@ static int push_t(const hsv_op_s* op, const ApplyArgs& a0, bool* done, int64_t* 
     HSV_TRY(stream_sync());
   }
   const int64_t nk = (int64_t)h[1];
-  if (h[1] > p.cap_keys) {   // cannot happen (per-source bound); stay safe
+  // h[1] > cap_keys cannot happen (per-source bound); more than INT_MAX keys
+  // would truncate CUB's int item count: both go to the pull kernel
+  if (h[1] > p.cap_keys || nk > (int64_t)INT32_MAX) {
     dfree(keys); dfree(src); dfree(cnt);
     return HSV_OK;
   }
@@ -352,14 +365,13 @@ static int push_t(const hsv_op_s* op, const ApplyArgs& a0, bool* done, int64_t* 
       HSV_TRY_CUDA(cudaMemsetAsync(a0.out + p.lo, 0, rows * sizeof(double2), stream()));
     const int end_bit = gbits + bits_for((uint64_t)rows);
     const uint64_t* sorted = keys;
-    void* tmp = nullptr;
     if (nk > 1) {
-      HSV_TRY(dalloc(&keys2, nk));
+      HSV_PUSH_ALLOC(&keys2, nk);
       size_t tmp_bytes = 0;
       cub::DoubleBuffer<uint64_t> db(keys, keys2);
       HSV_TRY_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, db, (int)nk, 0, end_bit,
                                                   stream()));
-      HSV_TRY(dalloc(reinterpret_cast<char**>(&tmp), tmp_bytes));
+      HSV_PUSH_ALLOC(reinterpret_cast<char**>(&tmp), tmp_bytes);
       HSV_TRY_CUDA(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, db, (int)nk, 0, end_bit,
                                                   stream()));
       sorted = db.Current();
@@ -374,8 +386,9 @@ static int push_t(const hsv_op_s* op, const ApplyArgs& a0, bool* done, int64_t* 
     }
     if (a0.epart) HSV_TRY(reduce_sum_f64(eblk, nblk, 2, 2, a0.epart));
     dfree(eblk);
-    dfree(reinterpret_cast<char*>(tmp));
   }
+#undef HSV_PUSH_ALLOC
+  dfree(reinterpret_cast<char*>(tmp));
   dfree(keys2);
   dfree(keys);
   dfree(src);

@@ -678,17 +678,14 @@ static int forward_psi(const hsv_sector_s* sec, uint64_t hf_key, const uint64_t*
                                stream()));
   HSV_TRY_CUDA(cudaMemcpyAsync(psi->d_arow + sec->Ra[sa], &one_flag, sizeof(uint32_t),
                                cudaMemcpyHostToDevice, stream()));
-  if (tuning().sweep == 2) {   // batched sweep (hsv_sweep.cu); keeps the support map
+  if (tuning().sweep == 2) {   // batched sweep (hsv_sweep.cu) + the plan's support map
     if (!psi->d_smap) HSV_TRY(dalloc(&psi->d_smap, sec->dim));
-    static thread_local uint8_t one_b;
-    one_b = 1;
-    HSV_TRY_CUDA(cudaMemsetAsync(psi->d_smap, 0, sec->dim, stream()));
-    HSV_TRY_CUDA(cudaMemcpyAsync(psi->d_smap + hidx, &one_b, 1, cudaMemcpyHostToDevice, stream()));
     static thread_local std::vector<OpMasks> ops;
     ops.clear();
     for (int64_t i = 0; i < k; ++i) ops.push_back(compress_op(sec, occ[i], virt[i]));
-    HSV_TRY(launch_bsweep(sec, 0, ops, cs, sn, psi->d_amp, nullptr, psi->d_smap, psi->d_norm2,
-                          nullptr, sc.err, sc.err_val));
+    bool used = false;
+    HSV_TRY(launch_bsweep(sec, 0, hidx, ops, cs, sn, psi->d_amp, nullptr, psi->d_smap,
+                          psi->d_norm2, nullptr, sc.err, sc.err_val, &used));
     HSV_TRY(smap_arow_async(sec, psi->d_smap, psi->d_arow));
     psi->norm2_valid = psi->arow_valid = psi->smap_valid = true;
     psi->dense_hint = false;
@@ -761,7 +758,9 @@ int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const 
   PairLists pl;
   // K1r: the adjoint sweep reads w = H psi only on the structural support of
   // psi (rotation pairs never straddle it), so w is computed there
-  const bool rows_only = tuning().restrict_rows != 0 && tuning().sweep;
+  // (the support map closes over every rotation, theta = 0 included, in the
+  // batched sweep only)
+  const bool rows_only = tuning().restrict_rows != 0 && tuning().sweep == 2;
   HSV_TRY(forward_psi(sec, hf_key, occ, virt, cs, sn, k, psi, sc, pl, rows_only));
   int64_t used = 0;
   if (rows_only && psi->smap_valid)
@@ -818,7 +817,7 @@ int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
   double* d_grad = nullptr;
   HSV_TRY(dalloc(&d_grad, k + 2));
   HSV_TRY(state_dot_async(psi, w, d_grad + k));
-  if (tuning().sweep != 2) {   // flags of the one-barrier-per-rotation sweeps
+  if (tuning().sweep == 0) {   // flags of the per-rotation launches
     HSV_TRY(state_arow_async(psi));
     HSV_TRY(state_arow_async(w));
   }
@@ -826,14 +825,17 @@ int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
   PairScratch sc;
   HSV_TRY(sc.init(sec, 3));
   PairLists pl;
-  if (tuning().sweep == 2) {
+  bool batched = false;
+  if (tuning().sweep == 2 && psi->smap_valid) {   // psi came from the batched forward sweep
     static thread_local std::vector<OpMasks> bops;
     bops.clear();
     for (int64_t i = 0; i < k; ++i) bops.push_back(compress_op(sec, occ[i], virt[i]));
-    HSV_TRY(launch_bsweep(sec, 1, bops, cs, sn, psi->d_amp, w->d_amp,
-                          psi->smap_valid ? psi->d_smap : nullptr, w->d_norm2, d_grad, sc.err,
-                          sc.err_val));
-  } else if (tuning().sweep) {
+    HSV_TRY(launch_bsweep(sec, 1, -1, bops, cs, sn, psi->d_amp, w->d_amp, nullptr, w->d_norm2,
+                          d_grad, sc.err, sc.err_val, &batched));
+  }
+  if (!batched && tuning().sweep) {
+    HSV_TRY(state_arow_async(psi));
+    HSV_TRY(state_arow_async(w));
     static thread_local std::vector<SweepOp> ops;
     ops.clear();
     for (int64_t i = 0; i < k; ++i) ops.push_back(sweep_op(sec, occ[i], virt[i], cs[i], sn[i]));

@@ -20,8 +20,9 @@
 // order, so the plan and every reduction over it are deterministic.
 //
 // Support.  The forward sweep maintains the structural support map of psi
-// (hsv_state_s::d_smap; a rotation with s != 0 marks both rows of a pair if
-// either is marked).  Orbits with no marked row hold only exact zeros: the
+// (hsv_state_s::d_smap; every rotation -- also one at theta = 0, whose
+// gradient reads w on T psi -- marks both rows of a pair if either is
+// marked).  Orbits with no marked row hold only exact zeros: the
 // forward sweep skips them, and so does the adjoint sweep (it reads w = H psi
 // only on the support, see K1r).
 #include <cooperative_groups.h>
@@ -43,12 +44,12 @@ constexpr int kOrb = 1 << kBatch;
 enum { kFwd = 0, kAdj = 1 };
 
 struct BatchDev {
-  uint32_t oa[kBatch], va[kBatch], ob[kBatch], vb[kBatch];
   double c[kBatch], s[kBatch];
   int n;                 // rotations in the batch
   int op0;               // index (in sweep-list order) of the batch's first rotation
-  const uint2* items;    // orbit representatives (sa, sb)
-  const uint32_t* count; // number of items (device)
+  const uint32_t* rows;  // live orbits: kOrb rows each (plan)
+  const uint32_t* masks; // live orbits: touched | srcm_j << 8 (j + 1)
+  uint32_t count;        // live orbits of the batch
 };
 
 struct BSweepArgs {
@@ -147,13 +148,20 @@ __global__ void k_plan_candidates(const BuildArgs a) {
   a.flag[t] = keep ? 1 : 0;
 }
 
-// One orbit of a batch: forward rotations (MODE kFwd) or, in reverse order,
-// gradient partial + adjoint rotation + uncompute (kAdj).
-template <int MODE>
-__device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B, uint2 rep,
-                                         double (&acc)[kBatch][3], unsigned& npairs) {
-  uint32_t ea[kOrb], eb[kOrb];
-  unsigned touched = 0u, srcm[kBatch];
+// Geometry of one orbit: its rows, the rows a rotation of the batch touches
+// and, per rotation j, the orbit elements that are its sources (partner of
+// element t is t ^ (1 << j)).
+struct BatchMasks {
+  uint32_t oa[kBatch], va[kBatch], ob[kBatch], vb[kBatch];
+  int n;
+};
+
+__device__ __forceinline__ void orbit_geom(uint2 rep, const BatchMasks& B, int n_alpha,
+                                           int n_beta, const uint32_t* __restrict__ Ra,
+                                           const uint32_t* __restrict__ Rb, uint32_t Nb,
+                                           uint32_t (&row)[kOrb], unsigned& touched,
+                                           unsigned (&srcm)[kBatch]) {
+  touched = 0u;
 #pragma unroll
   for (int j = 0; j < kBatch; ++j) srcm[j] = 0u;
 #pragma unroll
@@ -162,9 +170,9 @@ __device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B,
 #pragma unroll
     for (int j = 0; j < kBatch; ++j)
       if (((t >> j) & 1) && j < B.n) { x ^= B.oa[j] | B.va[j]; y ^= B.ob[j] | B.vb[j]; }
-    ea[t] = x;
-    eb[t] = y;
-    if (t >= (1 << B.n) || __popc(x) != a.n_alpha || __popc(y) != a.n_beta) continue;
+    row[t] = 0u;
+    if (t >= (1 << B.n) || __popc(x) != n_alpha || __popc(y) != n_beta) continue;
+    row[t] = __ldg(Ra + x) * Nb + __ldg(Rb + y);
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
       if (j >= B.n) continue;
@@ -174,19 +182,120 @@ __device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B,
       }
     }
   }
-  uint32_t row[kOrb];
-  unsigned marked = 0u;
+}
+
+// Plan filter (cooperative, once per operator list): the structural support
+// closure of the HF row under every rotation, batch by batch, and for every
+// candidate orbit whether it holds a supported row when its batch runs (the
+// orbit is closed under the batch, so that is also whether it holds one after
+// it).  Only those "live" orbits are ever rotated, forward or adjoint.
+struct FilterArgs {
+  const BatchMasks* bm;
+  const uint2* const* cand;
+  const uint32_t* const* cand_count;
+  const int64_t* flag_off;
+  int n_batches;
+  uint8_t* flags;
+  uint8_t* smap;
+  int n_alpha, n_beta;
+  uint32_t Nb;
+  const uint32_t* Ra;
+  const uint32_t* Rb;
+  uint32_t* live_count;
+};
+
+__global__ void __launch_bounds__(256) k_plan_filter(const FilterArgs a) {
+  __shared__ BatchMasks B;
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  const int lane = threadIdx.x & 31;
+  for (int bi = 0; bi < a.n_batches; ++bi) {
+    if (threadIdx.x == 0) B = a.bm[bi];
+    __syncthreads();
+    const uint32_t n = __ldg(a.cand_count[bi]);
+    unsigned live_n = 0u;
+    for (int64_t it = gt; it < n; it += nt) {
+      uint32_t row[kOrb];
+      unsigned touched, srcm[kBatch];
+      orbit_geom(__ldg(a.cand[bi] + it), B, a.n_alpha, a.n_beta, a.Ra, a.Rb, a.Nb, row, touched,
+                 srcm);
+      unsigned marked = 0u;
 #pragma unroll
-  for (int t = 0; t < kOrb; ++t) {
-    row[t] = 0u;
-    if ((touched >> t) & 1u) {
-      row[t] = __ldg(a.Ra + ea[t]) * (uint32_t)a.Nb + __ldg(a.Rb + eb[t]);
-      if (!a.smap || a.smap[row[t]]) marked |= 1u << t;
+      for (int t = 0; t < kOrb; ++t)
+        if (((touched >> t) & 1u) && a.smap[row[t]]) marked |= 1u << t;
+      const bool live = marked != 0u;
+      a.flags[a.flag_off[bi] + it] = live ? 1 : 0;
+      if (!live) continue;
+      ++live_n;
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j)
+#pragma unroll
+        for (int t = 0; t < kOrb; ++t) {
+          if (!((srcm[j] >> t) & 1u)) continue;
+          const int p = t ^ (1 << j);
+          if ((marked >> t | marked >> p) & 1u) marked |= (1u << t) | (1u << p);
+        }
+#pragma unroll
+      for (int t = 0; t < kOrb; ++t)
+        if ((marked >> t) & 1u) a.smap[row[t]] = 1;
     }
+    const unsigned tot = __reduce_add_sync(0xffffffffu, live_n);
+    if (lane == 0 && tot) atomicAdd(a.live_count + bi, tot);
+    __syncthreads();
+    grid_sync();   // batch bi + 1 sees the marks of batch bi
   }
-  if (!marked) return;               // exact zeros only (or outside the support)
+}
+
+// Live orbit i (global order = batch order, then candidate order): its touched
+// rows and masks (touched | srcm_j << 8 (j + 1)), precomputed once per plan.
+struct GatherArgs {
+  const BatchMasks* bm;
+  const uint2* const* cand;
+  const int64_t* flag_off;
+  int n_batches;
+  const int* sel;
+  const int* n_sel;
+  int n_alpha, n_beta;
+  uint32_t Nb;
+  const uint32_t* Ra;
+  const uint32_t* Rb;
+  uint32_t* rows;
+  uint32_t* masks;
+};
+
+__global__ void k_plan_gather(const GatherArgs a) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= *a.n_sel) return;
+  const int64_t g = a.sel[i];
+  int lo = 0, hi = a.n_batches;   // last batch with flag_off <= g
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) / 2;
+    if (a.flag_off[mid] <= g) lo = mid; else hi = mid;
+  }
+  const BatchMasks B = a.bm[lo];
+  uint32_t row[kOrb];
+  unsigned touched, srcm[kBatch];
+  orbit_geom(a.cand[lo][g - a.flag_off[lo]], B, a.n_alpha, a.n_beta, a.Ra, a.Rb, a.Nb, row,
+             touched, srcm);
+  unsigned m = touched;
 #pragma unroll
-  for (int j = 0; j < kBatch; ++j) npairs += __popc(srcm[j]);
+  for (int j = 0; j < kBatch; ++j) m |= srcm[j] << (8 * (j + 1));
+  a.masks[i] = m;
+  uint4* r = reinterpret_cast<uint4*>(a.rows + i * kOrb);
+  r[0] = make_uint4(row[0], row[1], row[2], row[3]);
+  r[1] = make_uint4(row[4], row[5], row[6], row[7]);
+}
+
+// One live orbit of a batch: forward rotations (MODE kFwd) or, in reverse
+// order, gradient partial + adjoint rotation + uncompute (kAdj).
+template <int MODE>
+__device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B, int64_t it,
+                                         double (&acc)[kBatch][3], unsigned& npairs) {
+  const unsigned m = __ldg(B.masks + it);
+  const unsigned touched = m & 0xffu;
+  const uint4* rp = reinterpret_cast<const uint4*>(B.rows + it * kOrb);
+  const uint4 r0 = __ldg(rp), r1 = __ldg(rp + 1);
+  const uint32_t row[kOrb] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
   double2 v[kOrb];
   double2 l[kOrb];
 #pragma unroll
@@ -201,10 +310,12 @@ __device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B,
   if (MODE == kFwd) {
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
-      if (j >= B.n || (B.c[j] == 1.0 && B.s[j] == 0.0)) continue;   // theta == 0: skipped
+      const unsigned sj = (m >> (8 * (j + 1))) & 0xffu;
+      npairs += __popc(sj);
+      if (j >= B.n || (B.c[j] == 1.0 && B.s[j] == 0.0)) continue;   // theta == 0: identity
 #pragma unroll
       for (int t = 0; t < kOrb; ++t) {
-        if (!((srcm[j] >> t) & 1u)) continue;
+        if (!((sj >> t) & 1u)) continue;
         const int p = t ^ (1 << j);
         double2 nb, np;
         rot(v[t], v[p], B.c[j], B.s[j], nb, np);
@@ -212,23 +323,21 @@ __device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B,
         acc[j][1] += n2(nb) + n2(np);
         v[t] = nb;
         v[p] = np;
-        if ((marked >> t | marked >> p) & 1u) marked |= (1u << t) | (1u << p);
       }
     }
 #pragma unroll
-    for (int t = 0; t < kOrb; ++t) {
-      if (!((touched >> t) & 1u)) continue;
-      a.psi[row[t]] = v[t];
-      if (a.smap && ((marked >> t) & 1u)) a.smap[row[t]] = 1;
-    }
+    for (int t = 0; t < kOrb; ++t)
+      if ((touched >> t) & 1u) a.psi[row[t]] = v[t];
   } else {
 #pragma unroll
     for (int jj = kBatch - 1; jj >= 0; --jj) {
       if (jj >= B.n) continue;
+      const unsigned sj = (m >> (8 * (jj + 1))) & 0xffu;
+      npairs += __popc(sj);
       const bool unc = B.op0 + jj > 0;   // psi of the first rotation is never read again
 #pragma unroll
       for (int t = 0; t < kOrb; ++t) {
-        if (!((srcm[jj] >> t) & 1u)) continue;
+        if (!((sj >> t) & 1u)) continue;
         const int p = t ^ (1 << jj);
         const double2 pb = v[t], pp = v[p], lb = l[t], lp = l[p];
         acc[jj][0] += (lp.x * pb.x + lp.y * pb.y) - (lb.x * pp.x + lb.y * pp.y);
@@ -256,7 +365,7 @@ __device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B,
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256) k_bsweep(const BSweepArgs a) {
+__global__ void __launch_bounds__(256, MODE == kFwd ? 3 : 2) k_bsweep(const BSweepArgs a) {
   constexpr int NV = MODE == kAdj ? 3 : 2;
   __shared__ double sh[8][kBatch][NV];
   __shared__ BatchDev B;
@@ -266,13 +375,12 @@ __global__ void __launch_bounds__(256) k_bsweep(const BSweepArgs a) {
   for (int bi = 0; bi < a.n_batches; ++bi) {
     if (threadIdx.x == 0) B = a.batches[bi];
     __syncthreads();
-    const uint32_t n_items = __ldg(B.count);
+    const uint32_t n_items = B.count;
     double acc[kBatch][3];
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
     unsigned npairs = 0u;
-    for (int64_t it = gt; it < n_items; it += nt)
-      do_orbit<MODE>(a, B, __ldg(B.items + it), acc, npairs);
+    for (int64_t it = gt; it < n_items; it += nt) do_orbit<MODE>(a, B, it, acc, npairs);
     if (a.stats) {
       const unsigned tot = __reduce_add_sync(0xffffffffu, npairs);
       if (lane == 0 && tot) atomicAdd(a.stats + (MODE == kFwd ? kStatPairsFwd : kStatPairsAdj),
@@ -312,40 +420,81 @@ __global__ void __launch_bounds__(256) k_bsweep(const BSweepArgs a) {
     }
   }
   grid_sync();
-  if (blockIdx.x == 0 && threadIdx.x == 0) {   // norm chain in sweep order (svengine.py:234-236)
-    double nn = *a.norm2;
-    for (int o = 0; o < a.n_ops; ++o) {
-      const int op = MODE == kFwd ? o : a.n_ops - 1 - o;
-      const double* tot = a.red + (int64_t)op * NV;
-      const double dold = MODE == kAdj ? __ldcg(tot + 1) : __ldcg(tot);
-      const double dnew = MODE == kAdj ? __ldcg(tot + 2) : __ldcg(tot + 1);
-      const double nnew = nn - dold + dnew;
-      const double nrm = sqrt(fmax(nn, 0.0));
-      const double drift = fabs(sqrt(fmax(nnew, 0.0)) - nrm);
-      if (drift > kNormDriftTol * fmax(1.0, nrm)) {
-        if (atomicExch(a.err, 1) == 0) *a.err_val = drift;
+  if (blockIdx.x == 0) {   // norm chain in sweep order (svengine.py:234-236)
+    // the totals are staged in shared memory by the whole block first, so the
+    // sequential chain runs on on-chip loads (400 dependent L2 loads cost
+    // ~0.3 ms at k = 400)
+    constexpr int kChunk = 1024;
+    __shared__ double tsh[kChunk * NV];
+    double nn = 0.0;
+    if (threadIdx.x == 0) nn = *a.norm2;
+    for (int o0 = 0; o0 < a.n_ops; o0 += kChunk) {
+      const int n = min(kChunk, a.n_ops - o0);
+      __syncthreads();
+      for (int i = threadIdx.x; i < n * NV; i += blockDim.x) {
+        const int o = o0 + i / NV;
+        const int op = MODE == kFwd ? o : a.n_ops - 1 - o;
+        tsh[i] = __ldcg(a.red + (int64_t)op * NV + i % NV);
       }
-      nn = nnew;
-      if (MODE == kAdj) a.grads[op] = 2.0 * __ldcg(tot);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int i = 0; i < n; ++i) {
+          const double* tot = tsh + i * NV;
+          const double dold = MODE == kAdj ? tot[1] : tot[0];
+          const double dnew = MODE == kAdj ? tot[2] : tot[1];
+          const double nnew = nn - dold + dnew;
+          const double nrm = sqrt(fmax(nn, 0.0));
+          const double drift = fabs(sqrt(fmax(nnew, 0.0)) - nrm);
+          if (drift > kNormDriftTol * fmax(1.0, nrm)) {
+            if (atomicExch(a.err, 1) == 0) *a.err_val = drift;
+          }
+          nn = nnew;
+        }
+      }
+      if (MODE == kAdj)
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+          const int o = o0 + i;
+          a.grads[a.n_ops - 1 - o] = 2.0 * tsh[i * NV];
+        }
     }
-    *a.norm2 = nn;
+    if (threadIdx.x == 0) *a.norm2 = nn;
   }
 }
 
 // ----------------------------------------------------------------- plans
 struct PlanBatch {
   std::vector<OpMasks> m;
-  int64_t n_cand = 0;
-  uint2* items = nullptr;
-  uint32_t* count = nullptr;
+  int64_t n_cand = 0;             // upper bound of the candidate count
+  uint2* cand = nullptr;          // canonical orbit representatives
+  uint32_t* cand_count = nullptr; // device count
 };
 
+// Cached per (sector, HF row, operator list): batches with their candidate
+// orbits (reused by prefix: an appended operator changes the last batch only),
+// and -- after the filter -- the live orbits with precomputed rows and the
+// structural support closure of HF (the K1r rows).
 struct Plan {
   const hsv_sector_s* sec = nullptr;
+  int64_t hf_row = -1;
   std::vector<PlanBatch> b;
+  bool filtered = false;
+  uint8_t* smap = nullptr;
+  uint32_t* rows = nullptr;
+  uint32_t* masks = nullptr;
+  std::vector<int64_t> live_off, live_cnt;
+  int64_t max_live = 0;
+  void drop_live() {
+    dfree(rows); dfree(masks);
+    rows = masks = nullptr;
+    filtered = false;
+  }
   void clear() {
-    for (auto& x : b) { dfree(x.items); dfree(x.count); }
+    for (auto& x : b) { dfree(x.cand); dfree(x.cand_count); }
     b.clear();
+    drop_live();
+    dfree(smap);
+    smap = nullptr;
+    hf_row = -1;
   }
 };
 
@@ -377,6 +526,15 @@ std::vector<std::vector<int>> partition(const std::vector<OpMasks>& ops) {
   return out;
 }
 
+BatchMasks batch_masks(const PlanBatch& pb) {
+  BatchMasks m{};
+  m.n = (int)pb.m.size();
+  for (int j = 0; j < m.n; ++j) {
+    m.oa[j] = pb.m[j].oa; m.va[j] = pb.m[j].va; m.ob[j] = pb.m[j].ob; m.vb[j] = pb.m[j].vb;
+  }
+  return m;
+}
+
 int build_batch(const hsv_sector_s* sec, PlanBatch& pb) {
   BuildArgs a{};
   a.n = (int)pb.m.size();
@@ -391,16 +549,15 @@ int build_batch(const hsv_sector_s* sec, PlanBatch& pb) {
     if (a.ca[j] == 0 || a.cb[j] == 0) a.ca[j] = a.cb[j] = 0;
     a.off[j + 1] = a.off[j] + a.ca[j] * a.cb[j];
   }
-  if (a.cb[0] == 0) a.cb[0] = 1;   // guard the division of an empty range
-  for (int j = 1; j < a.n; ++j)
+  for (int j = 0; j < a.n; ++j)   // guard the division of an empty range
     if (a.cb[j] == 0) a.cb[j] = 1;
   const int64_t T = a.off[a.n];
   pb.n_cand = T;
-  HSV_TRY(dalloc(&pb.items, std::max<int64_t>(T, 1)));
-  HSV_TRY(dalloc(&pb.count, 1));
-  HSV_TRY_CUDA(cudaMemsetAsync(pb.count, 0, sizeof(uint32_t), stream()));
+  HSV_TRY(dalloc(&pb.cand, std::max<int64_t>(T, 1)));
+  HSV_TRY(dalloc(&pb.cand_count, 1));
+  HSV_TRY_CUDA(cudaMemsetAsync(pb.cand_count, 0, sizeof(uint32_t), stream()));
   if (T == 0) return HSV_OK;
-  HSV_REQUIRE(T < (int64_t)UINT32_MAX, HSV_ERR_UNSUPPORTED, "batch plan too large");
+  HSV_REQUIRE(T < (int64_t)INT32_MAX, HSV_ERR_UNSUPPORTED, "batch plan too large");
   uint2* cand = nullptr;
   uint8_t* flag = nullptr;
   HSV_TRY(dalloc(&cand, T));
@@ -411,29 +568,147 @@ int build_batch(const hsv_sector_s* sec, PlanBatch& pb) {
   count_launch();
   HSV_CHECK_LAUNCH();
   size_t tb = 0;
-  HSV_TRY_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, cand, flag, pb.items, pb.count, (int)T,
+  HSV_TRY_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, cand, flag, pb.cand, pb.cand_count, (int)T,
                                           stream()));
-  void* tmp = nullptr;
-  HSV_TRY(dalloc(reinterpret_cast<char**>(&tmp), tb));
-  HSV_TRY_CUDA(cub::DeviceSelect::Flagged(tmp, tb, cand, flag, pb.items, pb.count, (int)T,
+  char* tmp = nullptr;
+  HSV_TRY(dalloc(&tmp, tb));
+  HSV_TRY_CUDA(cub::DeviceSelect::Flagged(tmp, tb, cand, flag, pb.cand, pb.cand_count, (int)T,
                                           stream()));
   count_launch();
-  dfree(reinterpret_cast<char*>(tmp));
+  dfree(tmp);
   dfree(cand);
   dfree(flag);
   return HSV_OK;
 }
 
-// Plan for the operator list `ops`; batches equal to the cached ones at the
-// same position are reused.
-int get_plan(const hsv_sector_s* sec, const std::vector<OpMasks>& ops,
-             std::vector<std::vector<int>>& parts) {
+int coop_grid(const void* fn, int64_t want) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, 0) != cudaSuccess) {
+    cudaGetLastError();
+    occ = 1;
+  }
+  const int64_t resident = (int64_t)ctx().num_sms * std::max(occ, 1);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(resident, want));
+}
+
+// The filter + gather of a plan whose batches are built (hsv: k_plan_filter).
+int filter_plan(Plan& P) {
+  const hsv_sector_s* sec = P.sec;
+  const int nb = (int)P.b.size();
+  P.drop_live();
+  if (!P.smap) HSV_TRY(dalloc(&P.smap, sec->dim));
+  static thread_local uint8_t one;
+  one = 1;
+  HSV_TRY_CUDA(cudaMemsetAsync(P.smap, 0, sec->dim, stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(P.smap + P.hf_row, &one, 1, cudaMemcpyHostToDevice, stream()));
+  P.live_off.assign(nb + 1, 0);
+  P.live_cnt.assign(nb, 0);
+  P.max_live = 0;
+  if (nb == 0) return stream_sync();
+  std::vector<BatchMasks> hm(nb);
+  std::vector<const uint2*> hc(nb);
+  std::vector<const uint32_t*> hn(nb);
+  std::vector<int64_t> off(nb + 1, 0);
+  int64_t max_cand = 1;
+  for (int q = 0; q < nb; ++q) {
+    hm[q] = batch_masks(P.b[q]);
+    hc[q] = P.b[q].cand;
+    hn[q] = P.b[q].cand_count;
+    off[q + 1] = off[q] + P.b[q].n_cand;
+    max_cand = std::max(max_cand, P.b[q].n_cand);
+  }
+  const int64_t total = off[nb];
+  HSV_REQUIRE(total < (int64_t)INT32_MAX, HSV_ERR_UNSUPPORTED, "sweep plan too large");
+  BatchMasks* d_m = nullptr;
+  const uint2** d_c = nullptr;
+  const uint32_t** d_n = nullptr;
+  int64_t* d_off = nullptr;
+  uint8_t* flags = nullptr;
+  uint32_t* live = nullptr;
+  int *sel = nullptr, *n_sel = nullptr;
+  HSV_TRY(dalloc(&d_m, nb));
+  HSV_TRY(dalloc(&d_c, nb));
+  HSV_TRY(dalloc(&d_n, nb));
+  HSV_TRY(dalloc(&d_off, nb + 1));
+  HSV_TRY(dalloc(&flags, std::max<int64_t>(total, 1)));
+  HSV_TRY(dalloc(&live, nb));
+  HSV_TRY(dalloc(&sel, std::max<int64_t>(total, 1)));
+  HSV_TRY(dalloc(&n_sel, 1));
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_m, hm.data(), nb * sizeof(BatchMasks), cudaMemcpyHostToDevice,
+                               stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_c, hc.data(), nb * sizeof(void*), cudaMemcpyHostToDevice,
+                               stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_n, hn.data(), nb * sizeof(void*), cudaMemcpyHostToDevice,
+                               stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_off, off.data(), (nb + 1) * sizeof(int64_t),
+                               cudaMemcpyHostToDevice, stream()));
+  HSV_TRY_CUDA(cudaMemsetAsync(flags, 0, std::max<int64_t>(total, 1), stream()));
+  HSV_TRY_CUDA(cudaMemsetAsync(live, 0, nb * sizeof(uint32_t), stream()));
+  FilterArgs fa{};
+  fa.bm = d_m; fa.cand = d_c; fa.cand_count = d_n; fa.flag_off = d_off; fa.n_batches = nb;
+  fa.flags = flags; fa.smap = P.smap; fa.n_alpha = sec->n_alpha; fa.n_beta = sec->n_beta;
+  fa.Nb = (uint32_t)sec->Nb; fa.Ra = sec->d_Ra; fa.Rb = sec->d_Rb; fa.live_count = live;
+  {
+    ProfScope prof("sweep_plan");
+    const int grid = coop_grid((const void*)k_plan_filter, (max_cand + 255) / 256);
+    void* params[] = {&fa};
+    HSV_TRY_CUDA(cudaLaunchCooperativeKernel((const void*)k_plan_filter, dim3(grid), dim3(256),
+                                             params, 0, stream()));
+    count_launch();
+    size_t tb = 0;
+    cub::CountingInputIterator<int> idx(0);
+    HSV_TRY_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, idx, flags, sel, n_sel, (int)total,
+                                            stream()));
+    char* tmp = nullptr;
+    HSV_TRY(dalloc(&tmp, tb));
+    HSV_TRY_CUDA(cub::DeviceSelect::Flagged(tmp, tb, idx, flags, sel, n_sel, (int)total,
+                                            stream()));
+    count_launch();
+    dfree(tmp);
+  }
+  std::vector<uint32_t> hl(nb);
+  HSV_TRY_CUDA(cudaMemcpyAsync(hl.data(), live, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               stream()));
+  HSV_TRY(stream_sync());
+  for (int q = 0; q < nb; ++q) {
+    P.live_cnt[q] = hl[q];
+    P.live_off[q + 1] = P.live_off[q] + hl[q];
+    P.max_live = std::max<int64_t>(P.max_live, hl[q]);
+  }
+  const int64_t n_live = P.live_off[nb];
+  HSV_TRY(dalloc(&P.rows, std::max<int64_t>(n_live, 1) * kOrb));
+  HSV_TRY(dalloc(&P.masks, std::max<int64_t>(n_live, 1)));
+  if (n_live > 0) {
+    GatherArgs ga{};
+    ga.bm = d_m; ga.cand = d_c; ga.flag_off = d_off; ga.n_batches = nb; ga.sel = sel;
+    ga.n_sel = n_sel; ga.n_alpha = sec->n_alpha; ga.n_beta = sec->n_beta;
+    ga.Nb = (uint32_t)sec->Nb; ga.Ra = sec->d_Ra; ga.Rb = sec->d_Rb;
+    ga.rows = P.rows; ga.masks = P.masks;
+    ProfScope prof("sweep_plan");
+    k_plan_gather<<<(unsigned)((n_live + 255) / 256), 256, 0, stream()>>>(ga);
+    count_launch();
+    HSV_CHECK_LAUNCH();
+  }
+  dfree(d_m); dfree(d_c); dfree(d_n); dfree(d_off); dfree(flags); dfree(live); dfree(sel);
+  dfree(n_sel);
+  P.filtered = true;
+  return HSV_OK;
+}
+
+// Plan for (hf_row, ops): cached batches equal to the requested ones at the
+// same position are reused; the live lists are refiltered whenever anything
+// changed.  hf_row < 0: the caller (the adjoint sweep) needs the current plan
+// as it is; *ok = false when it does not match.
+int get_plan(const hsv_sector_s* sec, int64_t hf_row, const std::vector<OpMasks>& ops,
+             std::vector<std::vector<int>>& parts, bool* ok) {
   Plan& P = plan();
+  *ok = true;
+  parts = partition(ops);
   if (P.sec != sec) {
+    if (hf_row < 0) { *ok = false; return HSV_OK; }
     P.clear();
     P.sec = sec;
   }
-  parts = partition(ops);
   size_t keep = 0;
   while (keep < parts.size() && keep < P.b.size()) {
     const auto& idx = parts[keep];
@@ -443,7 +718,11 @@ int get_plan(const hsv_sector_s* sec, const std::vector<OpMasks>& ops,
     if (!eq) break;
     ++keep;
   }
-  for (size_t q = keep; q < P.b.size(); ++q) { dfree(P.b[q].items); dfree(P.b[q].count); }
+  const bool unchanged = keep == parts.size() && keep == P.b.size() &&
+                         (hf_row < 0 || hf_row == P.hf_row) && P.filtered;
+  if (unchanged) return HSV_OK;
+  if (hf_row < 0) { *ok = false; return HSV_OK; }
+  for (size_t q = keep; q < P.b.size(); ++q) { dfree(P.b[q].cand); dfree(P.b[q].cand_count); }
   P.b.resize(keep);
   for (size_t q = keep; q < parts.size(); ++q) {
     PlanBatch pb;
@@ -451,22 +730,34 @@ int get_plan(const hsv_sector_s* sec, const std::vector<OpMasks>& ops,
     HSV_TRY(build_batch(sec, pb));
     P.b.push_back(pb);
   }
-  return HSV_OK;
+  P.hf_row = hf_row;
+  return filter_plan(P);
 }
 
 }  // namespace
 
 // Batched sweep over the rotation list (ops[i], cs[i], sn[i]) in list order:
-// MODE 0 forward (psi rotated, smap maintained), 1 adjoint (reverse order;
-// gradients into d_grads[i]; psi uncomputed, lam = w rotated).
-int launch_bsweep(const hsv_sector_s* sec, int mode, const std::vector<OpMasks>& ops,
-                  const double* cs, const double* sn, double2* psi, double2* lam, uint8_t* smap,
-                  double* norm2, double* d_grads, int* err, double* err_val) {
+// mode 0 forward from |hf_row> (psi rotated; the plan's support map copied to
+// smap_out), 1 adjoint (reverse order; gradients into d_grads[i]; psi
+// uncomputed, lam = w rotated; hf_row ignored, the forward's plan is reused).
+// *used = false: no matching plan (the caller runs the per-rotation sweep).
+int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
+                  const std::vector<OpMasks>& ops, const double* cs, const double* sn,
+                  double2* psi, double2* lam, uint8_t* smap_out, double* norm2, double* d_grads,
+                  int* err, double* err_val, bool* used) {
+  *used = true;
   const int k = (int)ops.size();
-  if (k == 0) return HSV_OK;
   std::vector<std::vector<int>> parts;
-  HSV_TRY(get_plan(sec, ops, parts));
+  bool ok = true;
+  HSV_TRY(get_plan(sec, mode == kFwd ? hf_row : -1, ops, parts, &ok));
+  if (!ok) {
+    *used = false;
+    return HSV_OK;
+  }
   Plan& P = plan();
+  if (smap_out)
+    HSV_TRY_CUDA(cudaMemcpyAsync(smap_out, P.smap, sec->dim, cudaMemcpyDeviceToDevice, stream()));
+  if (k == 0) return HSV_OK;
   const int nb = (int)parts.size();
   static thread_local std::vector<BatchDev> hb;
   hb.assign(nb, BatchDev{});
@@ -477,47 +768,37 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, const std::vector<OpMasks>&
     d.op0 = parts[bq][0];
     for (int j = 0; j < d.n; ++j) {
       const int i = parts[bq][j];
-      d.oa[j] = ops[i].oa; d.va[j] = ops[i].va; d.ob[j] = ops[i].ob; d.vb[j] = ops[i].vb;
       d.c[j] = cs[i];
       d.s[j] = sn[i];
     }
-    d.items = P.b[bq].items;
-    d.count = P.b[bq].count;
+    d.rows = P.rows + P.live_off[bq] * kOrb;
+    d.masks = P.masks + P.live_off[bq];
+    d.count = (uint32_t)P.live_cnt[bq];
   }
   BatchDev* d_b = nullptr;
   HSV_TRY(dalloc(&d_b, nb));
   HSV_TRY_CUDA(cudaMemcpyAsync(d_b, hb.data(), nb * sizeof(BatchDev), cudaMemcpyHostToDevice,
                                stream()));
-  static int occ[2] = {0, 0};
-  if (!occ[mode]) {
-    HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &occ[mode], mode == kFwd ? (const void*)k_bsweep<kFwd> : (const void*)k_bsweep<kAdj>, 256,
-        0));
-    occ[mode] = std::max(occ[mode], 1);
-  }
-  int64_t max_items = 1;
-  for (int q = 0; q < nb; ++q) max_items = std::max(max_items, P.b[q].n_cand);
-  const int64_t resident = (int64_t)ctx().num_sms * occ[mode];
-  const int64_t want = tuning().sweep_grid > 0 ? tuning().sweep_grid
-                       : std::min<int64_t>(resident, (max_items + 255) / 256);
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(resident, want));
+  const void* fn = mode == kFwd ? (const void*)k_bsweep<kFwd> : (const void*)k_bsweep<kAdj>;
+  const int64_t want = tuning().sweep_grid > 0 ? tuning().sweep_grid : (P.max_live + 255) / 256;
+  const int grid = coop_grid(fn, std::max<int64_t>(want, 1));
   const int NV = mode == kAdj ? 3 : 2;
   double *part = nullptr, *red = nullptr;
   HSV_TRY(dalloc(&part, (int64_t)nb * grid * kBatch * NV));
   HSV_TRY(dalloc(&red, (int64_t)k * NV));
+  HSV_TRY_CUDA(cudaMemsetAsync(red, 0, (int64_t)k * NV * sizeof(double), stream()));
   BSweepArgs a{};
   a.batches = d_b; a.n_batches = nb; a.n_ops = k;
   a.n_alpha = sec->n_alpha; a.n_beta = sec->n_beta; a.Nb = sec->Nb;
   a.Ra = sec->d_Ra; a.Rb = sec->d_Rb;
-  a.psi = psi; a.lam = lam; a.smap = smap; a.part = part; a.red = red;
+  a.psi = psi; a.lam = lam; a.smap = nullptr; a.part = part; a.red = red;
   a.norm2 = norm2; a.grads = d_grads; a.err = err; a.err_val = err_val;
   a.stats = ctx().d_stats;
   void* params[] = {&a};
   {
     ProfScope prof(mode == kFwd ? "qeb" : "adjoint");
-    HSV_TRY_CUDA(cudaLaunchCooperativeKernel(
-        mode == kFwd ? (const void*)k_bsweep<kFwd> : (const void*)k_bsweep<kAdj>,
-        dim3((unsigned)grid), dim3(256), params, 0, stream()));
+    HSV_TRY_CUDA(cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(256), params, 0,
+                                             stream()));
   }
   count_launch();
   dfree(d_b);
@@ -526,7 +807,13 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, const std::vector<OpMasks>&
   return HSV_OK;
 }
 
-void release_sweep_plans() { plan().clear(); }
+void release_sweep_plans(const hsv_sector_s* s) {
+  Plan& P = plan();
+  if (!s || P.sec == s) {
+    P.clear();
+    P.sec = nullptr;
+  }
+}
 
 // Alpha-row occupancy flags from the structural support map (a superset of
 // the nonzeros, which is all the flags promise): one warp per alpha row.

@@ -107,6 +107,11 @@ class PeerExchange:
         except Exception:
             pass
 
+    def check(self) -> None:
+        """Raise RuntimeError if a bounded device-side wait timed out or a peer
+        aborted since the last check (hsv_peer_check; synchronizes)."""
+        N.call("hsv_peer_check", self.handle)
+
     def data(self) -> int:
         ptr, n = N.C.c_void_p(), N.i64()
         N.call("hsv_peer_data", self.handle, N.C.byref(ptr), N.C.byref(n))
@@ -220,6 +225,8 @@ class DistributedSvAdaptEngine:
         else:
             tot = gather_and_combine(sc.partial, self.group)
         host = tot.cpu().numpy()
+        if self.peer is not None:
+            self.peer.check()                     # bounded waits: timeout / peer abort
         return float(host[0]), host[2:2 + sc.pool.n].copy()
 
     def screen(self, state, pool):
@@ -258,6 +265,8 @@ class DistributedSvAdaptEngine:
         N.call("hsv_eg_backward", self.matrix.handle, self._psi.handle, self._w.handle,
                N.ptr_u64(occ), N.ptr_u64(virt), N.ptr_f64(cs), N.ptr_f64(sn), th.size,
                N.C.byref(e), N.ptr_f64(g))
+        if not rep and self.peer is not None:
+            self.peer.check()
         return float(e.value), g
 
 
