@@ -43,14 +43,16 @@ constexpr int kBatch = 3;               // rotations per batch (orbits of 2^kBat
 constexpr int kOrb = 1 << kBatch;
 enum { kFwd = 0, kAdj = 1 };
 
-struct BatchDev {
+struct __align__(16) BatchDev {
   double c[kBatch], s[kBatch];
-  int n;                 // rotations in the batch
-  int op0;               // index (in sweep-list order) of the batch's first rotation
   const uint32_t* rows;  // live orbits: kOrb rows each (plan)
   const uint32_t* masks; // live orbits: touched | srcm_j << 8 (j + 1)
+  int n;                 // rotations in the batch
+  int op0;               // index (in sweep-list order) of the batch's first rotation
   uint32_t count;        // live orbits of the batch
 };
+constexpr int kBChunk = 96;   // batch descriptors staged in shared memory at a time
+static_assert(sizeof(BatchDev) % 16 == 0, "BatchDev is copied as 16-byte words");
 
 struct BSweepArgs {
   const BatchDev* batches;
@@ -368,13 +370,22 @@ template <int MODE>
 __global__ void __launch_bounds__(256, MODE == kFwd ? 3 : 2) k_bsweep(const BSweepArgs a) {
   constexpr int NV = MODE == kAdj ? 3 : 2;
   __shared__ double sh[8][kBatch][NV];
-  __shared__ BatchDev B;
+  // batch descriptors staged in shared memory kBChunk at a time by the whole
+  // block: no serial descriptor load between a grid barrier and the next batch
+  __shared__ __align__(16) BatchDev sB[kBChunk];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nt = (int64_t)gridDim.x * blockDim.x;
   for (int bi = 0; bi < a.n_batches; ++bi) {
-    if (threadIdx.x == 0) B = a.batches[bi];
-    __syncthreads();
+    if (bi % kBChunk == 0) {
+      const int n = min(kBChunk, a.n_batches - bi);
+      constexpr int W4 = sizeof(BatchDev) / 16;
+      const uint4* src = reinterpret_cast<const uint4*>(a.batches + bi);
+      uint4* dst = reinterpret_cast<uint4*>(sB);
+      for (int i = threadIdx.x; i < n * W4; i += blockDim.x) dst[i] = __ldg(src + i);
+      __syncthreads();
+    }
+    const BatchDev& B = sB[bi % kBChunk];
     const uint32_t n_items = B.count;
     double acc[kBatch][3];
 #pragma unroll

@@ -119,12 +119,13 @@ def test_rb0_shared_memory_is_bitwise_equal(hsv, N, name):
 def test_bperm_is_bitwise_equal(hsv, N, name):
     """K1 pass-1 partner ranks from the per-xb 16-bit permutation rows (tuning
     bperm, on by default where built) equal the Rb0 gather: rows and energy
-    bitwise, with and without bucket splits, at R = 8 and at R = 2."""
+    bitwise, with and without bucket splits.  The permutation rows are used by
+    the R = 8 kernel only (hsv_apply.cu launch_apply), so R = 8 is the case."""
     sysm = hsv.MolecularSystem.bundled(name)
     op = hsv.assemble_subspace_hamiltonian(sysm.hamiltonian, sysm.basis)
     st = dense_state(hsv, sysm)
     try:
-        for split, r in ((1, 8), (8, 8), (8, 2)):
+        for split, r in ((1, 8), (8, 8), (32, 8)):
             N.call("hsv_set_tuning", b"bperm", 0)
             y0, e0 = rows_of(N, op, st, split, r)
             N.call("hsv_set_tuning", b"bperm", 1)
