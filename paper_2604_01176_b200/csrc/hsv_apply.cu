@@ -384,9 +384,9 @@ __global__ void k_combine_splits_map(const double2* __restrict__ part, int S, in
   put_row(out, peers, n_peers, off + i, y);
 }
 
-static void launch_combine_splits_map(const double2* part, int S, int64_t rows, double2* out,
-                                      int64_t off, const uint8_t* smap, double2* const* peers,
-                                      int n_peers) {
+void launch_combine_splits_map(const double2* part, int S, int64_t rows, double2* out,
+                               int64_t off, const uint8_t* smap, double2* const* peers,
+                               int n_peers) {
   k_combine_splits_map<<<(unsigned)((rows + 255) / 256), 256, 0, stream()>>>(
       part, S, rows, out, off, smap, peers, n_peers);
 }
@@ -429,7 +429,7 @@ static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_wa
   // 32, while that leaves fewer than 8 units per warp (rank shards: H12 / 8
   // 0.354 against 0.42 ms with the earlier at-most-8 rule).  Capped so the
   // partial rows stay under 32 GB.
-  int S = tuning().apply_split;
+  int S = a0.nsplit > 0 ? a0.nsplit : tuning().apply_split;
   if (S <= 0) {
     S = 8;
     while (S < 32 && units1_full * S < 8 * max_warps) S *= 2;
@@ -492,6 +492,35 @@ static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_wa
   return HSV_OK;
 }
 
+// Rows per lane of the register-row K1 (launch_apply's automatic choice).
+static int k1_auto_r(const hsv_sector_s* s, int64_t a_lo, int64_t a_hi) {
+  const int64_t units8 = (a_hi - a_lo) * ((s->Nb + 255) / 256);
+  const int64_t warps8 = (int64_t)ctx().num_sms * 2 * 8;
+  const int64_t units4 = (a_hi - a_lo) * ((s->Nb + 127) / 128);
+  const int64_t warps4 = (int64_t)ctx().num_sms * 3 * 8;
+  const bool dyn = tuning().apply_interleave < 0 || tuning().apply_interleave == 2;
+  return (dyn ? 32 * units8 >= warps8 : 4 * units8 >= 3 * warps8) ? 8 : units4 >= warps4 ? 4 : 2;
+}
+
+// The bucket split count the default register-row K1 uses for rows
+// [a_lo, a_hi) (launch_apply_t's rule; its occupancy is the launch-bounds
+// minimum: R = 8 -> 2, 4 -> 3, 2 -> 4 blocks of 256 per SM).  Every kernel that
+// must reproduce K1's rows bit for bit (K1r, K1v) uses this S.
+int k1_default_split(const hsv_op_s* op, int64_t a_lo, int64_t a_hi, bool has_out) {
+  if (!op->d_splits) return 1;
+  if (tuning().apply_split > 0) return tuning().apply_split;
+  const hsv_sector_s* s = op->sec;
+  const int R = tuning().apply_r > 0 ? tuning().apply_r : k1_auto_r(s, a_lo, a_hi);
+  const int occ = R == 8 ? 2 : R == 4 ? 3 : 4;
+  const int64_t units1 = (a_hi - a_lo) * ((s->Nb + 32 * R - 1) / (32 * R));
+  const int64_t max_warps = (int64_t)ctx().num_sms * occ * 8;
+  int S = 8;
+  while (S < 32 && units1 * S < 8 * max_warps) S *= 2;
+  const int64_t rows_all = (a_hi - a_lo) * s->Nb;
+  while (S > 1 && has_out && S * rows_all * (int64_t)sizeof(double2) > (32ll << 30)) S /= 2;
+  return S;
+}
+
 int apply_warps(const hsv_op_s* op) {
   // upper bound on the warps the apply kernel uses (energy-partial sizing):
   // 256-thread blocks, at most 8 resident per SM
@@ -523,6 +552,14 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
     bool done = false;
     HSV_TRY(launch_push(op, a, &done, n_warps, dense_hint));
     if (done) return HSV_OK;
+  }
+  if (out && tuning().staged != 1) {   // K1v: valid beta lists (hsv_apply_v.cu)
+    bool done = false;
+    HSV_TRY(launch_apply_v(op, a, k1_default_split(op, a_lo, a_hi, true), &done));
+    if (done) {
+      if (n_warps) *n_warps = 1;   // epart[0..1] holds the total
+      return HSV_OK;
+    }
   }
   {   // small beta rows: partner rows staged on chip by TMA (hsv_apply_staged.cu)
     bool done = false;
@@ -687,6 +724,15 @@ int launch_apply_rows(const hsv_op_s* op, const double2* psi, double2* out, int6
   a.Nb = s->Nb; a.a_lo = a_lo; a.a_hi = a_hi; a.prune = 0.0; a.energy_only = 0;
   // rows per lane: 8 while the full row range gives a 256-row unit to every
   // resident warp (the full kernel's rule), else 4
+  const int S = k1_default_split(op, a_lo, a_hi, true);
+  {   // K1v over the support rows (hsv_apply_v.cu)
+    bool done = false;
+    ApplyArgs av = a;
+    av.smap = smap;
+    HSV_TRY(launch_apply_v(op, av, S, &done));
+    if (done) return HSV_OK;
+  }
+  a.nsplit = S;
   const int64_t units8 = (a_hi - a_lo) * ((s->Nb + 255) / 256);
   const int R = 32 * units8 >= (int64_t)ctx().num_sms * 2 * 8 ? 8 : 4;
   RowList rl;
@@ -1179,13 +1225,48 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
                                                   (uint32_t)op->groups[q].x) - xbs.begin()) * NbP);
     }
   }
+  // K1v valid lists: per distinct beta flip xb of a hashed group, the beta
+  // strings whose partner stays in the sector, rank-ascending, with chunk
+  // offsets (Rec.pad1 = list * (nchunks + 1)).  Nb <= 65535 (16-bit ranks).
+  std::vector<uint2> vl;
+  std::vector<int> vloff;
+  std::vector<uint32_t> vslot(ghash.size(), 0u);
+  const int vchunk = 1024;
+  const int vnch = (int)((s->Nb + vchunk - 1) / vchunk);
+  if (SH == 16 && s->Nb <= 65535) {
+    std::vector<uint32_t> xbs;
+    for (size_t q = 0; q < ghash.size(); ++q)
+      if (ghash[q].tab >= 0) xbs.push_back((uint32_t)op->groups[q].x);
+    std::sort(xbs.begin(), xbs.end());
+    xbs.erase(std::unique(xbs.begin(), xbs.end()), xbs.end());
+    for (size_t i = 0; i < xbs.size(); ++i) {
+      const uint32_t xb = xbs[i];
+      const int need = __builtin_popcount(xb) / 2;
+      int c = 0;
+      for (int64_t rb = 0; rb < s->Nb; ++rb) {
+        while (c <= vnch && rb >= (int64_t)c * vchunk) { vloff.push_back((int)vl.size()); ++c; }
+        const uint32_t sb = s->Sb[rb];
+        if (__builtin_popcount(sb & xb) != need) continue;
+        const uint32_t rp = s->Rb[sb ^ xb];
+        if (rp == ~0u) continue;
+        vl.push_back(make_uint2((uint32_t)rb | (rp << 16), sb));
+      }
+      while (c <= vnch) { vloff.push_back((int)vl.size()); ++c; }
+    }
+    for (size_t q = 0; q < ghash.size(); ++q)
+      if (ghash[q].tab >= 0)
+        vslot[q] = (uint32_t)((std::lower_bound(xbs.begin(), xbs.end(),
+                                                (uint32_t)op->groups[q].x) - xbs.begin()) *
+                              (vnch + 1));
+  }
   if (SH == 16) {
     recs.resize(ghash.size() * 32);
     for (size_t q = 0; q < ghash.size(); ++q) {
       const GroupHash& h = ghash[q];
       uint32_t r[8] = {(uint32_t)op->groups[q].x,
                        (uint32_t)op->groups[q].y | ((uint32_t)h.shift << 8), (uint32_t)h.xm,
-                       (uint32_t)h.z0, (uint32_t)h.mul, (uint32_t)std::max(h.tab, 0), bslot[q], 0u};
+                       (uint32_t)h.z0, (uint32_t)h.mul, (uint32_t)std::max(h.tab, 0), bslot[q],
+                       vslot[q]};
       memcpy(&recs[q * 32], r, 32);
     }
   } else {
@@ -1230,6 +1311,16 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
     HSV_TRY_CUDA(cudaMemcpyAsync(op->d_bperm, bperm.data(), bperm.size() * sizeof(uint16_t),
                                  cudaMemcpyHostToDevice, st));
   }
+  if (!vl.empty()) {
+    if ((rc = dalloc(&op->d_vl, vl.size())) || (rc = dalloc(&op->d_vloff, vloff.size())))
+      return fail(rc);
+    HSV_TRY_CUDA(cudaMemcpyAsync(op->d_vl, vl.data(), vl.size() * sizeof(uint2),
+                                 cudaMemcpyHostToDevice, st));
+    HSV_TRY_CUDA(cudaMemcpyAsync(op->d_vloff, vloff.data(), vloff.size() * sizeof(int),
+                                 cudaMemcpyHostToDevice, st));
+    op->vl_chunk = vchunk;
+    op->vl_nchunks = vnch;
+  }
   if (!ghash.empty())
     HSV_TRY_CUDA(cudaMemcpyAsync(op->d_ghash, ghash.data(), ghash.size() * sizeof(GroupHash),
                                  cudaMemcpyHostToDevice, st));
@@ -1266,6 +1357,8 @@ int hsv_op_destroy(hsv_op op) {
   dfree(reinterpret_cast<SzTerm*>(op->d_szt));
   dfree(op->d_gxa);
   dfree(op->d_bperm);
+  dfree(op->d_vl);
+  dfree(op->d_vloff);
   delete op;
   return HSV_OK;
 }

@@ -177,6 +177,13 @@ struct hsv_op_s {
   GroupHash* d_ghash = nullptr;
   void* d_recs = nullptr;       // packed Rec<W> per group (kernel layout)
   uint16_t* d_bperm = nullptr;  // per-xb beta rank permutations (Rec.pad0 = slot), or nullptr
+  // K1v valid lists (hsv_apply_v.cu): for each distinct beta flip xb of a hashed
+  // group, the beta strings whose partner sb ^ xb stays in the sector, in rank
+  // order, as {rb | rank(sb ^ xb) << 16, sb}; d_vloff[Rec.pad1 + c] = first
+  // entry with rb >= c * vl_chunk (vl_nchunks + 1 per list).  nullptr: not built.
+  uint2* d_vl = nullptr;
+  int* d_vloff = nullptr;
+  int vl_chunk = 0, vl_nchunks = 0;
   int64_t n_buckets_h = 0;      // buckets [0, n_buckets_h) are x-local (hashed)
   int* d_splits = nullptr;      // split cuts (SplitTable::cut_off)
   int4* d_vbuckets = nullptr;   // virtual buckets of the split tables

@@ -24,6 +24,11 @@ struct Tuning {
                           // 0/-1 off (default: measured 1-3% slower at H12/H14)
   int restrict_rows = -1; // K1r in the adjoint evaluation (w = H psi on the structural
                           // support of psi only): -1/1 on, 0 off (full K1 / push)
+  int apply_v = 0;        // K1v (per-group valid beta lists, shared-memory row accumulators):
+                          // 1 on where built, 0/-1 off.  Bitwise equal to K1 but measured
+                          // 2.4x slower at H12 (5.80 vs 2.40 ms): the per-group chain (record
+                          // -> list offsets -> entries -> gathers -> shared-memory update,
+                          // __syncwarp) serializes groups that K1 pipelines in registers
   int staged = 0;         // K1s (TMA-staged partner rows) where the sector fits: 1 on, 0 off.
                           // Off by default: it cuts K1's global load sectors 8.4x at H12
                           // but not its time (K1 is issue-bound; 3.04 vs 3.07 ms)
@@ -78,6 +83,11 @@ struct ApplyArgs {
   const uint32_t* rcnt;
   const uint2* utab;
   const uint32_t* d_units;
+  // K1v (valid lists, hsv_apply_v.cu)
+  const uint2* vl;
+  const int* vloff;
+  int vl_chunk, vl_nchunks;
+  const uint8_t* smap;     // K1v row-restricted mode: rows outside the map are skipped
 };
 
 // K1r: row lists of the rows marked in smap (or, smap == nullptr, of the
@@ -150,10 +160,17 @@ int apply_warps(const hsv_op_s* op);
 // dense_hint (optional, per state): skip when set, set when psi is found dense.
 int launch_push(const hsv_op_s* op, const ApplyArgs& a, bool* done, int64_t* n_warps,
                 bool* dense_hint);
+// K1v (hsv_apply_v.cu): *done = false when the operator has no valid lists.
+// S = the bucket split count the register-row K1 would use (same row values).
+int launch_apply_v(const hsv_op_s* op, const ApplyArgs& a, int S, bool* done);
 // K1s (hsv_apply_staged.cu): *done = false when the sector does not fit on chip.
 int launch_apply_staged(const hsv_op_s* op, const ApplyArgs& a, int64_t* n_warps, bool* done);
 void launch_combine_splits(const double2* part, int S, int64_t rows, double2* out, int64_t off,
                            double prune, double2* const* peers, int n_peers);
+void launch_combine_splits_map(const double2* part, int S, int64_t rows, double2* out,
+                               int64_t off, const uint8_t* smap, double2* const* peers,
+                               int n_peers);
+int k1_default_split(const hsv_op_s* op, int64_t a_lo, int64_t a_hi, bool has_out);
 int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* epart,
                  int64_t a_lo, int64_t a_hi, double prune, int energy_only, int64_t* n_warps,
                  const uint32_t* arow = nullptr, bool* dense_hint = nullptr);

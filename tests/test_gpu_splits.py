@@ -26,9 +26,11 @@ def hsv():
 @pytest.fixture()
 def N():
     from paper_2604_01176_b200 import _native as N
+    N.call("hsv_set_tuning", b"apply_v", 0)      # these tests target the register-row K1
     yield N
     N.call("hsv_set_tuning", b"apply_split", 0)
     N.call("hsv_set_tuning", b"apply_r", 0)
+    N.call("hsv_set_tuning", b"apply_v", -1)
 
 
 def dense_state(hsv, sysm):
