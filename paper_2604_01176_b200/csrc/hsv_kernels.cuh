@@ -18,6 +18,11 @@ struct Tuning {
   int sweep = 2;          // adjoint/forward sweeps: 2 batched (orbits of kBatch rotations per
                           // grid barrier, hsv_sweep.cu), 1 one barrier per rotation, 0 launch per op
   int sweep_grid = 0;     // sweep blocks: 0 = min(co-resident, work items)
+  int sweep_p2p = 0;      // batched sweeps without grid barriers (per-row versions, k_psweep):
+                          // 1 on, 0 off.  Exact, but measured 2.9x slower at H12 depth 400
+                          // (2.60 vs 0.88 ms forward): consecutive batches share rows densely
+                          // (a batch touches ~25% of the support), so the version waits
+                          // chain batch after batch and the spinning adds latency
   int bperm = -1;         // K1 (R=8) pass-1 ranks from per-xb 16-bit permutation rows (built
                           // for 32-bit words, Nb <= 65536, <= 256 MB): -1/1 on, 0 off
   int rb0_smem = 0;       // K1 (R=8) pass-1 Rb0 table in shared memory: 1 on (norb <= 15),

@@ -80,6 +80,9 @@ int hsv_set_tuning(const char* key, int64_t value) {
   } else if (k == "apply_v") {
     HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "apply_v must be -1, 0 or 1");
     g_tuning.apply_v = (int)value;
+  } else if (k == "sweep_p2p") {
+    HSV_REQUIRE(value == 0 || value == 1, HSV_ERR_INVALID, "sweep_p2p must be 0 or 1");
+    g_tuning.sweep_p2p = (int)value;
   } else if (k == "restrict_rows") {
     HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "restrict_rows must be -1, 0 or 1");
     g_tuning.restrict_rows = (int)value;

@@ -47,6 +47,7 @@ struct __align__(16) BatchDev {
   double c[kBatch], s[kBatch];
   const uint32_t* rows;  // live orbits: kOrb rows each (plan)
   const uint32_t* masks; // live orbits: touched | srcm_j << 8 (j + 1)
+  const uint32_t* ranks; // live orbits: per element, write rank | row writers << 16
   int n;                 // rotations in the batch
   int op0;               // index (in sweep-list order) of the batch's first rotation
   uint32_t count;        // live orbits of the batch
@@ -72,6 +73,15 @@ struct BSweepArgs {
   int* err;
   double* err_val;
   unsigned long long* stats;   // pairs processed (kStatPairsFwd / kStatPairsAdj)
+  uint32_t* ver;               // barrier-free sweep: writes completed per row (zeroed)
+  // barrier-free sweep: the plan's global (padded) orbit arrays, chunk maps
+  const uint32_t* rows;
+  const uint32_t* masks;
+  const uint32_t* ranks;
+  int64_t n_chunks;
+  const int* chunk_batch;       // physical chunk -> batch (plan order)
+  const uint32_t* chunk_order;  // sweep order -> physical chunk (nullptr: identity)
+  const int64_t* chunk_off;     // batch -> first chunk (n_batches + 1)
 };
 
 __device__ __forceinline__ void rot(double2 vb, double2 vp, double c, double s, double2& nb,
@@ -204,6 +214,8 @@ struct FilterArgs {
   const uint32_t* Ra;
   const uint32_t* Rb;
   uint32_t* live_count;
+  uint32_t* wcount;       // per row: live orbits (so far, in batch order) that touch it
+  uint16_t* wrank;        // per candidate and orbit element: the orbit's rank among them
 };
 
 __global__ void __launch_bounds__(256) k_plan_filter(const FilterArgs a) {
@@ -240,6 +252,16 @@ __global__ void __launch_bounds__(256) k_plan_filter(const FilterArgs a) {
 #pragma unroll
       for (int t = 0; t < kOrb; ++t)
         if ((marked >> t) & 1u) a.smap[row[t]] = 1;
+      // write ranks for the barrier-free sweep: orbits of one batch are
+      // disjoint, and the grid barrier orders batches, so a plain increment
+      // gives every row's writers their batch order
+#pragma unroll
+      for (int t = 0; t < kOrb; ++t)
+        if (a.wcount && ((touched >> t) & 1u)) {
+          const uint32_t r = a.wcount[row[t]];
+          a.wcount[row[t]] = r + 1;
+          a.wrank[(a.flag_off[bi] + it) * kOrb + t] = (uint16_t)min(r, 65535u);
+        }
     }
     const unsigned tot = __reduce_add_sync(0xffffffffu, live_n);
     if (lane == 0 && tot) atomicAdd(a.live_count + bi, tot);
@@ -263,6 +285,11 @@ struct GatherArgs {
   const uint32_t* Rb;
   uint32_t* rows;
   uint32_t* masks;
+  const uint16_t* wrank;
+  const uint32_t* wcount;
+  uint32_t* ranks;        // per live orbit element: rank | (writers of the row) << 16
+  const int64_t* loff_cmp;  // live orbits before batch b (compact) ...
+  const int64_t* loff_pad;  // ... and in the padded layout (whole 32-orbit chunks per batch)
 };
 
 __global__ void k_plan_gather(const GatherArgs a) {
@@ -279,13 +306,71 @@ __global__ void k_plan_gather(const GatherArgs a) {
   unsigned touched, srcm[kBatch];
   orbit_geom(a.cand[lo][g - a.flag_off[lo]], B, a.n_alpha, a.n_beta, a.Ra, a.Rb, a.Nb, row,
              touched, srcm);
+  const int64_t si = i;   // compact index (selection order)
+  const int64_t pi = a.loff_pad[lo] + (si - a.loff_cmp[lo]);   // padded slot
   unsigned m = touched;
 #pragma unroll
   for (int j = 0; j < kBatch; ++j) m |= srcm[j] << (8 * (j + 1));
-  a.masks[i] = m;
-  uint4* r = reinterpret_cast<uint4*>(a.rows + i * kOrb);
+  a.masks[pi] = m;
+  uint4* r = reinterpret_cast<uint4*>(a.rows + pi * kOrb);
   r[0] = make_uint4(row[0], row[1], row[2], row[3]);
   r[1] = make_uint4(row[4], row[5], row[6], row[7]);
+  if (a.ranks) {
+    uint32_t k[kOrb];
+#pragma unroll
+    for (int t = 0; t < kOrb; ++t)
+      k[t] = ((touched >> t) & 1u)
+                 ? (uint32_t)a.wrank[g * kOrb + t] | (min(a.wcount[row[t]], 65535u) << 16)
+                 : 0u;
+    uint4* kr = reinterpret_cast<uint4*>(a.ranks + pi * kOrb);
+    kr[0] = make_uint4(k[0], k[1], k[2], k[3]);
+    kr[1] = make_uint4(k[4], k[5], k[6], k[7]);
+  }
+}
+
+// Norm-drift chain in sweep order (svengine.py:234-236) and, adjoint, the
+// gradients: block 0, after the per-rotation totals are complete.
+template <int MODE, int NV>
+__device__ __forceinline__ void norm_chain(const BSweepArgs& a) {
+  if (blockIdx.x == 0) {   // norm chain in sweep order (svengine.py:234-236)
+    // the totals are staged in shared memory by the whole block first, so the
+    // sequential chain runs on on-chip loads (400 dependent L2 loads cost
+    // ~0.3 ms at k = 400)
+    constexpr int kChunk = 1024;
+    __shared__ double tsh[kChunk * NV];
+    double nn = 0.0;
+    if (threadIdx.x == 0) nn = *a.norm2;
+    for (int o0 = 0; o0 < a.n_ops; o0 += kChunk) {
+      const int n = min(kChunk, a.n_ops - o0);
+      __syncthreads();
+      for (int i = threadIdx.x; i < n * NV; i += blockDim.x) {
+        const int o = o0 + i / NV;
+        const int op = MODE == kFwd ? o : a.n_ops - 1 - o;
+        tsh[i] = __ldcg(a.red + (int64_t)op * NV + i % NV);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int i = 0; i < n; ++i) {
+          const double* tot = tsh + i * NV;
+          const double dold = MODE == kAdj ? tot[1] : tot[0];
+          const double dnew = MODE == kAdj ? tot[2] : tot[1];
+          const double nnew = nn - dold + dnew;
+          const double nrm = sqrt(fmax(nn, 0.0));
+          const double drift = fabs(sqrt(fmax(nnew, 0.0)) - nrm);
+          if (drift > kNormDriftTol * fmax(1.0, nrm)) {
+            if (atomicExch(a.err, 1) == 0) *a.err_val = drift;
+          }
+          nn = nnew;
+        }
+      }
+      if (MODE == kAdj)
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+          const int o = o0 + i;
+          a.grads[a.n_ops - 1 - o] = 2.0 * tsh[i * NV];
+        }
+    }
+    if (threadIdx.x == 0) *a.norm2 = nn;
+  }
 }
 
 // One live orbit of a batch: forward rotations (MODE kFwd) or, in reverse
@@ -431,45 +516,177 @@ __global__ void __launch_bounds__(256, MODE == kFwd ? 3 : 2) k_bsweep(const BSwe
     }
   }
   grid_sync();
-  if (blockIdx.x == 0) {   // norm chain in sweep order (svengine.py:234-236)
-    // the totals are staged in shared memory by the whole block first, so the
-    // sequential chain runs on on-chip loads (400 dependent L2 loads cost
-    // ~0.3 ms at k = 400)
-    constexpr int kChunk = 1024;
-    __shared__ double tsh[kChunk * NV];
-    double nn = 0.0;
-    if (threadIdx.x == 0) nn = *a.norm2;
-    for (int o0 = 0; o0 < a.n_ops; o0 += kChunk) {
-      const int n = min(kChunk, a.n_ops - o0);
-      __syncthreads();
-      for (int i = threadIdx.x; i < n * NV; i += blockDim.x) {
-        const int o = o0 + i / NV;
-        const int op = MODE == kFwd ? o : a.n_ops - 1 - o;
-        tsh[i] = __ldcg(a.red + (int64_t)op * NV + i % NV);
-      }
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        for (int i = 0; i < n; ++i) {
-          const double* tot = tsh + i * NV;
-          const double dold = MODE == kAdj ? tot[1] : tot[0];
-          const double dnew = MODE == kAdj ? tot[2] : tot[1];
-          const double nnew = nn - dold + dnew;
-          const double nrm = sqrt(fmax(nn, 0.0));
-          const double drift = fabs(sqrt(fmax(nnew, 0.0)) - nrm);
-          if (drift > kNormDriftTol * fmax(1.0, nrm)) {
-            if (atomicExch(a.err, 1) == 0) *a.err_val = drift;
-          }
-          nn = nnew;
-        }
-      }
-      if (MODE == kAdj)
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-          const int o = o0 + i;
-          a.grads[a.n_ops - 1 - o] = 2.0 * tsh[i * NV];
-        }
-    }
-    if (threadIdx.x == 0) *a.norm2 = nn;
+  norm_chain<MODE, NV>(a);
+}
+
+// ------------------------------------------------- barrier-free variant
+// The same orbit work without grid barriers between batches: every row
+// carries a version (writes completed in this sweep); an orbit of batch b
+// waits, per touched row, until the orbits of earlier batches (forward order;
+// later ones in the adjoint) that touch it have written it -- its rank among
+// the row's writers, from the plan -- then rotates and publishes version + 1
+// with a release store.  Orbits of one batch are disjoint, so each row's
+// writers are totally ordered and the amplitudes are exactly the sequential
+// ones; warps run ahead into later batches wherever the rows allow, instead
+// of the whole grid waiting for the slowest block of every batch (67% of the
+// barrier sweep's stall samples were grid/block barriers, ncu).
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <int MODE>
+__device__ __forceinline__ void do_orbit_p2p(const BSweepArgs& a, const BatchDev& B, int64_t it,
+                                             double (&acc)[kBatch][3], unsigned& npairs) {
+  // it: global (padded) orbit index of the plan; padding orbits have masks 0
+  const unsigned m = __ldg(a.masks + it);
+  const unsigned touched = m & 0xffu;
+  if (!touched) return;
+  const uint4* rp = reinterpret_cast<const uint4*>(a.rows + it * kOrb);
+  const uint4 r0 = __ldg(rp), r1 = __ldg(rp + 1);
+  const uint32_t row[kOrb] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+  const uint4* kp = reinterpret_cast<const uint4*>(a.ranks + it * kOrb);
+  const uint4 k0 = __ldg(kp), k1 = __ldg(kp + 1);
+  const uint32_t rk[kOrb] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+  uint32_t need[kOrb];
+#pragma unroll
+  for (int t = 0; t < kOrb; ++t) {
+    const uint32_t r = rk[t] & 0xffffu, n = rk[t] >> 16;
+    need[t] = MODE == kFwd ? r : n - 1u - r;
   }
+#pragma unroll
+  for (int t = 0; t < kOrb; ++t) {
+    if (!((touched >> t) & 1u)) continue;
+    unsigned ns = 32;
+    while (ld_acquire(a.ver + row[t]) != need[t]) {   // backoff: hot rows have many waiters
+      __nanosleep(ns);
+      ns = min(ns * 2, 1024u);
+    }
+  }
+  double2 v[kOrb];
+  double2 l[kOrb];
+#pragma unroll
+  for (int t = 0; t < kOrb; ++t) {
+    v[t] = make_double2(0.0, 0.0);
+    l[t] = make_double2(0.0, 0.0);
+    if ((touched >> t) & 1u) {
+      v[t] = __ldcg(a.psi + row[t]);
+      if (MODE == kAdj) l[t] = __ldcg(a.lam + row[t]);
+    }
+  }
+  if (MODE == kFwd) {
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) {
+      const unsigned sj = (m >> (8 * (j + 1))) & 0xffu;
+      npairs += __popc(sj);
+      if (j >= B.n || (B.c[j] == 1.0 && B.s[j] == 0.0)) continue;
+#pragma unroll
+      for (int t = 0; t < kOrb; ++t) {
+        if (!((sj >> t) & 1u)) continue;
+        const int p = t ^ (1 << j);
+        double2 nb, np;
+        rot(v[t], v[p], B.c[j], B.s[j], nb, np);
+        acc[j][0] += n2(v[t]) + n2(v[p]);
+        acc[j][1] += n2(nb) + n2(np);
+        v[t] = nb;
+        v[p] = np;
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kOrb; ++t)
+      if ((touched >> t) & 1u) __stcg(a.psi + row[t], v[t]);
+  } else {
+#pragma unroll
+    for (int jj = kBatch - 1; jj >= 0; --jj) {
+      if (jj >= B.n) continue;
+      const unsigned sj = (m >> (8 * (jj + 1))) & 0xffu;
+      npairs += __popc(sj);
+      const bool unc = B.op0 + jj > 0;
+#pragma unroll
+      for (int t = 0; t < kOrb; ++t) {
+        if (!((sj >> t) & 1u)) continue;
+        const int p = t ^ (1 << jj);
+        const double2 pb = v[t], pp = v[p], lb = l[t], lp = l[p];
+        acc[jj][0] += (lp.x * pb.x + lp.y * pb.y) - (lb.x * pp.x + lb.y * pp.y);
+        double2 nb, np;
+        rot(lb, lp, B.c[jj], -B.s[jj], nb, np);
+        acc[jj][1] += n2(lb) + n2(lp);
+        acc[jj][2] += n2(nb) + n2(np);
+        l[t] = nb;
+        l[p] = np;
+        if (unc) {
+          double2 qb, qp;
+          rot(pb, pp, B.c[jj], -B.s[jj], qb, qp);
+          v[t] = qb;
+          v[p] = qp;
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kOrb; ++t) {
+      if (!((touched >> t) & 1u)) continue;
+      __stcg(a.lam + row[t], l[t]);
+      __stcg(a.psi + row[t], v[t]);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < kOrb; ++t)
+    if ((touched >> t) & 1u) st_release(a.ver + row[t], need[t] + 1u);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) k_psweep(const BSweepArgs a) {
+  constexpr int NV = MODE == kAdj ? 3 : 2;
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  // Live orbits are laid out batch after batch, each batch padded to whole
+  // 32-orbit chunks; warps take chunks round robin in sweep order (adjoint:
+  // batches reversed), so consecutive batches run on different warps at the
+  // same time, ordered only by the rows they share.
+  for (int64_t L = gw; L < a.n_chunks; L += nw) {
+    const int64_t c = a.chunk_order ? (int64_t)__ldg(a.chunk_order + L) : L;
+    const int bi = __ldg(a.chunk_batch + c);
+    const BatchDev& B = a.batches[bi];
+    double acc[kBatch][3];
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j) acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
+    unsigned npairs = 0u;
+    do_orbit_p2p<MODE>(a, B, c * 32 + lane, acc, npairs);
+    if (a.stats) {
+      const unsigned tot = __reduce_add_sync(0xffffffffu, npairs);
+      if (lane == 0 && tot) atomicAdd(a.stats + (MODE == kFwd ? kStatPairsFwd : kStatPairsAdj),
+                                      (unsigned long long)tot);
+    }
+#pragma unroll
+    for (int j = 0; j < kBatch; ++j)
+#pragma unroll
+      for (int q = 0; q < NV; ++q) {
+        const double x = warp_sum(acc[j][q]);
+        if (lane == 0) a.part[(c * kBatch + j) * NV + q] = x;
+      }
+  }
+  grid_sync();   // every chunk partial written
+  // per-rotation totals: one rotation per warp, the batch's chunks in order
+  for (int64_t oi = gw; oi < (int64_t)a.n_batches * kBatch; oi += nw) {
+    const int bi = (int)(oi / kBatch), j = (int)(oi - (int64_t)bi * kBatch);
+    const BatchDev& B = a.batches[bi];
+    if (j >= B.n) continue;
+    const int64_t c0 = __ldg(a.chunk_off + bi), c1 = __ldg(a.chunk_off + bi + 1);
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double x = 0.0;
+      for (int64_t k = c0 + lane; k < c1; k += 32) x += __ldcg(a.part + (k * kBatch + j) * NV + q);
+      x = warp_sum(x);
+      if (lane == 0) a.red[(int64_t)(B.op0 + j) * NV + q] = x;
+    }
+  }
+  grid_sync();
+  norm_chain<MODE, NV>(a);
 }
 
 // ----------------------------------------------------------------- plans
@@ -492,11 +709,21 @@ struct Plan {
   uint8_t* smap = nullptr;
   uint32_t* rows = nullptr;
   uint32_t* masks = nullptr;
+  uint32_t* ranks = nullptr;   // barrier-free sweep: per element write rank | writers << 16
+  uint32_t* ver = nullptr;     // per-row versions (dim), zeroed before each barrier-free sweep
+  int* chunk_batch = nullptr;  // physical 32-orbit chunk -> batch
+  uint32_t* chunk_rev = nullptr;   // adjoint order: chunks of the batches in reverse
+  int64_t* chunk_off = nullptr;    // batch -> first chunk
+  int64_t n_chunks = 0;
   std::vector<int64_t> live_off, live_cnt;
   int64_t max_live = 0;
   void drop_live() {
-    dfree(rows); dfree(masks);
-    rows = masks = nullptr;
+    dfree(rows); dfree(masks); dfree(ranks);
+    dfree(chunk_batch); dfree(chunk_rev); dfree(chunk_off);
+    rows = masks = ranks = chunk_rev = nullptr;
+    chunk_batch = nullptr;
+    chunk_off = nullptr;
+    n_chunks = 0;
     filtered = false;
   }
   void clear() {
@@ -504,7 +731,9 @@ struct Plan {
     b.clear();
     drop_live();
     dfree(smap);
+    dfree(ver);
     smap = nullptr;
+    ver = nullptr;
     hf_row = -1;
   }
 };
@@ -602,6 +831,12 @@ int coop_grid(const void* fn, int64_t want) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(resident, want));
 }
 
+int64_t ops_total(const Plan& P) {
+  int64_t n = 0;
+  for (const auto& b : P.b) n += (int64_t)b.m.size();
+  return n;
+}
+
 // The filter + gather of a plan whose batches are built (hsv: k_plan_filter).
 int filter_plan(Plan& P) {
   const hsv_sector_s* sec = P.sec;
@@ -637,6 +872,14 @@ int filter_plan(Plan& P) {
   uint8_t* flags = nullptr;
   uint32_t* live = nullptr;
   int *sel = nullptr, *n_sel = nullptr;
+  uint32_t* wcount = nullptr;
+  uint16_t* wrank = nullptr;
+  const bool ranks = (int64_t)ops_total(P) < 65535;
+  if (ranks) {
+    HSV_TRY(dalloc(&wcount, sec->dim));
+    HSV_TRY(dalloc(&wrank, std::max<int64_t>(total, 1) * kOrb));
+    HSV_TRY_CUDA(cudaMemsetAsync(wcount, 0, sec->dim * sizeof(uint32_t), stream()));
+  }
   HSV_TRY(dalloc(&d_m, nb));
   HSV_TRY(dalloc(&d_c, nb));
   HSV_TRY(dalloc(&d_n, nb));
@@ -659,6 +902,7 @@ int filter_plan(Plan& P) {
   fa.bm = d_m; fa.cand = d_c; fa.cand_count = d_n; fa.flag_off = d_off; fa.n_batches = nb;
   fa.flags = flags; fa.smap = P.smap; fa.n_alpha = sec->n_alpha; fa.n_beta = sec->n_beta;
   fa.Nb = (uint32_t)sec->Nb; fa.Ra = sec->d_Ra; fa.Rb = sec->d_Rb; fa.live_count = live;
+  fa.wcount = wcount; fa.wrank = wrank;
   {
     ProfScope prof("sweep_plan");
     const int grid = coop_grid((const void*)k_plan_filter, (max_cand + 255) / 256);
@@ -681,27 +925,69 @@ int filter_plan(Plan& P) {
   HSV_TRY_CUDA(cudaMemcpyAsync(hl.data(), live, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                stream()));
   HSV_TRY(stream_sync());
+  std::vector<int64_t> cmp(nb + 1, 0);
   for (int q = 0; q < nb; ++q) {
     P.live_cnt[q] = hl[q];
-    P.live_off[q + 1] = P.live_off[q] + hl[q];
+    cmp[q + 1] = cmp[q] + hl[q];
+    P.live_off[q + 1] = P.live_off[q] + ((int64_t)hl[q] + 31) / 32 * 32;   // whole chunks
     P.max_live = std::max<int64_t>(P.max_live, hl[q]);
   }
-  const int64_t n_live = P.live_off[nb];
-  HSV_TRY(dalloc(&P.rows, std::max<int64_t>(n_live, 1) * kOrb));
-  HSV_TRY(dalloc(&P.masks, std::max<int64_t>(n_live, 1)));
+  const int64_t n_live = cmp[nb];
+  const int64_t n_slots = P.live_off[nb];
+  HSV_TRY(dalloc(&P.rows, std::max<int64_t>(n_slots, 1) * kOrb));
+  HSV_TRY(dalloc(&P.masks, std::max<int64_t>(n_slots, 1)));
+  HSV_TRY_CUDA(cudaMemsetAsync(P.masks, 0, std::max<int64_t>(n_slots, 1) * sizeof(uint32_t),
+                               stream()));
+  if (ranks) HSV_TRY(dalloc(&P.ranks, std::max<int64_t>(n_slots, 1) * kOrb));
+  // chunk maps of the barrier-free sweep
+  P.n_chunks = n_slots / 32;
+  {
+    std::vector<int> cb(std::max<int64_t>(P.n_chunks, 1));
+    std::vector<uint32_t> rev;
+    std::vector<int64_t> choff(nb + 1);
+    rev.reserve(P.n_chunks);
+    for (int q = 0; q < nb; ++q) {
+      choff[q] = P.live_off[q] / 32;
+      for (int64_t c = P.live_off[q] / 32; c < P.live_off[q + 1] / 32; ++c) cb[c] = q;
+    }
+    choff[nb] = P.n_chunks;
+    for (int q = nb - 1; q >= 0; --q)
+      for (int64_t c = P.live_off[q] / 32; c < P.live_off[q + 1] / 32; ++c) rev.push_back((uint32_t)c);
+    HSV_TRY(dalloc(&P.chunk_batch, cb.size()));
+    HSV_TRY(dalloc(&P.chunk_rev, std::max<size_t>(rev.size(), 1)));
+    HSV_TRY(dalloc(&P.chunk_off, nb + 1));
+    HSV_TRY_CUDA(cudaMemcpyAsync(P.chunk_batch, cb.data(), cb.size() * sizeof(int),
+                                 cudaMemcpyHostToDevice, stream()));
+    if (!rev.empty())
+      HSV_TRY_CUDA(cudaMemcpyAsync(P.chunk_rev, rev.data(), rev.size() * sizeof(uint32_t),
+                                   cudaMemcpyHostToDevice, stream()));
+    HSV_TRY_CUDA(cudaMemcpyAsync(P.chunk_off, choff.data(), (nb + 1) * sizeof(int64_t),
+                                 cudaMemcpyHostToDevice, stream()));
+    HSV_TRY(stream_sync());   // host vectors die here
+  }
+  int64_t *d_cmp = nullptr, *d_pad = nullptr;
+  HSV_TRY(dalloc(&d_cmp, nb + 1));
+  HSV_TRY(dalloc(&d_pad, nb + 1));
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_cmp, cmp.data(), (nb + 1) * sizeof(int64_t),
+                               cudaMemcpyHostToDevice, stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_pad, P.live_off.data(), (nb + 1) * sizeof(int64_t),
+                               cudaMemcpyHostToDevice, stream()));
   if (n_live > 0) {
     GatherArgs ga{};
     ga.bm = d_m; ga.cand = d_c; ga.flag_off = d_off; ga.n_batches = nb; ga.sel = sel;
     ga.n_sel = n_sel; ga.n_alpha = sec->n_alpha; ga.n_beta = sec->n_beta;
     ga.Nb = (uint32_t)sec->Nb; ga.Ra = sec->d_Ra; ga.Rb = sec->d_Rb;
     ga.rows = P.rows; ga.masks = P.masks;
+    ga.wrank = wrank; ga.wcount = wcount; ga.ranks = P.ranks;
+    ga.loff_cmp = d_cmp; ga.loff_pad = d_pad;
     ProfScope prof("sweep_plan");
     k_plan_gather<<<(unsigned)((n_live + 255) / 256), 256, 0, stream()>>>(ga);
     count_launch();
     HSV_CHECK_LAUNCH();
   }
   dfree(d_m); dfree(d_c); dfree(d_n); dfree(d_off); dfree(flags); dfree(live); dfree(sel);
-  dfree(n_sel);
+  dfree(n_sel); dfree(wcount); dfree(wrank); dfree(d_cmp); dfree(d_pad);
+  HSV_TRY(stream_sync());   // the host offset vectors above must outlive their copies
   P.filtered = true;
   return HSV_OK;
 }
@@ -770,10 +1056,12 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
     HSV_TRY_CUDA(cudaMemcpyAsync(smap_out, P.smap, sec->dim, cudaMemcpyDeviceToDevice, stream()));
   if (k == 0) return HSV_OK;
   const int nb = (int)parts.size();
+  const bool p2p = P.ranks && tuning().sweep_p2p != 0;
   static thread_local std::vector<BatchDev> hb;
   hb.assign(nb, BatchDev{});
   for (int q = 0; q < nb; ++q) {
-    const int bq = mode == kFwd ? q : nb - 1 - q;
+    // barrier version: descriptors in processing order; barrier-free: plan order
+    const int bq = (mode == kFwd || p2p) ? q : nb - 1 - q;
     BatchDev& d = hb[q];
     d.n = (int)parts[bq].size();
     d.op0 = parts[bq][0];
@@ -784,18 +1072,26 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
     }
     d.rows = P.rows + P.live_off[bq] * kOrb;
     d.masks = P.masks + P.live_off[bq];
+    d.ranks = P.ranks ? P.ranks + P.live_off[bq] * kOrb : nullptr;
     d.count = (uint32_t)P.live_cnt[bq];
   }
   BatchDev* d_b = nullptr;
   HSV_TRY(dalloc(&d_b, nb));
   HSV_TRY_CUDA(cudaMemcpyAsync(d_b, hb.data(), nb * sizeof(BatchDev), cudaMemcpyHostToDevice,
                                stream()));
-  const void* fn = mode == kFwd ? (const void*)k_bsweep<kFwd> : (const void*)k_bsweep<kAdj>;
-  const int64_t want = tuning().sweep_grid > 0 ? tuning().sweep_grid : (P.max_live + 255) / 256;
+  const void* fn = p2p ? (mode == kFwd ? (const void*)k_psweep<kFwd> : (const void*)k_psweep<kAdj>)
+                       : (mode == kFwd ? (const void*)k_bsweep<kFwd> : (const void*)k_bsweep<kAdj>);
+  const int64_t want = tuning().sweep_grid > 0 ? tuning().sweep_grid
+                       : p2p ? (int64_t)ctx().num_sms * 2 : (P.max_live + 255) / 256;
   const int grid = coop_grid(fn, std::max<int64_t>(want, 1));
   const int NV = mode == kAdj ? 3 : 2;
   double *part = nullptr, *red = nullptr;
-  HSV_TRY(dalloc(&part, (int64_t)nb * grid * kBatch * NV));
+  // barrier version: [batch][block][rotation][NV]; barrier-free: [batch][warp][...]
+  HSV_TRY(dalloc(&part, (p2p ? std::max<int64_t>(P.n_chunks, 1) : (int64_t)nb * grid) * kBatch * NV));
+  if (p2p) {
+    if (!P.ver) HSV_TRY(dalloc(&P.ver, sec->dim));
+    HSV_TRY_CUDA(cudaMemsetAsync(P.ver, 0, sec->dim * sizeof(uint32_t), stream()));
+  }
   HSV_TRY(dalloc(&red, (int64_t)k * NV));
   HSV_TRY_CUDA(cudaMemsetAsync(red, 0, (int64_t)k * NV * sizeof(double), stream()));
   BSweepArgs a{};
@@ -805,6 +1101,10 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
   a.psi = psi; a.lam = lam; a.smap = nullptr; a.part = part; a.red = red;
   a.norm2 = norm2; a.grads = d_grads; a.err = err; a.err_val = err_val;
   a.stats = ctx().d_stats;
+  a.ver = P.ver;
+  a.rows = P.rows; a.masks = P.masks; a.ranks = P.ranks;
+  a.n_chunks = P.n_chunks; a.chunk_batch = P.chunk_batch; a.chunk_off = P.chunk_off;
+  a.chunk_order = mode == kFwd ? nullptr : P.chunk_rev;
   void* params[] = {&a};
   {
     ProfScope prof(mode == kFwd ? "qeb" : "adjoint");

@@ -64,7 +64,8 @@ def main():
                               "k1r_rows": st[2] // args.reps}), flush=True)
             for key, v in kv:   # back to defaults
                 N.call("hsv_set_tuning", key.encode(),
-                       {"sweep": 2, "restrict_rows": -1, "push": -1}.get(key, -1))
+                       {"sweep": 2, "restrict_rows": -1, "push": -1, "sweep_p2p": 0,
+                        "apply_v": 0}.get(key, -1))
 
 
 if __name__ == "__main__":
