@@ -267,6 +267,18 @@ HSV_API int hsv_eg_forward_peer_async(hsv_op op, uint64_t hf_key, const uint64_t
  * "rb0_smem" (1: Rb0 staged in shared memory, opt-in) ---- */
 HSV_API int hsv_set_tuning(const char* key, int64_t value);
 
+/* ---- device Hamiltonian build (mapping.py:79-126, pauli.py:165-198) ---- */
+/* Jordan-Wigner image of the spin-orbital tables h[n*n], g[n^4] (chemists'
+ * order, mapping.py:48-76) plus core_energy: the merged real Pauli sum with
+ * |c| > drop_tol, sorted by (x, z) -- the PauliSum hsv_op_create takes.  The
+ * products are expanded and summed on the device in the reference's order, so
+ * the coefficients are bit-identical to its dict accumulation.  n <= 32.
+ * Call with xs == NULL to get *n_out, then with capacity cap >= *n_out.
+ * HSV_ERR_NONREAL: residual imaginary coefficient > 1e-12 (not Hermitian). */
+HSV_API int hsv_jordan_wigner(int n_qubits, const double* h, const double* g, double core_energy,
+                              double drop_tol, int64_t* xs, int64_t* zs, double* coeffs,
+                              int64_t cap, int64_t* n_out);
+
 /* ---- Krylov basis blocks (FCI reference: thick-restart Lanczos, fci.py;
  * replaces scipy eigsh in oracle.py:99-142) ---- */
 /* c_j = <q_j|w> (complex, c_out[2j], c_out[2j+1]; c_out may be NULL) for the m

@@ -101,6 +101,8 @@ _SIGNATURES = {
     "hsv_eg_forward_peer_async": (C.c_int, [vp, C.c_uint64, P_u64, P_u64, P_dbl, P_dbl, i64,
                                             i64, i64, vp, vp, vp]),
     "hsv_set_tuning": (C.c_int, [C.c_char_p, i64]),
+    "hsv_jordan_wigner": (C.c_int, [C.c_int, P_dbl, P_dbl, dbl, dbl, P_i64, P_i64, P_dbl, i64,
+                                    P_i64]),
     "hsv_krylov_project": (C.c_int, [C.POINTER(vp), i64, vp, C.c_int, P_dbl]),
     "hsv_krylov_combine": (C.c_int, [C.POINTER(vp), i64, P_dbl, vp]),
     "hsv_prof_enable": (C.c_int, [C.c_int]),

@@ -218,6 +218,32 @@ def _jordan_wigner_tables(h: np.ndarray, g: np.ndarray, core_energy: float, n: i
     return PauliSum(n, keys[keep, 0], keys[keep, 1], acc.real[keep])
 
 
+def jordan_wigner_device(h, g=None, core_energy: float | None = None, n: int | None = None,
+                         drop_tol: float = JW_DROP_TOL) -> PauliSum:
+    """JW image built on the device (hsv_jordan_wigner, csrc/hsv_jw.cu): the products
+    are expanded and merged in the reference's order (mapping.py:79-126), so the
+    coefficients are bit-identical to its dict accumulation.  Same call forms as
+    `jordan_wigner`."""
+    from . import _native as N
+    if isinstance(h, SecondQuantizedHamiltonian):
+        if isinstance(g, float):
+            drop_tol, g = g, None
+        h, g, core_energy, n = h.h, h.g, h.core_energy, h.n_spin_orbitals
+    hh = np.ascontiguousarray(h, dtype=np.float64)
+    gg = np.ascontiguousarray(g, dtype=np.float64)
+    N.init()
+    cnt = N.i64()
+    N.call("hsv_jordan_wigner", int(n), N.ptr_f64(hh), N.ptr_f64(gg), float(core_energy),
+           float(drop_tol), None, None, None, 0, N.C.byref(cnt))
+    m = cnt.value
+    xs = np.empty(m, dtype=np.int64)
+    zs = np.empty(m, dtype=np.int64)
+    cs = np.empty(m)
+    N.call("hsv_jordan_wigner", int(n), N.ptr_f64(hh), N.ptr_f64(gg), float(core_energy),
+           float(drop_tol), N.ptr_i64(xs), N.ptr_i64(zs), N.ptr_f64(cs), m, N.C.byref(cnt))
+    return PauliSum(int(n), xs, zs, cs, _trusted=True)
+
+
 def molecular_system(ints: IntegralSet, ordering: str = "interleaved"):
     """MolecularSystem from integrals (mirrors MolecularSystem.from_integrals, system.py:33-37)."""
     from .system import IntegralInfo, MolecularSystem

@@ -553,6 +553,14 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
     HSV_TRY(launch_push(op, a, &done, n_warps, dense_hint));
     if (done) return HSV_OK;
   }
+  if (tuning().staged != 1) {   // K1t: alpha tiles (hsv_apply_t.cu)
+    bool done = false;
+    HSV_TRY(launch_apply_t(op, a, k1_default_split(op, a_lo, a_hi, out != nullptr), &done));
+    if (done) {
+      if (n_warps) *n_warps = 1;   // epart[0..1] holds the total
+      return HSV_OK;
+    }
+  }
   if (out && tuning().staged != 1) {   // K1v: valid beta lists (hsv_apply_v.cu)
     bool done = false;
     HSV_TRY(launch_apply_v(op, a, k1_default_split(op, a_lo, a_hi, true), &done));

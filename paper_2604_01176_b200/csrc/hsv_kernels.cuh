@@ -29,6 +29,11 @@ struct Tuning {
                           // 0/-1 off (default: measured 1-3% slower at H12/H14)
   int restrict_rows = -1; // K1r in the adjoint evaluation (w = H psi on the structural
                           // support of psi only): -1/1 on, 0 off (full K1 / push)
+  int apply_t = 0;        // K1t (alpha tiles: 8 alpha rows x 1 beta string per lane,
+                          // hsv_apply_t.cu): 1 on, 0/-1 off.  Bitwise equal to K1 but
+                          // measured 2.2x slower at H12 (5.21 vs 2.39 ms): 1.88e9 vs 1.25e9
+                          // warp instructions (per-row predication of the alpha mask) and
+                          // L1 hit 66 vs 78% (a lane gathers from 8 partner alpha rows)
   int apply_v = 0;        // K1v (per-group valid beta lists, shared-memory row accumulators):
                           // 1 on where built, 0/-1 off.  Bitwise equal to K1 but measured
                           // 2.4x slower at H12 (5.80 vs 2.40 ms): the per-group chain (record
@@ -165,6 +170,8 @@ int apply_warps(const hsv_op_s* op);
 // dense_hint (optional, per state): skip when set, set when psi is found dense.
 int launch_push(const hsv_op_s* op, const ApplyArgs& a, bool* done, int64_t* n_warps,
                 bool* dense_hint);
+// K1t (hsv_apply_t.cu): *done = false when not selected (tuning apply_t) or wide words.
+int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a, int S, bool* done);
 // K1v (hsv_apply_v.cu): *done = false when the operator has no valid lists.
 // S = the bucket split count the register-row K1 would use (same row values).
 int launch_apply_v(const hsv_op_s* op, const ApplyArgs& a, int S, bool* done);

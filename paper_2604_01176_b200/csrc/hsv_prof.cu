@@ -77,6 +77,9 @@ int hsv_set_tuning(const char* key, int64_t value) {
   } else if (k == "rb0_smem") {
     HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "rb0_smem must be -1, 0 or 1");
     g_tuning.rb0_smem = (int)value;
+  } else if (k == "apply_t") {
+    HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "apply_t must be -1, 0 or 1");
+    g_tuning.apply_t = (int)value;
   } else if (k == "apply_v") {
     HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "apply_v must be -1, 0 or 1");
     g_tuning.apply_v = (int)value;

@@ -1081,8 +1081,12 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
                                stream()));
   const void* fn = p2p ? (mode == kFwd ? (const void*)k_psweep<kFwd> : (const void*)k_psweep<kAdj>)
                        : (mode == kFwd ? (const void*)k_bsweep<kFwd> : (const void*)k_bsweep<kAdj>);
+  // barrier version: one block per SM at most -- a cheaper grid barrier beats more
+  // resident warps (H12 depth 400: 0.67 vs 0.89 ms forward, 0.84 vs 0.98 adjoint;
+  // equal at depth 100/200, profiles/r02/sweep_probe_grid.txt)
   const int64_t want = tuning().sweep_grid > 0 ? tuning().sweep_grid
-                       : p2p ? (int64_t)ctx().num_sms * 2 : (P.max_live + 255) / 256;
+                       : p2p ? (int64_t)ctx().num_sms * 2
+                             : std::min<int64_t>(ctx().num_sms, (P.max_live + 255) / 256);
   const int grid = coop_grid(fn, std::max<int64_t>(want, 1));
   const int NV = mode == kAdj ? 3 : 2;
   double *part = nullptr, *red = nullptr;
