@@ -7,8 +7,11 @@
 // same sequential sum the reference forms per x-group (svengine.py:137-146),
 // so every matrix element is bit-identical to the reference CSR value.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <numeric>
 
 #include <cub/cub.cuh>
@@ -56,14 +59,22 @@ template <typename W, int SH>
 __global__ void k_diag(const uint32_t* __restrict__ Sa, const uint32_t* __restrict__ Sb,
                        int64_t Na, int64_t Nb, const Term* __restrict__ terms, int t0, int t1,
                        double* __restrict__ diag) {
+  // the diagonal terms staged in shared memory (H16: 529 terms, 8.5 KB); the
+  // sum stays sequential in term order (svengine.py:137-146)
+  extern __shared__ Term tsh[];
+  const int nt = t1 - t0;
+  for (int i = threadIdx.x; i < nt; i += blockDim.x) tsh[i] = terms[t0 + i];
+  __syncthreads();
   const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (idx >= Na * Nb) return;
   const int64_t ra = idx / Nb, rb = idx - ra * Nb;
   const W s = (W)Sa[ra] | ((W)Sb[rb] << SH);
   double amp = 0.0;
-  for (int t = t0; t < t1; ++t) {
-    const Term T = terms[t];
-    amp += (popc(s & (W)T.z) & 1) ? -T.c : T.c;
+#pragma unroll 4
+  for (int t = 0; t < nt; ++t) {
+    const Term T = tsh[t];
+    const int sgn = popc(s & (W)T.z) << 31;   // exact +-c: flip the sign bit
+    amp += __hiloint2double(__double2hiint(T.c) ^ sgn, __double2loint(T.c));
   }
   diag[idx] = amp;
 }
@@ -847,6 +858,17 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
   HSV_REQUIRE(n_qubits == s->n_qubits, HSV_ERR_INVALID,
               "Pauli sum and basis disagree on qubit count");
   const int SH = s->wide ? 32 : 16;
+  // HSV_TIMING=1: host wall time of each setup phase on stderr
+  static const bool timing = getenv("HSV_TIMING") && getenv("HSV_TIMING")[0] == '1';
+  auto t_last = std::chrono::steady_clock::now();
+  auto op_phase = [&](const char* name) {
+    if (!timing) return;
+    cudaStreamSynchronize(stream());
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "hsv_op_create %-14s %8.2f ms\n", name,
+            std::chrono::duration<double, std::milli>(now - t_last).count());
+    t_last = now;
+  };
   const uint64_t qmask = n_qubits >= 64 ? ~0ull : ((1ull << n_qubits) - 1);
   for (int64_t t = 0; t < n_terms; ++t)
     HSV_REQUIRE(((uint64_t)xs[t] & ~qmask) == 0 && ((uint64_t)zs[t] & ~qmask) == 0,
@@ -901,6 +923,7 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
   int rc = HSV_OK;
   auto fail = [&](int code) { hsv_op_destroy(op); return code; };
 
+  op_phase("grouping");
   // ---- device validation: sector leak per off-diagonal group ----
   Term* d_all = nullptr;
   if ((rc = dalloc(&d_all, all_terms.size()))) return fail(rc);
@@ -927,9 +950,65 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
     const uint64_t xp = (uint64_t)g.xa | ((uint64_t)g.xb << SH);
     const uint64_t z0 = all_terms[g.t0].z;
     bool local = true;
-    for (int t = g.t0; t < g.t1 && local; ++t) local = ((all_terms[t].z ^ z0) & ~xp) == 0;
-    if (!local || __builtin_popcountll(xp) > 16) {
+    for (int t = g.t0; t < g.t1; ++t) local = local && ((all_terms[t].z ^ z0) & ~xp) == 0;
+    // single-Z form: a reference term zr (the one without an extra number-operator
+    // Z) every term differs from by <= 1 bit off the flip mask
+    uint64_t zr = z0;
+    bool single_z = false;
+    if (!local)
+      for (int r = g.t0; r < g.t1 && !single_z; ++r) {
+        bool fits = true;
+        for (int t = g.t0; t < g.t1 && fits; ++t)
+          fits = __builtin_popcountll((all_terms[t].z ^ all_terms[r].z) & ~xp) <= 1;
+        if (fits) { zr = all_terms[r].z; single_z = true; }
+      }
+    if (__builtin_popcountll(xp) > 16 || !(local || single_z)) {
       on_dev.push_back(j);
+      continue;
+    }
+    if (!local) {
+      // single-Z group (a single excitation with its number-operator Z's): per
+      // out-of-sector pattern p of b on x, amp(b) = +-(C0 + sum_r C_r (-1)^{b_r})
+      // (terms grouped by their one extra Z bit r), so |amp| <= |C0| + sum |C_r|,
+      // and the reference's sequential sum adds at most gamma * sum |c_t| of
+      // rounding.  A group whose bound is below the tolerance cannot leak; any
+      // other goes to the exact per-row device check.
+      double worst = 0.0, abs_sum = 0.0;
+      const int nt = g.t1 - g.t0;
+      for (int t = g.t0; t < g.t1; ++t) abs_sum += std::fabs(all_terms[t].c);
+      const double eps = std::numeric_limits<double>::epsilon();
+      const double gamma = nt * eps / (1.0 - nt * eps);
+      const uint64_t amask = (SH == 16 ? 0xffffull : 0xffffffffull);
+      std::vector<std::pair<uint64_t, double>> cr;
+      for (uint64_t p = xp;; p = (p - 1) & xp) {
+        const int na_p = __builtin_popcountll(p & amask), nb_p = __builtin_popcountll(p >> SH);
+        const bool real_a = s->n_alpha - na_p >= 0 && s->n_alpha - na_p <= s->norb - g.pa;
+        const bool real_b = s->n_beta - nb_p >= 0 && s->n_beta - nb_p <= s->norb - g.pb;
+        const bool stays = 2 * na_p == g.pa && 2 * nb_p == g.pb;
+        if (real_a && real_b && !stays) {
+          double c0 = 0.0;
+          cr.clear();
+          for (int t = g.t0; t < g.t1; ++t) {
+            const Term& T = all_terms[t];
+            const double c = (__builtin_popcountll(p & (T.z ^ zr) & xp) & 1) ? -T.c : T.c;
+            const uint64_t out = (T.z ^ zr) & ~xp;
+            if (!out) { c0 += c; continue; }
+            bool found = false;
+            for (auto& e : cr)
+              if (e.first == out) { e.second += c; found = true; break; }
+            if (!found) cr.push_back({out, c});
+          }
+          double bound = std::fabs(c0);
+          for (const auto& e : cr) bound += std::fabs(e.second);
+          worst = std::max(worst, bound + 2.0 * gamma * abs_sum);
+        }
+        if (p == 0) break;
+      }
+      if (worst > kSectorLeakTol) {   // possibly leaking: exact device check
+        on_dev.push_back(j);
+        continue;
+      }
+      memcpy(&leak[j], &worst, 8);   // a bound below the tolerance
       continue;
     }
     double worst = 0.0;
@@ -951,6 +1030,8 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
     }
     memcpy(&leak[j], &worst, 8);
   }
+  if (timing) fprintf(stderr, "hsv_op_create leak: %d of %d groups on the device\n",
+                      (int)on_dev.size(), n_off);
   if (!on_dev.empty() && s->dim > 0) {
     const int n_dev = (int)on_dev.size();
     std::vector<uint32_t> gxa(n_dev), gxb(n_dev);
@@ -1019,20 +1100,29 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
       }
     }
   }
+  op_phase("leak");
   // ---- diagonal table ----
   for (const HGroup& g : hg) {
     if (g.x != 0 || s->dim == 0) continue;
     if ((rc = dalloc(&op->d_diag, s->dim))) return fail(rc);
     const unsigned nb = (unsigned)((s->dim + 255) / 256);
+    const size_t tsm = (size_t)(g.t1 - g.t0) * sizeof(Term);
+    if (tsm > 48 * 1024) {
+      HSV_TRY_CUDA(cudaFuncSetAttribute(k_diag<uint64_t, 32>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+      HSV_TRY_CUDA(cudaFuncSetAttribute(k_diag<uint32_t, 16>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsm));
+    }
     if (s->wide)
-      k_diag<uint64_t, 32><<<nb, 256, 0, stream()>>>(s->d_Sa, s->d_Sb, s->Na, s->Nb, d_all,
-                                                     g.t0, g.t1, op->d_diag);
+      k_diag<uint64_t, 32><<<nb, 256, tsm, stream()>>>(s->d_Sa, s->d_Sb, s->Na, s->Nb, d_all,
+                                                       g.t0, g.t1, op->d_diag);
     else
-      k_diag<uint32_t, 16><<<nb, 256, 0, stream()>>>(s->d_Sa, s->d_Sb, s->Na, s->Nb, d_all,
-                                                     g.t0, g.t1, op->d_diag);
+      k_diag<uint32_t, 16><<<nb, 256, tsm, stream()>>>(s->d_Sa, s->d_Sb, s->Na, s->Nb, d_all,
+                                                       g.t0, g.t1, op->d_diag);
     count_launch();
     HSV_CHECK_LAUNCH();
   }
+  op_phase("diag");
   // ---- active groups, bucketed by alpha flip part ----
   std::vector<int> act;
   for (int g = 0; g < (int)hg.size(); ++g)
@@ -1051,6 +1141,7 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
   }
   op->n_active = (int64_t)act.size();
   op->n_buckets = (int64_t)op->buckets.size();
+  op_phase("buckets");
   // ---- pattern tables for x-local groups ----
   std::vector<GroupHash> ghash(op->groups.size());
   std::vector<double> tabs;
@@ -1204,6 +1295,7 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
       cuts.push_back(T.nb);
     }
   }
+  op_phase("tables+splits");
   std::vector<unsigned char> recs;
   // K1 pass-1 beta rank permutations: for each distinct beta flip xb of a hashed
   // group, bperm[slot + rb] = rank(Sb[rb] ^ xb) (0 out of sector, as Rb0), rows
@@ -1241,7 +1333,7 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
   std::vector<uint32_t> vslot(ghash.size(), 0u);
   const int vchunk = 1024;
   const int vnch = (int)((s->Nb + vchunk - 1) / vchunk);
-  if (SH == 16 && s->Nb <= 65535) {
+  if (SH == 16 && s->Nb <= 65535 && tuning().apply_v == 1) {   // only for the opt-in K1v
     std::vector<uint32_t> xbs;
     for (size_t q = 0; q < ghash.size(); ++q)
       if (ghash[q].tab >= 0) xbs.push_back((uint32_t)op->groups[q].x);
@@ -1289,6 +1381,7 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
       memcpy(&recs[q * 48 + 16], r2, 32);
     }
   }
+  op_phase("bperm+recs");
   if ((rc = dalloc(&op->d_buckets, op->buckets.size())) ||
       (rc = dalloc(&op->d_groups, op->groups.size())) ||
       (rc = dalloc(&op->d_terms, op->terms.size())) ||
@@ -1345,6 +1438,7 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
     HSV_TRY_CUDA(cudaMemcpyAsync(op->d_terms, op->terms.data(), op->terms.size() * sizeof(Term),
                                  cudaMemcpyHostToDevice, st));
   if ((rc = stream_sync())) return fail(rc);
+  op_phase("upload");
   dfree(d_all);
   *out = op;
   return HSV_OK;

@@ -22,6 +22,9 @@ def hsv():
 @pytest.fixture()
 def N():
     from paper_2604_01176_b200 import _native as N
+    # the valid lists are built at operator creation only while K1v is enabled:
+    # every operator of these tests is created after this point
+    N.call("hsv_set_tuning", b"apply_v", 1)
     yield N
     for k in (b"apply_v", b"apply_split", b"push", b"restrict_rows"):
         N.call("hsv_set_tuning", k, {b"apply_split": 0, b"apply_v": 0}.get(k, -1))

@@ -236,6 +236,23 @@ def test_errors(hsv):
         hsv.SvState.from_configuration(basis, 0b0101)   # two alpha electrons
 
 
+def test_leak_checks_host_and_device_paths(hsv):
+    """Sector-leak validation (svengine.py:153-160) through both checkers: an
+    x-local group (host, per pattern), a single-Z group with a leak (its bound
+    exceeds the tolerance -> exact per-row device check), and a conserving
+    single-Z group (bound below tolerance -> accepted)."""
+    basis = hsv.enumerate_basis(6, 1, 1)             # 3 alpha, 3 beta orbitals
+    # x = alpha orbitals 0 and 1 (qubits 0, 2), with and without an extra Z on qubit 1
+    leaky = hsv.PauliSum.from_strings([(1.0, "XIXIII"), (0.5, "XZXIII")])
+    with pytest.raises(ValueError, match="not spin-conserving"):
+        hsv.assemble_subspace_hamiltonian(leaky, basis)
+    # XX + YY with equal coefficients (a number-conserving hop) and the same extra Z
+    ok = hsv.PauliSum.from_strings([(0.25, "XIXIII"), (0.25, "YIYIII"), (0.125, "XZXIII"),
+                                    (0.125, "YZYIII")])
+    m = hsv.assemble_subspace_hamiltonian(ok, basis)
+    assert m.nnz > 0
+
+
 def test_identity_and_z_terms(hsv):
     basis = hsv.enumerate_basis(4, 1, 1)
     m = hsv.assemble_subspace_hamiltonian(hsv.PauliSum.from_strings([(2.5, "IIII")]), basis)
