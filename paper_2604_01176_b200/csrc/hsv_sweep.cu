@@ -376,12 +376,10 @@ __device__ __forceinline__ void norm_chain(const BSweepArgs& a) {
 // One live orbit of a batch: forward rotations (MODE kFwd) or, in reverse
 // order, gradient partial + adjoint rotation + uncompute (kAdj).
 template <int MODE>
-__device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B, int64_t it,
-                                         double (&acc)[kBatch][3], unsigned& npairs) {
-  const unsigned m = __ldg(B.masks + it);
+__device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B, unsigned m,
+                                         uint4 r0, uint4 r1, double (&acc)[kBatch][3],
+                                         unsigned& npairs) {
   const unsigned touched = m & 0xffu;
-  const uint4* rp = reinterpret_cast<const uint4*>(B.rows + it * kOrb);
-  const uint4 r0 = __ldg(rp), r1 = __ldg(rp + 1);
   const uint32_t row[kOrb] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
   double2 v[kOrb];
   double2 l[kOrb];
@@ -451,18 +449,37 @@ __device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B,
   }
 }
 
+// An orbit's plan record (masks + 8 rows): loaded before the grid barrier that
+// precedes its batch -- it does not depend on amplitudes -- so after the
+// barrier only the amplitude loads remain on the critical path.
+struct OrbitRec {
+  unsigned m;
+  uint4 r0, r1;
+};
+__device__ __forceinline__ OrbitRec load_orbit(const BatchDev& B, int64_t it) {
+  OrbitRec o;
+  o.m = __ldg(B.masks + it);
+  const uint4* rp = reinterpret_cast<const uint4*>(B.rows + it * kOrb);
+  o.r0 = __ldg(rp);
+  o.r1 = __ldg(rp + 1);
+  return o;
+}
+
 template <int MODE>
-__global__ void __launch_bounds__(256, MODE == kFwd ? 3 : 2) k_bsweep(const BSweepArgs a) {
+__global__ void __launch_bounds__(256, 1) k_bsweep(const BSweepArgs a) {   // one block per SM (launch_bsweep)
   constexpr int NV = MODE == kAdj ? 3 : 2;
-  __shared__ double sh[8][kBatch][NV];
   // batch descriptors staged in shared memory kBChunk at a time by the whole
   // block: no serial descriptor load between a grid barrier and the next batch
   __shared__ __align__(16) BatchDev sB[kBChunk];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
   const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t nt = (int64_t)gridDim.x * blockDim.x;
+  const int64_t gw = gt >> 5, nw = nt >> 5;
+  OrbitRec next{};
+  bool have_next = false;
   for (int bi = 0; bi < a.n_batches; ++bi) {
     if (bi % kBChunk == 0) {
+      __syncthreads();
       const int n = min(kBChunk, a.n_batches - bi);
       constexpr int W4 = sizeof(BatchDev) / 16;
       const uint4* src = reinterpret_cast<const uint4*>(a.batches + bi);
@@ -476,41 +493,48 @@ __global__ void __launch_bounds__(256, MODE == kFwd ? 3 : 2) k_bsweep(const BSwe
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) acc[j][0] = acc[j][1] = acc[j][2] = 0.0;
     unsigned npairs = 0u;
-    for (int64_t it = gt; it < n_items; it += nt) do_orbit<MODE>(a, B, it, acc, npairs);
+    for (int64_t it = gt; it < n_items; it += nt) {
+      const OrbitRec o = (it == gt && have_next) ? next : load_orbit(B, it);
+      do_orbit<MODE>(a, B, o.m, o.r0, o.r1, acc, npairs);
+    }
     if (a.stats) {
       const unsigned tot = __reduce_add_sync(0xffffffffu, npairs);
       if (lane == 0 && tot) atomicAdd(a.stats + (MODE == kFwd ? kStatPairsFwd : kStatPairsAdj),
                                       (unsigned long long)tot);
     }
-    // block partials per rotation (fixed shuffle tree and warp order)
+    // warp partials per rotation (fixed shuffle tree; no block barrier)
+    if (gw * 32 < (int64_t)n_items) {
 #pragma unroll
-    for (int j = 0; j < kBatch; ++j)
+      for (int j = 0; j < kBatch; ++j)
 #pragma unroll
-      for (int q = 0; q < NV; ++q) {
-        const double x = warp_sum(acc[j][q]);
-        if (lane == 0) sh[w][j][q] = x;
-      }
-    __syncthreads();
-    if (threadIdx.x < kBatch * NV) {
-      const int j = threadIdx.x / NV, q = threadIdx.x - j * NV;
-      double x = 0.0;
-      for (int k = 0; k < 8; ++k) x += sh[k][j][q];
-      a.part[(((int64_t)bi * gridDim.x + blockIdx.x) * kBatch + j) * NV + q] = x;
+        for (int q = 0; q < NV; ++q) {
+          const double x = warp_sum(acc[j][q]);
+          if (lane == 0) a.part[(((int64_t)bi * nw + gw) * kBatch + j) * NV + q] = x;
+        }
     }
-    __syncthreads();
+    // prefetch this thread's first orbit of the next batch
+    have_next = false;
+    if (bi + 1 < a.n_batches) {
+      const BatchDev& Bn = ((bi + 1) % kBChunk) ? sB[(bi + 1) % kBChunk] : a.batches[bi + 1];
+      if (gt < (int64_t)Bn.count) {
+        next = load_orbit(Bn, gt);
+        have_next = true;
+      }
+    }
     grid_sync();   // batch bi+1 reads rows batch bi wrote
   }
-  // per-rotation totals: one rotation per warp, blocks summed in a fixed order
-  const int64_t gw = gt >> 5, nw = nt >> 5;
+  // per-rotation totals: one rotation per warp, warps summed in a fixed order
+  // (warps whose first orbit index is past the batch wrote nothing: skipped)
   for (int64_t oi = gw; oi < (int64_t)a.n_batches * kBatch; oi += nw) {
     const int bi = (int)(oi / kBatch), j = (int)(oi - (int64_t)bi * kBatch);
     const BatchDev& B = a.batches[bi];
     if (j >= B.n) continue;
+    const int64_t used = min((int64_t)nw, ((int64_t)B.count + 31) / 32);
 #pragma unroll
     for (int q = 0; q < NV; ++q) {
       double x = 0.0;
-      for (int k = lane; k < (int)gridDim.x; k += 32)
-        x += __ldcg(a.part + (((int64_t)bi * gridDim.x + k) * kBatch + j) * NV + q);
+      for (int64_t k = lane; k < used; k += 32)
+        x += __ldcg(a.part + (((int64_t)bi * nw + k) * kBatch + j) * NV + q);
       x = warp_sum(x);
       if (lane == 0) a.red[(int64_t)(B.op0 + j) * NV + q] = x;
     }
@@ -1091,7 +1115,8 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
   const int NV = mode == kAdj ? 3 : 2;
   double *part = nullptr, *red = nullptr;
   // barrier version: [batch][block][rotation][NV]; barrier-free: [batch][warp][...]
-  HSV_TRY(dalloc(&part, (p2p ? std::max<int64_t>(P.n_chunks, 1) : (int64_t)nb * grid) * kBatch * NV));
+  HSV_TRY(dalloc(&part, (p2p ? std::max<int64_t>(P.n_chunks, 1) : (int64_t)nb * grid * 8) *
+                            kBatch * NV));
   if (p2p) {
     if (!P.ver) HSV_TRY(dalloc(&P.ver, sec->dim));
     HSV_TRY_CUDA(cudaMemsetAsync(P.ver, 0, sec->dim * sizeof(uint32_t), stream()));
