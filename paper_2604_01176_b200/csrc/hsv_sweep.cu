@@ -39,14 +39,23 @@ namespace hsv {
 
 namespace {
 
-constexpr int kBatch = 3;               // rotations per batch (orbits of 2^kBatch rows)
+constexpr int kBatch = 3;   // rotations per batch (orbits of 2^kBatch rows); 4 measured slower (H12 depth 400: 0.79 vs 0.60 ms forward)
 constexpr int kOrb = 1 << kBatch;
+constexpr int kRW = kOrb / 4;           // uint4 words of an orbit's rows
+static_assert(kBatch <= 7 && kOrb <= 16, "orbit masks are 16-bit fields of one uint4");
+
+// 16-bit field f of an orbit's masks: f = 0 touched elements, f = j + 1 the
+// elements that are sources of rotation j
+__host__ __device__ __forceinline__ unsigned mfield(const uint4& mk, int f) {
+  const unsigned w = f < 2 ? mk.x : f < 4 ? mk.y : f < 6 ? mk.z : mk.w;
+  return (f & 1) ? (w >> 16) : (w & 0xffffu);
+}
 enum { kFwd = 0, kAdj = 1 };
 
 struct __align__(16) BatchDev {
   double c[kBatch], s[kBatch];
   const uint32_t* rows;  // live orbits: kOrb rows each (plan)
-  const uint32_t* masks; // live orbits: touched | srcm_j << 8 (j + 1)
+  const uint4* masks;    // live orbits: 16-bit fields touched, srcm_0 .. (mfield)
   const uint32_t* ranks; // live orbits: per element, write rank | row writers << 16
   int n;                 // rotations in the batch
   int op0;               // index (in sweep-list order) of the batch's first rotation
@@ -76,7 +85,7 @@ struct BSweepArgs {
   uint32_t* ver;               // barrier-free sweep: writes completed per row (zeroed)
   // barrier-free sweep: the plan's global (padded) orbit arrays, chunk maps
   const uint32_t* rows;
-  const uint32_t* masks;
+  const uint4* masks;
   const uint32_t* ranks;
   int64_t n_chunks;
   const int* chunk_batch;       // physical chunk -> batch (plan order)
@@ -284,7 +293,7 @@ struct GatherArgs {
   const uint32_t* Ra;
   const uint32_t* Rb;
   uint32_t* rows;
-  uint32_t* masks;
+  uint4* masks;
   const uint16_t* wrank;
   const uint32_t* wcount;
   uint32_t* ranks;        // per live orbit element: rank | (writers of the row) << 16
@@ -308,13 +317,15 @@ __global__ void k_plan_gather(const GatherArgs a) {
              touched, srcm);
   const int64_t si = i;   // compact index (selection order)
   const int64_t pi = a.loff_pad[lo] + (si - a.loff_cmp[lo]);   // padded slot
-  unsigned m = touched;
+  unsigned f[8] = {touched, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 #pragma unroll
-  for (int j = 0; j < kBatch; ++j) m |= srcm[j] << (8 * (j + 1));
-  a.masks[pi] = m;
+  for (int j = 0; j < kBatch; ++j) f[j + 1] = srcm[j];
+  a.masks[pi] = make_uint4(f[0] | f[1] << 16, f[2] | f[3] << 16, f[4] | f[5] << 16,
+                           f[6] | f[7] << 16);
   uint4* r = reinterpret_cast<uint4*>(a.rows + pi * kOrb);
-  r[0] = make_uint4(row[0], row[1], row[2], row[3]);
-  r[1] = make_uint4(row[4], row[5], row[6], row[7]);
+#pragma unroll
+  for (int q = 0; q < kRW; ++q)
+    r[q] = make_uint4(row[4 * q], row[4 * q + 1], row[4 * q + 2], row[4 * q + 3]);
   if (a.ranks) {
     uint32_t k[kOrb];
 #pragma unroll
@@ -323,8 +334,8 @@ __global__ void k_plan_gather(const GatherArgs a) {
                  ? (uint32_t)a.wrank[g * kOrb + t] | (min(a.wcount[row[t]], 65535u) << 16)
                  : 0u;
     uint4* kr = reinterpret_cast<uint4*>(a.ranks + pi * kOrb);
-    kr[0] = make_uint4(k[0], k[1], k[2], k[3]);
-    kr[1] = make_uint4(k[4], k[5], k[6], k[7]);
+#pragma unroll
+    for (int q = 0; q < kRW; ++q) kr[q] = make_uint4(k[4 * q], k[4 * q + 1], k[4 * q + 2], k[4 * q + 3]);
   }
 }
 
@@ -375,12 +386,21 @@ __device__ __forceinline__ void norm_chain(const BSweepArgs& a) {
 
 // One live orbit of a batch: forward rotations (MODE kFwd) or, in reverse
 // order, gradient partial + adjoint rotation + uncompute (kAdj).
+struct OrbitRec {
+  uint4 mk;
+  uint4 r[kRW];
+};
+
 template <int MODE>
-__device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B, unsigned m,
-                                         uint4 r0, uint4 r1, double (&acc)[kBatch][3],
-                                         unsigned& npairs) {
-  const unsigned touched = m & 0xffu;
-  const uint32_t row[kOrb] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
+__device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B, const OrbitRec& o,
+                                         double (&acc)[kBatch][3], unsigned& npairs) {
+  const unsigned touched = mfield(o.mk, 0);
+  uint32_t row[kOrb];
+#pragma unroll
+  for (int q = 0; q < kRW; ++q) {
+    row[4 * q] = o.r[q].x; row[4 * q + 1] = o.r[q].y;
+    row[4 * q + 2] = o.r[q].z; row[4 * q + 3] = o.r[q].w;
+  }
   double2 v[kOrb];
   double2 l[kOrb];
 #pragma unroll
@@ -395,7 +415,7 @@ __device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B,
   if (MODE == kFwd) {
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
-      const unsigned sj = (m >> (8 * (j + 1))) & 0xffu;
+      const unsigned sj = mfield(o.mk, j + 1);
       npairs += __popc(sj);
       if (j >= B.n || (B.c[j] == 1.0 && B.s[j] == 0.0)) continue;   // theta == 0: identity
 #pragma unroll
@@ -417,7 +437,7 @@ __device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B,
 #pragma unroll
     for (int jj = kBatch - 1; jj >= 0; --jj) {
       if (jj >= B.n) continue;
-      const unsigned sj = (m >> (8 * (jj + 1))) & 0xffu;
+      const unsigned sj = mfield(o.mk, jj + 1);
       npairs += __popc(sj);
       const bool unc = B.op0 + jj > 0;   // psi of the first rotation is never read again
 #pragma unroll
@@ -452,16 +472,12 @@ __device__ __forceinline__ void do_orbit(const BSweepArgs& a, const BatchDev& B,
 // An orbit's plan record (masks + 8 rows): loaded before the grid barrier that
 // precedes its batch -- it does not depend on amplitudes -- so after the
 // barrier only the amplitude loads remain on the critical path.
-struct OrbitRec {
-  unsigned m;
-  uint4 r0, r1;
-};
 __device__ __forceinline__ OrbitRec load_orbit(const BatchDev& B, int64_t it) {
   OrbitRec o;
-  o.m = __ldg(B.masks + it);
+  o.mk = __ldg(B.masks + it);
   const uint4* rp = reinterpret_cast<const uint4*>(B.rows + it * kOrb);
-  o.r0 = __ldg(rp);
-  o.r1 = __ldg(rp + 1);
+#pragma unroll
+  for (int q = 0; q < kRW; ++q) o.r[q] = __ldg(rp + q);
   return o;
 }
 
@@ -495,7 +511,7 @@ __global__ void __launch_bounds__(256, 1) k_bsweep(const BSweepArgs a) {   // on
     unsigned npairs = 0u;
     for (int64_t it = gt; it < n_items; it += nt) {
       const OrbitRec o = (it == gt && have_next) ? next : load_orbit(B, it);
-      do_orbit<MODE>(a, B, o.m, o.r0, o.r1, acc, npairs);
+      do_orbit<MODE>(a, B, o, acc, npairs);
     }
     if (a.stats) {
       const unsigned tot = __reduce_add_sync(0xffffffffu, npairs);
@@ -567,15 +583,18 @@ template <int MODE>
 __device__ __forceinline__ void do_orbit_p2p(const BSweepArgs& a, const BatchDev& B, int64_t it,
                                              double (&acc)[kBatch][3], unsigned& npairs) {
   // it: global (padded) orbit index of the plan; padding orbits have masks 0
-  const unsigned m = __ldg(a.masks + it);
-  const unsigned touched = m & 0xffu;
+  const uint4 mk = __ldg(a.masks + it);
+  const unsigned touched = mfield(mk, 0);
   if (!touched) return;
+  uint32_t row[kOrb], rk[kOrb];
   const uint4* rp = reinterpret_cast<const uint4*>(a.rows + it * kOrb);
-  const uint4 r0 = __ldg(rp), r1 = __ldg(rp + 1);
-  const uint32_t row[kOrb] = {r0.x, r0.y, r0.z, r0.w, r1.x, r1.y, r1.z, r1.w};
   const uint4* kp = reinterpret_cast<const uint4*>(a.ranks + it * kOrb);
-  const uint4 k0 = __ldg(kp), k1 = __ldg(kp + 1);
-  const uint32_t rk[kOrb] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
+#pragma unroll
+  for (int q = 0; q < kRW; ++q) {
+    const uint4 r = __ldg(rp + q), k = __ldg(kp + q);
+    row[4 * q] = r.x; row[4 * q + 1] = r.y; row[4 * q + 2] = r.z; row[4 * q + 3] = r.w;
+    rk[4 * q] = k.x; rk[4 * q + 1] = k.y; rk[4 * q + 2] = k.z; rk[4 * q + 3] = k.w;
+  }
   uint32_t need[kOrb];
 #pragma unroll
   for (int t = 0; t < kOrb; ++t) {
@@ -605,7 +624,7 @@ __device__ __forceinline__ void do_orbit_p2p(const BSweepArgs& a, const BatchDev
   if (MODE == kFwd) {
 #pragma unroll
     for (int j = 0; j < kBatch; ++j) {
-      const unsigned sj = (m >> (8 * (j + 1))) & 0xffu;
+      const unsigned sj = mfield(mk, j + 1);
       npairs += __popc(sj);
       if (j >= B.n || (B.c[j] == 1.0 && B.s[j] == 0.0)) continue;
 #pragma unroll
@@ -627,7 +646,7 @@ __device__ __forceinline__ void do_orbit_p2p(const BSweepArgs& a, const BatchDev
 #pragma unroll
     for (int jj = kBatch - 1; jj >= 0; --jj) {
       if (jj >= B.n) continue;
-      const unsigned sj = (m >> (8 * (jj + 1))) & 0xffu;
+      const unsigned sj = mfield(mk, jj + 1);
       npairs += __popc(sj);
       const bool unc = B.op0 + jj > 0;
 #pragma unroll
@@ -663,7 +682,7 @@ __device__ __forceinline__ void do_orbit_p2p(const BSweepArgs& a, const BatchDev
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256, 2) k_psweep(const BSweepArgs a) {
+__global__ void __launch_bounds__(256, 1) k_psweep(const BSweepArgs a) {
   constexpr int NV = MODE == kAdj ? 3 : 2;
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -732,7 +751,7 @@ struct Plan {
   bool filtered = false;
   uint8_t* smap = nullptr;
   uint32_t* rows = nullptr;
-  uint32_t* masks = nullptr;
+  uint4* masks = nullptr;
   uint32_t* ranks = nullptr;   // barrier-free sweep: per element write rank | writers << 16
   uint32_t* ver = nullptr;     // per-row versions (dim), zeroed before each barrier-free sweep
   int* chunk_batch = nullptr;  // physical 32-orbit chunk -> batch
@@ -744,7 +763,8 @@ struct Plan {
   void drop_live() {
     dfree(rows); dfree(masks); dfree(ranks);
     dfree(chunk_batch); dfree(chunk_rev); dfree(chunk_off);
-    rows = masks = ranks = chunk_rev = nullptr;
+    rows = ranks = chunk_rev = nullptr;
+    masks = nullptr;
     chunk_batch = nullptr;
     chunk_off = nullptr;
     n_chunks = 0;
@@ -960,7 +980,7 @@ int filter_plan(Plan& P) {
   const int64_t n_slots = P.live_off[nb];
   HSV_TRY(dalloc(&P.rows, std::max<int64_t>(n_slots, 1) * kOrb));
   HSV_TRY(dalloc(&P.masks, std::max<int64_t>(n_slots, 1)));
-  HSV_TRY_CUDA(cudaMemsetAsync(P.masks, 0, std::max<int64_t>(n_slots, 1) * sizeof(uint32_t),
+  HSV_TRY_CUDA(cudaMemsetAsync(P.masks, 0, std::max<int64_t>(n_slots, 1) * sizeof(uint4),
                                stream()));
   if (ranks) HSV_TRY(dalloc(&P.ranks, std::max<int64_t>(n_slots, 1) * kOrb));
   // chunk maps of the barrier-free sweep
@@ -1109,7 +1129,7 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
   // resident warps (H12 depth 400: 0.67 vs 0.89 ms forward, 0.84 vs 0.98 adjoint;
   // equal at depth 100/200, profiles/r02/sweep_probe_grid.txt)
   const int64_t want = tuning().sweep_grid > 0 ? tuning().sweep_grid
-                       : p2p ? (int64_t)ctx().num_sms * 2
+                       : p2p ? (int64_t)ctx().num_sms
                              : std::min<int64_t>(ctx().num_sms, (P.max_live + 255) / 256);
   const int grid = coop_grid(fn, std::max<int64_t>(want, 1));
   const int NV = mode == kAdj ? 3 : 2;
