@@ -1366,7 +1366,7 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
       uint32_t r[8] = {(uint32_t)op->groups[q].x,
                        (uint32_t)op->groups[q].y | ((uint32_t)h.shift << 8), (uint32_t)h.xm,
                        (uint32_t)h.z0, (uint32_t)h.mul, (uint32_t)std::max(h.tab, 0), bslot[q],
-                       vslot[q]};
+                       0u};
       memcpy(&recs[q * 32], r, 32);
     }
   } else {
@@ -1413,8 +1413,11 @@ int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const int64_t* 
                                  cudaMemcpyHostToDevice, st));
   }
   if (!vl.empty()) {
-    if ((rc = dalloc(&op->d_vl, vl.size())) || (rc = dalloc(&op->d_vloff, vloff.size())))
+    if ((rc = dalloc(&op->d_vl, vl.size())) || (rc = dalloc(&op->d_vloff, vloff.size())) ||
+        (rc = dalloc(&op->d_vgslot, vslot.size())))
       return fail(rc);
+    HSV_TRY_CUDA(cudaMemcpyAsync(op->d_vgslot, vslot.data(), vslot.size() * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, st));
     HSV_TRY_CUDA(cudaMemcpyAsync(op->d_vl, vl.data(), vl.size() * sizeof(uint2),
                                  cudaMemcpyHostToDevice, st));
     HSV_TRY_CUDA(cudaMemcpyAsync(op->d_vloff, vloff.data(), vloff.size() * sizeof(int),
@@ -1461,6 +1464,7 @@ int hsv_op_destroy(hsv_op op) {
   dfree(op->d_bperm);
   dfree(op->d_vl);
   dfree(op->d_vloff);
+  dfree(op->d_vgslot);
   delete op;
   return HSV_OK;
 }

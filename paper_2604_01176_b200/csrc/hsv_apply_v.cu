@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(32 * kVWarps) k_apply_v(const ApplyArgs a) {
       const double2* __restrict__ prow = a.psi + (size_t)ra2 * Nb;
       for (int g = B.z; g < B.w; ++g) {
         const Rec<uint32_t> cur = ldrec(rp + g);
-        const int lo = __ldg(a.vloff + cur.pad1 + ch), hi = __ldg(a.vloff + cur.pad1 + ch + 1);
+        const uint32_t vs = __ldg(a.vgslot + g);
+        const int lo = __ldg(a.vloff + vs + ch), hi = __ldg(a.vloff + vs + ch + 1);
         const int shift = (int)((cur.meta >> 8) & 0xffu);
         const double* __restrict__ tab = a.tabs + cur.tab;
         // four entries per lane in flight: their list loads, table loads and
@@ -215,6 +216,7 @@ int launch_apply_v(const hsv_op_s* op, const ApplyArgs& a0, int S, bool* done) {
   ApplyArgs a = a0;
   a.vl = op->d_vl;
   a.vloff = op->d_vloff;
+  a.vgslot = op->d_vgslot;
   a.vl_chunk = op->vl_chunk;
   a.vl_nchunks = op->vl_nchunks;
   a.nsplit = S;

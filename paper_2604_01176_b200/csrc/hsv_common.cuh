@@ -177,6 +177,7 @@ struct hsv_op_s {
   GroupHash* d_ghash = nullptr;
   void* d_recs = nullptr;       // packed Rec<W> per group (kernel layout)
   uint16_t* d_bperm = nullptr;  // per-xb beta rank permutations (Rec.pad0 = slot), or nullptr
+  uint32_t* d_vgslot = nullptr; // K1v: per group, its valid list's offset slot
   // K1v valid lists (hsv_apply_v.cu): for each distinct beta flip xb of a hashed
   // group, the beta strings whose partner sb ^ xb stays in the sector, in rank
   // order, as {rb | rank(sb ^ xb) << 16, sb}; d_vloff[Rec.pad1 + c] = first

@@ -98,6 +98,7 @@ struct ApplyArgs {
   const int* vloff;
   int vl_chunk, vl_nchunks;
   const uint8_t* smap;     // K1v row-restricted mode: rows outside the map are skipped
+  const uint32_t* vgslot;  // K1v: per group, its list's offset slot
 };
 
 // K1r: row lists of the rows marked in smap (or, smap == nullptr, of the
