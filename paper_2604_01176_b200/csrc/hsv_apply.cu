@@ -723,7 +723,8 @@ void RowList::release() {
 }
 
 int launch_apply_rows(const hsv_op_s* op, const double2* psi, double2* out, int64_t a_lo,
-                      int64_t a_hi, const uint32_t* arow, const uint8_t* smap) {
+                      int64_t a_hi, const uint32_t* arow, const uint8_t* smap,
+                      int64_t support_rows) {
   const hsv_sector_s* s = op->sec;
   HSV_REQUIRE(s->dim < ((int64_t)1 << 32), HSV_ERR_UNSUPPORTED,
               "sector dimension %lld exceeds the 32-bit row index of the apply kernel",
@@ -752,18 +753,31 @@ int launch_apply_rows(const hsv_op_s* op, const double2* psi, double2* out, int6
     if (done) return HSV_OK;
   }
   a.nsplit = S;
+  // rows per lane: a lane's R rows are consecutive list entries of one alpha
+  // row, and the group loop runs for all R whether the entries exist or not, so
+  // R follows the support's rows per alpha row (H12 depth 100: 24 of 924)
   const int64_t units8 = (a_hi - a_lo) * ((s->Nb + 255) / 256);
-  const int R = 32 * units8 >= (int64_t)ctx().num_sms * 2 * 8 ? 8 : 4;
+  int R = 32 * units8 >= (int64_t)ctx().num_sms * 2 * 8 ? 8 : 4;
+  if (support_rows > 0 && tuning().apply_r == 0) {
+    const double per_row = (double)support_rows * s->Nb / (double)s->dim;   // per alpha row
+    const int Rs = per_row >= 192 ? 8 : per_row >= 96 ? 4 : per_row >= 48 ? 2 : 1;
+    R = std::min(R, Rs);
+  }
   RowList rl;
   int rc = rl.build(s, smap, nullptr, a_lo, a_hi, 32 * R);
   if (rc == HSV_OK) {
     a.rlist = rl.rlist; a.rcnt = rl.rcnt; a.utab = rl.utab; a.d_units = rl.d_units;
-    if (s->wide)
-      rc = R == 8 ? launch_apply_t<uint64_t, 32, 8, 2, 0, 1>(op, a, nullptr, smap, rl.max_units)
-                  : launch_apply_t<uint64_t, 32, 4, 3, 0, 1>(op, a, nullptr, smap, rl.max_units);
-    else
-      rc = R == 8 ? launch_apply_t<uint32_t, 16, 8, 2, 0, 1>(op, a, nullptr, smap, rl.max_units)
-                  : launch_apply_t<uint32_t, 16, 4, 3, 0, 1>(op, a, nullptr, smap, rl.max_units);
+#define HSV_ROWS_CASES(W, SH)                                                               \
+  rc = R == 8   ? launch_apply_t<W, SH, 8, 2, 0, 1>(op, a, nullptr, smap, rl.max_units)       \
+       : R == 4 ? launch_apply_t<W, SH, 4, 3, 0, 1>(op, a, nullptr, smap, rl.max_units)       \
+       : R == 2 ? launch_apply_t<W, SH, 2, 4, 0, 1>(op, a, nullptr, smap, rl.max_units)       \
+                : launch_apply_t<W, SH, 1, 4, 0, 1>(op, a, nullptr, smap, rl.max_units);
+    if (s->wide) {
+      HSV_ROWS_CASES(uint64_t, 32)
+    } else {
+      HSV_ROWS_CASES(uint32_t, 16)
+    }
+#undef HSV_ROWS_CASES
   }
   rl.release();
   return rc;

@@ -190,7 +190,8 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
 // K1r: out = H psi on the rows marked in smap (exactly the K1 values there),
 // 0 on every other row of [a_lo, a_hi); no energy partials.
 int launch_apply_rows(const hsv_op_s* op, const double2* psi, double2* out, int64_t a_lo,
-                      int64_t a_hi, const uint32_t* arow, const uint8_t* smap);
+                      int64_t a_hi, const uint32_t* arow, const uint8_t* smap,
+                      int64_t support_rows = -1);
 
 // Compressed QEB masks of one excitation operator.
 struct OpMasks {
@@ -213,6 +214,8 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
                   double2* psi, double2* lam, uint8_t* smap_out, double* norm2, double* d_grads,
                   int* err, double* err_val, bool* used);
 int smap_arow_async(const hsv_sector_s* sec, const uint8_t* smap, uint32_t* flags);
+// rows of the cached plan's support map (-1: no plan for this sector)
+int64_t sweep_plan_support(const hsv_sector_s* s);
 // drop the cached sweep plan (of sector s only, when s != nullptr)
 void release_sweep_plans(const hsv_sector_s* s = nullptr);
 

@@ -225,6 +225,7 @@ struct FilterArgs {
   uint32_t* live_count;
   uint32_t* wcount;       // per row: live orbits (so far, in batch order) that touch it
   uint16_t* wrank;        // per candidate and orbit element: the orbit's rank among them
+  unsigned long long* n_marked;   // rows added to the support map
 };
 
 __global__ void __launch_bounds__(256) k_plan_filter(const FilterArgs a) {
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(256) k_plan_filter(const FilterArgs a) {
     if (threadIdx.x == 0) B = a.bm[bi];
     __syncthreads();
     const uint32_t n = __ldg(a.cand_count[bi]);
-    unsigned live_n = 0u;
+    unsigned live_n = 0u, new_n = 0u;
     for (int64_t it = gt; it < n; it += nt) {
       uint32_t row[kOrb];
       unsigned touched, srcm[kBatch];
@@ -260,7 +261,10 @@ __global__ void __launch_bounds__(256) k_plan_filter(const FilterArgs a) {
         }
 #pragma unroll
       for (int t = 0; t < kOrb; ++t)
-        if ((marked >> t) & 1u) a.smap[row[t]] = 1;
+        if ((marked >> t) & 1u) {
+          if (!a.smap[row[t]]) ++new_n;
+          a.smap[row[t]] = 1;
+        }
       // write ranks for the barrier-free sweep: orbits of one batch are
       // disjoint, and the grid barrier orders batches, so a plain increment
       // gives every row's writers their batch order
@@ -274,6 +278,8 @@ __global__ void __launch_bounds__(256) k_plan_filter(const FilterArgs a) {
     }
     const unsigned tot = __reduce_add_sync(0xffffffffu, live_n);
     if (lane == 0 && tot) atomicAdd(a.live_count + bi, tot);
+    const unsigned totm = __reduce_add_sync(0xffffffffu, new_n);
+    if (lane == 0 && totm) atomicAdd(a.n_marked, (unsigned long long)totm);
     __syncthreads();
     grid_sync();   // batch bi + 1 sees the marks of batch bi
   }
@@ -758,6 +764,7 @@ struct Plan {
   uint32_t* chunk_rev = nullptr;   // adjoint order: chunks of the batches in reverse
   int64_t* chunk_off = nullptr;    // batch -> first chunk
   int64_t n_chunks = 0;
+  int64_t support_rows = 0;    // rows of the support map (HF closure)
   std::vector<int64_t> live_off, live_cnt;
   int64_t max_live = 0;
   void drop_live() {
@@ -894,6 +901,7 @@ int filter_plan(Plan& P) {
   P.live_off.assign(nb + 1, 0);
   P.live_cnt.assign(nb, 0);
   P.max_live = 0;
+  P.support_rows = 1;
   if (nb == 0) return stream_sync();
   std::vector<BatchMasks> hm(nb);
   std::vector<const uint2*> hc(nb);
@@ -918,12 +926,15 @@ int filter_plan(Plan& P) {
   int *sel = nullptr, *n_sel = nullptr;
   uint32_t* wcount = nullptr;
   uint16_t* wrank = nullptr;
+  unsigned long long* n_marked = nullptr;
   const bool ranks = (int64_t)ops_total(P) < 65535;
   if (ranks) {
     HSV_TRY(dalloc(&wcount, sec->dim));
     HSV_TRY(dalloc(&wrank, std::max<int64_t>(total, 1) * kOrb));
     HSV_TRY_CUDA(cudaMemsetAsync(wcount, 0, sec->dim * sizeof(uint32_t), stream()));
   }
+  HSV_TRY(dalloc(&n_marked, 1));
+  HSV_TRY_CUDA(cudaMemsetAsync(n_marked, 0, sizeof(unsigned long long), stream()));
   HSV_TRY(dalloc(&d_m, nb));
   HSV_TRY(dalloc(&d_c, nb));
   HSV_TRY(dalloc(&d_n, nb));
@@ -946,7 +957,7 @@ int filter_plan(Plan& P) {
   fa.bm = d_m; fa.cand = d_c; fa.cand_count = d_n; fa.flag_off = d_off; fa.n_batches = nb;
   fa.flags = flags; fa.smap = P.smap; fa.n_alpha = sec->n_alpha; fa.n_beta = sec->n_beta;
   fa.Nb = (uint32_t)sec->Nb; fa.Ra = sec->d_Ra; fa.Rb = sec->d_Rb; fa.live_count = live;
-  fa.wcount = wcount; fa.wrank = wrank;
+  fa.wcount = wcount; fa.wrank = wrank; fa.n_marked = n_marked;
   {
     ProfScope prof("sweep_plan");
     const int grid = coop_grid((const void*)k_plan_filter, (max_cand + 255) / 256);
@@ -966,9 +977,12 @@ int filter_plan(Plan& P) {
     dfree(tmp);
   }
   std::vector<uint32_t> hl(nb);
+  unsigned long long n_new = 0;
   HSV_TRY_CUDA(cudaMemcpyAsync(hl.data(), live, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(&n_new, n_marked, sizeof(n_new), cudaMemcpyDeviceToHost, stream()));
   HSV_TRY(stream_sync());
+  P.support_rows = 1 + (int64_t)n_new;   // HF + the rows the batches added
   std::vector<int64_t> cmp(nb + 1, 0);
   for (int q = 0; q < nb; ++q) {
     P.live_cnt[q] = hl[q];
@@ -1030,7 +1044,7 @@ int filter_plan(Plan& P) {
     HSV_CHECK_LAUNCH();
   }
   dfree(d_m); dfree(d_c); dfree(d_n); dfree(d_off); dfree(flags); dfree(live); dfree(sel);
-  dfree(n_sel); dfree(wcount); dfree(wrank); dfree(d_cmp); dfree(d_pad);
+  dfree(n_sel); dfree(wcount); dfree(wrank); dfree(d_cmp); dfree(d_pad); dfree(n_marked);
   HSV_TRY(stream_sync());   // the host offset vectors above must outlive their copies
   P.filtered = true;
   return HSV_OK;
@@ -1165,6 +1179,11 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
   dfree(part);
   dfree(red);
   return HSV_OK;
+}
+
+int64_t sweep_plan_support(const hsv_sector_s* s) {
+  const Plan& P = plan();
+  return P.sec == s && P.filtered ? P.support_rows : -1;
 }
 
 void release_sweep_plans(const hsv_sector_s* s) {
