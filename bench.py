@@ -503,7 +503,8 @@ def adapt_deep(world, iters=DEEP_ITERS, depths=DEEP_DEPTHS):
     row_nnz = eng.matrix.nnz / dim
     pk, _ = peaks()
     hbm = float(pk.get("hbm_gbs", 6650.0))
-    kern = ("apply_rows", "qeb", "adjoint", "apply", "screen", "push", "push_collect")
+    kern = ("apply_rows", "qeb", "adjoint", "apply", "screen", "push", "push_collect",
+            "sweep_plan")
     out = {}
     for k in depths:
         if f"thetas_at_{k}" not in tr.files or k + iters > len(sel):

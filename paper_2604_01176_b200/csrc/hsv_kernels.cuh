@@ -18,6 +18,8 @@ struct Tuning {
   int sweep = 2;          // adjoint/forward sweeps: 2 batched (orbits of kBatch rotations per
                           // grid barrier, hsv_sweep.cu), 1 one barrier per rotation, 0 launch per op
   int sweep_grid = 0;     // sweep blocks: 0 = min(co-resident, work items)
+  int sweep_incr = 1;     // sweep plans: 1 refilter only the batches an operator list change
+                          // touched (ADAPT appends), 0 refilter every batch
   int sweep_p2p = 0;      // batched sweeps without grid barriers (per-row versions, k_psweep):
                           // 1 on, 0 off.  Exact, but measured 2.9x slower at H12 depth 400
                           // (2.60 vs 0.88 ms forward): consecutive batches share rows densely

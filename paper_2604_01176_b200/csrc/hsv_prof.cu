@@ -83,6 +83,9 @@ int hsv_set_tuning(const char* key, int64_t value) {
   } else if (k == "apply_v") {
     HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "apply_v must be -1, 0 or 1");
     g_tuning.apply_v = (int)value;
+  } else if (k == "sweep_incr") {
+    HSV_REQUIRE(value == 0 || value == 1, HSV_ERR_INVALID, "sweep_incr must be 0 or 1");
+    g_tuning.sweep_incr = (int)value;
   } else if (k == "sweep_p2p") {
     HSV_REQUIRE(value == 0 || value == 1, HSV_ERR_INVALID, "sweep_p2p must be 0 or 1");
     g_tuning.sweep_p2p = (int)value;

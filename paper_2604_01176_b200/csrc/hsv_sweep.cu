@@ -225,7 +225,9 @@ struct FilterArgs {
   uint32_t* live_count;
   uint32_t* wcount;       // per row: live orbits (so far, in batch order) that touch it
   uint16_t* wrank;        // per candidate and orbit element: the orbit's rank among them
-  unsigned long long* n_marked;   // rows added to the support map
+  unsigned long long* n_marked;   // rows added to the support map (running count)
+  uint32_t* added;                // ... and the rows, in batch order (unmarked on a replan)
+  uint32_t* batch_new;            // per batch: rows it added (zeroed)
 };
 
 __global__ void __launch_bounds__(256) k_plan_filter(const FilterArgs a) {
@@ -262,7 +264,11 @@ __global__ void __launch_bounds__(256) k_plan_filter(const FilterArgs a) {
 #pragma unroll
       for (int t = 0; t < kOrb; ++t)
         if ((marked >> t) & 1u) {
-          if (!a.smap[row[t]]) ++new_n;
+          if (!a.smap[row[t]]) {
+            const unsigned long long pos = atomicAdd(a.n_marked, 1ull);
+            if (a.added) a.added[pos] = row[t];
+            ++new_n;
+          }
           a.smap[row[t]] = 1;
         }
       // write ranks for the barrier-free sweep: orbits of one batch are
@@ -278,8 +284,8 @@ __global__ void __launch_bounds__(256) k_plan_filter(const FilterArgs a) {
     }
     const unsigned tot = __reduce_add_sync(0xffffffffu, live_n);
     if (lane == 0 && tot) atomicAdd(a.live_count + bi, tot);
-    const unsigned totm = __reduce_add_sync(0xffffffffu, new_n);
-    if (lane == 0 && totm) atomicAdd(a.n_marked, (unsigned long long)totm);
+    const unsigned totn = __reduce_add_sync(0xffffffffu, new_n);
+    if (lane == 0 && totn && a.batch_new) atomicAdd(a.batch_new + bi, totn);
     __syncthreads();
     grid_sync();   // batch bi + 1 sees the marks of batch bi
   }
@@ -765,6 +771,9 @@ struct Plan {
   int64_t* chunk_off = nullptr;    // batch -> first chunk
   int64_t n_chunks = 0;
   int64_t support_rows = 0;    // rows of the support map (HF closure)
+  uint32_t* added = nullptr;   // rows each batch added to the map, batch after batch (dim)
+  std::vector<int64_t> added_end;   // per batch: rows added by batches <= it
+  bool has_ranks = false;
   std::vector<int64_t> live_off, live_cnt;
   int64_t max_live = 0;
   void drop_live() {
@@ -783,8 +792,10 @@ struct Plan {
     drop_live();
     dfree(smap);
     dfree(ver);
+    dfree(added);
     smap = nullptr;
     ver = nullptr;
+    added = nullptr;
     hf_row = -1;
   }
 };
@@ -888,34 +899,65 @@ int64_t ops_total(const Plan& P) {
   return n;
 }
 
-// The filter + gather of a plan whose batches are built (hsv: k_plan_filter).
-int filter_plan(Plan& P) {
+__global__ void k_unmark(const uint32_t* __restrict__ rows, int64_t n, uint8_t* __restrict__ smap) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) smap[rows[i]] = 0;
+}
+
+// The filter + gather of batches [first, nb) of a plan whose batches are built
+// (k_plan_filter).  first == 0: from scratch (support map = HF).  first > 0:
+// incremental -- batches [0, first) and their live orbits are kept, the
+// support map holds exactly their closure (get_plan unmarked the rows later
+// batches had added), and only the new batches are filtered and appended.
+// The barrier-free sweep's per-row write ranks need every batch: built (and
+// only then) from scratch when that sweep is enabled.
+int filter_plan(Plan& P, int first) {
   const hsv_sector_s* sec = P.sec;
   const int nb = (int)P.b.size();
-  P.drop_live();
+  const bool ranks = tuning().sweep_p2p != 0 && (int64_t)ops_total(P) < 65535;
+  if (ranks || !P.filtered || P.has_ranks) first = 0;
   if (!P.smap) HSV_TRY(dalloc(&P.smap, sec->dim));
-  static thread_local uint8_t one;
-  one = 1;
-  HSV_TRY_CUDA(cudaMemsetAsync(P.smap, 0, sec->dim, stream()));
-  HSV_TRY_CUDA(cudaMemcpyAsync(P.smap + P.hf_row, &one, 1, cudaMemcpyHostToDevice, stream()));
-  P.live_off.assign(nb + 1, 0);
-  P.live_cnt.assign(nb, 0);
-  P.max_live = 0;
-  P.support_rows = 1;
-  if (nb == 0) return stream_sync();
-  std::vector<BatchMasks> hm(nb);
-  std::vector<const uint2*> hc(nb);
-  std::vector<const uint32_t*> hn(nb);
-  std::vector<int64_t> off(nb + 1, 0);
-  int64_t max_cand = 1;
-  for (int q = 0; q < nb; ++q) {
-    hm[q] = batch_masks(P.b[q]);
-    hc[q] = P.b[q].cand;
-    hn[q] = P.b[q].cand_count;
-    off[q + 1] = off[q] + P.b[q].n_cand;
-    max_cand = std::max(max_cand, P.b[q].n_cand);
+  if (!P.added) HSV_TRY(dalloc(&P.added, sec->dim));
+  int64_t added0 = 0;
+  if (first == 0) {
+    P.drop_live();
+    static thread_local uint8_t one;
+    one = 1;
+    HSV_TRY_CUDA(cudaMemsetAsync(P.smap, 0, sec->dim, stream()));
+    HSV_TRY_CUDA(cudaMemcpyAsync(P.smap + P.hf_row, &one, 1, cudaMemcpyHostToDevice, stream()));
+    P.live_off.assign(1, 0);
+    P.live_cnt.clear();
+    P.added_end.clear();
+    P.max_live = 0;
+  } else {
+    added0 = P.added_end[first - 1];
+    P.live_off.resize(first + 1);
+    P.live_cnt.resize(first);
+    P.added_end.resize(first);
+    P.max_live = 0;
+    for (int q = 0; q < first; ++q) P.max_live = std::max(P.max_live, P.live_cnt[q]);
   }
-  const int64_t total = off[nb];
+  P.has_ranks = ranks;
+  const int nn = nb - first;   // batches to filter
+  P.support_rows = 1 + added0;
+  if (nn == 0) {
+    P.filtered = true;
+    return stream_sync();
+  }
+  std::vector<BatchMasks> hm(nn);
+  std::vector<const uint2*> hc(nn);
+  std::vector<const uint32_t*> hn(nn);
+  std::vector<int64_t> off(nn + 1, 0);
+  int64_t max_cand = 1;
+  for (int q = 0; q < nn; ++q) {
+    const PlanBatch& pb = P.b[first + q];
+    hm[q] = batch_masks(pb);
+    hc[q] = pb.cand;
+    hn[q] = pb.cand_count;
+    off[q + 1] = off[q] + pb.n_cand;
+    max_cand = std::max(max_cand, pb.n_cand);
+  }
+  const int64_t total = off[nn];
   HSV_REQUIRE(total < (int64_t)INT32_MAX, HSV_ERR_UNSUPPORTED, "sweep plan too large");
   BatchMasks* d_m = nullptr;
   const uint2** d_c = nullptr;
@@ -927,37 +969,42 @@ int filter_plan(Plan& P) {
   uint32_t* wcount = nullptr;
   uint16_t* wrank = nullptr;
   unsigned long long* n_marked = nullptr;
-  const bool ranks = (int64_t)ops_total(P) < 65535;
+  uint32_t* d_bnew = nullptr;
   if (ranks) {
     HSV_TRY(dalloc(&wcount, sec->dim));
     HSV_TRY(dalloc(&wrank, std::max<int64_t>(total, 1) * kOrb));
     HSV_TRY_CUDA(cudaMemsetAsync(wcount, 0, sec->dim * sizeof(uint32_t), stream()));
   }
+  static thread_local unsigned long long a0;
+  a0 = (unsigned long long)added0;
   HSV_TRY(dalloc(&n_marked, 1));
-  HSV_TRY_CUDA(cudaMemsetAsync(n_marked, 0, sizeof(unsigned long long), stream()));
-  HSV_TRY(dalloc(&d_m, nb));
-  HSV_TRY(dalloc(&d_c, nb));
-  HSV_TRY(dalloc(&d_n, nb));
-  HSV_TRY(dalloc(&d_off, nb + 1));
+  HSV_TRY_CUDA(cudaMemcpyAsync(n_marked, &a0, sizeof(a0), cudaMemcpyHostToDevice, stream()));
+  HSV_TRY(dalloc(&d_bnew, nn));
+  HSV_TRY_CUDA(cudaMemsetAsync(d_bnew, 0, nn * sizeof(uint32_t), stream()));
+  HSV_TRY(dalloc(&d_m, nn));
+  HSV_TRY(dalloc(&d_c, nn));
+  HSV_TRY(dalloc(&d_n, nn));
+  HSV_TRY(dalloc(&d_off, nn + 1));
   HSV_TRY(dalloc(&flags, std::max<int64_t>(total, 1)));
-  HSV_TRY(dalloc(&live, nb));
+  HSV_TRY(dalloc(&live, nn));
   HSV_TRY(dalloc(&sel, std::max<int64_t>(total, 1)));
   HSV_TRY(dalloc(&n_sel, 1));
-  HSV_TRY_CUDA(cudaMemcpyAsync(d_m, hm.data(), nb * sizeof(BatchMasks), cudaMemcpyHostToDevice,
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_m, hm.data(), nn * sizeof(BatchMasks), cudaMemcpyHostToDevice,
                                stream()));
-  HSV_TRY_CUDA(cudaMemcpyAsync(d_c, hc.data(), nb * sizeof(void*), cudaMemcpyHostToDevice,
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_c, hc.data(), nn * sizeof(void*), cudaMemcpyHostToDevice,
                                stream()));
-  HSV_TRY_CUDA(cudaMemcpyAsync(d_n, hn.data(), nb * sizeof(void*), cudaMemcpyHostToDevice,
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_n, hn.data(), nn * sizeof(void*), cudaMemcpyHostToDevice,
                                stream()));
-  HSV_TRY_CUDA(cudaMemcpyAsync(d_off, off.data(), (nb + 1) * sizeof(int64_t),
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_off, off.data(), (nn + 1) * sizeof(int64_t),
                                cudaMemcpyHostToDevice, stream()));
   HSV_TRY_CUDA(cudaMemsetAsync(flags, 0, std::max<int64_t>(total, 1), stream()));
-  HSV_TRY_CUDA(cudaMemsetAsync(live, 0, nb * sizeof(uint32_t), stream()));
+  HSV_TRY_CUDA(cudaMemsetAsync(live, 0, nn * sizeof(uint32_t), stream()));
   FilterArgs fa{};
-  fa.bm = d_m; fa.cand = d_c; fa.cand_count = d_n; fa.flag_off = d_off; fa.n_batches = nb;
+  fa.bm = d_m; fa.cand = d_c; fa.cand_count = d_n; fa.flag_off = d_off; fa.n_batches = nn;
   fa.flags = flags; fa.smap = P.smap; fa.n_alpha = sec->n_alpha; fa.n_beta = sec->n_beta;
   fa.Nb = (uint32_t)sec->Nb; fa.Ra = sec->d_Ra; fa.Rb = sec->d_Rb; fa.live_count = live;
   fa.wcount = wcount; fa.wrank = wrank; fa.n_marked = n_marked;
+  fa.added = P.added; fa.batch_new = d_bnew;
   {
     ProfScope prof("sweep_plan");
     const int grid = coop_grid((const void*)k_plan_filter, (max_cand + 255) / 256);
@@ -976,30 +1023,51 @@ int filter_plan(Plan& P) {
     count_launch();
     dfree(tmp);
   }
-  std::vector<uint32_t> hl(nb);
-  unsigned long long n_new = 0;
-  HSV_TRY_CUDA(cudaMemcpyAsync(hl.data(), live, nb * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+  std::vector<uint32_t> hl(nn);
+  std::vector<uint32_t> hbn(nn);
+  HSV_TRY_CUDA(cudaMemcpyAsync(hl.data(), live, nn * sizeof(uint32_t), cudaMemcpyDeviceToHost,
                                stream()));
-  HSV_TRY_CUDA(cudaMemcpyAsync(&n_new, n_marked, sizeof(n_new), cudaMemcpyDeviceToHost, stream()));
+  HSV_TRY_CUDA(cudaMemcpyAsync(hbn.data(), d_bnew, nn * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, stream()));
   HSV_TRY(stream_sync());
-  P.support_rows = 1 + (int64_t)n_new;   // HF + the rows the batches added
-  std::vector<int64_t> cmp(nb + 1, 0);
-  for (int q = 0; q < nb; ++q) {
-    P.live_cnt[q] = hl[q];
+  std::vector<int64_t> cmp(nn + 1, 0);
+  for (int q = 0; q < nn; ++q) {
+    P.live_cnt.push_back(hl[q]);
+    P.added_end.push_back((P.added_end.empty() ? 0 : P.added_end.back()) + (int64_t)hbn[q]);
     cmp[q + 1] = cmp[q] + hl[q];
-    P.live_off[q + 1] = P.live_off[q] + ((int64_t)hl[q] + 31) / 32 * 32;   // whole chunks
+    P.live_off.push_back(P.live_off.back() + ((int64_t)hl[q] + 31) / 32 * 32);   // whole chunks
     P.max_live = std::max<int64_t>(P.max_live, hl[q]);
   }
-  const int64_t n_live = cmp[nb];
+  P.support_rows = 1 + P.added_end.back();   // HF + the rows the batches added
+  const int64_t n_live = cmp[nn];
+  const int64_t keep_slots = P.live_off[first];
   const int64_t n_slots = P.live_off[nb];
-  HSV_TRY(dalloc(&P.rows, std::max<int64_t>(n_slots, 1) * kOrb));
-  HSV_TRY(dalloc(&P.masks, std::max<int64_t>(n_slots, 1)));
-  HSV_TRY_CUDA(cudaMemsetAsync(P.masks, 0, std::max<int64_t>(n_slots, 1) * sizeof(uint4),
-                               stream()));
+  {   // live-orbit arrays: keep the first batches' slots, append the new ones
+    uint32_t* rows = nullptr;
+    uint4* masks = nullptr;
+    HSV_TRY(dalloc(&rows, std::max<int64_t>(n_slots, 1) * kOrb));
+    HSV_TRY(dalloc(&masks, std::max<int64_t>(n_slots, 1)));
+    if (keep_slots > 0) {
+      HSV_TRY_CUDA(cudaMemcpyAsync(rows, P.rows, keep_slots * kOrb * sizeof(uint32_t),
+                                   cudaMemcpyDeviceToDevice, stream()));
+      HSV_TRY_CUDA(cudaMemcpyAsync(masks, P.masks, keep_slots * sizeof(uint4),
+                                   cudaMemcpyDeviceToDevice, stream()));
+    }
+    HSV_TRY_CUDA(cudaMemsetAsync(masks + keep_slots, 0,
+                                 std::max<int64_t>(n_slots - keep_slots, 0) * sizeof(uint4),
+                                 stream()));
+    dfree(P.rows);
+    dfree(P.masks);
+    P.rows = rows;
+    P.masks = masks;
+  }
+  dfree(P.ranks);
+  P.ranks = nullptr;
   if (ranks) HSV_TRY(dalloc(&P.ranks, std::max<int64_t>(n_slots, 1) * kOrb));
-  // chunk maps of the barrier-free sweep
   P.n_chunks = n_slots / 32;
-  {
+  dfree(P.chunk_batch); dfree(P.chunk_rev); dfree(P.chunk_off);
+  P.chunk_batch = nullptr; P.chunk_rev = nullptr; P.chunk_off = nullptr;
+  if (ranks) {   // chunk maps of the barrier-free sweep
     std::vector<int> cb(std::max<int64_t>(P.n_chunks, 1));
     std::vector<uint32_t> rev;
     std::vector<int64_t> choff(nb + 1);
@@ -1024,15 +1092,15 @@ int filter_plan(Plan& P) {
     HSV_TRY(stream_sync());   // host vectors die here
   }
   int64_t *d_cmp = nullptr, *d_pad = nullptr;
-  HSV_TRY(dalloc(&d_cmp, nb + 1));
-  HSV_TRY(dalloc(&d_pad, nb + 1));
-  HSV_TRY_CUDA(cudaMemcpyAsync(d_cmp, cmp.data(), (nb + 1) * sizeof(int64_t),
+  HSV_TRY(dalloc(&d_cmp, nn + 1));
+  HSV_TRY(dalloc(&d_pad, nn + 1));
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_cmp, cmp.data(), (nn + 1) * sizeof(int64_t),
                                cudaMemcpyHostToDevice, stream()));
-  HSV_TRY_CUDA(cudaMemcpyAsync(d_pad, P.live_off.data(), (nb + 1) * sizeof(int64_t),
+  HSV_TRY_CUDA(cudaMemcpyAsync(d_pad, P.live_off.data() + first, (nn + 1) * sizeof(int64_t),
                                cudaMemcpyHostToDevice, stream()));
   if (n_live > 0) {
     GatherArgs ga{};
-    ga.bm = d_m; ga.cand = d_c; ga.flag_off = d_off; ga.n_batches = nb; ga.sel = sel;
+    ga.bm = d_m; ga.cand = d_c; ga.flag_off = d_off; ga.n_batches = nn; ga.sel = sel;
     ga.n_sel = n_sel; ga.n_alpha = sec->n_alpha; ga.n_beta = sec->n_beta;
     ga.Nb = (uint32_t)sec->Nb; ga.Ra = sec->d_Ra; ga.Rb = sec->d_Rb;
     ga.rows = P.rows; ga.masks = P.masks;
@@ -1045,6 +1113,7 @@ int filter_plan(Plan& P) {
   }
   dfree(d_m); dfree(d_c); dfree(d_n); dfree(d_off); dfree(flags); dfree(live); dfree(sel);
   dfree(n_sel); dfree(wcount); dfree(wrank); dfree(d_cmp); dfree(d_pad); dfree(n_marked);
+  dfree(d_bnew);
   HSV_TRY(stream_sync());   // the host offset vectors above must outlive their copies
   P.filtered = true;
   return HSV_OK;
@@ -1077,6 +1146,21 @@ int get_plan(const hsv_sector_s* sec, int64_t hf_row, const std::vector<OpMasks>
                          (hf_row < 0 || hf_row == P.hf_row) && P.filtered;
   if (unchanged) return HSV_OK;
   if (hf_row < 0) { *ok = false; return HSV_OK; }
+  // incremental replan (the common ADAPT case: an appended operator changes the
+  // last batch or adds one): drop the support rows the replaced batches added,
+  // keep the prefix's live orbits, filter only the new batches
+  int first = 0;
+  if (tuning().sweep_incr != 0 && P.filtered && hf_row == P.hf_row && keep > 0 && !P.has_ranks &&
+      (int)P.added_end.size() == (int)P.b.size()) {
+    first = (int)keep;
+    const int64_t a0 = P.added_end[keep - 1], a1 = P.added_end.back();
+    if (a1 > a0) {
+      k_unmark<<<(unsigned)((a1 - a0 + 255) / 256), 256, 0, stream()>>>(P.added + a0, a1 - a0,
+                                                                        P.smap);
+      count_launch();
+      HSV_CHECK_LAUNCH();
+    }
+  }
   for (size_t q = keep; q < P.b.size(); ++q) { dfree(P.b[q].cand); dfree(P.b[q].cand_count); }
   P.b.resize(keep);
   for (size_t q = keep; q < parts.size(); ++q) {
@@ -1086,7 +1170,7 @@ int get_plan(const hsv_sector_s* sec, int64_t hf_row, const std::vector<OpMasks>
     P.b.push_back(pb);
   }
   P.hf_row = hf_row;
-  return filter_plan(P);
+  return filter_plan(P, first);
 }
 
 }  // namespace

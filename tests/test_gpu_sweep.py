@@ -134,3 +134,33 @@ def test_forward_drift_reported_by_backward(hsv, N, sweep):
     e1, g1 = eng.energy_and_gradient(ops, th)
     e2, g2 = eng.energy_and_gradient(ops, th)
     assert e1 == e2 and np.array_equal(g1, g2)
+
+
+@pytest.mark.parametrize("name", ["h8", "h12"])
+def test_incremental_plan_equals_fresh_plan(hsv, N, name):
+    """The sweep plan is refiltered incrementally when an operator is appended
+    (ADAPT): along a growing operator list, with operators repeated (a batch
+    boundary forced by a dependent flip) and one replaced in the middle (full
+    refilter), energies and gradients are bitwise equal to fresh plans."""
+    N.call("hsv_set_tuning", b"restrict_rows", -1)
+    sysm = hsv.MolecularSystem.bundled(name)
+    eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
+    pool = hsv.build_qeb_pool(sysm.n_qubits, sysm.integrals.nelec)
+    rng = np.random.default_rng(21)
+    idx = list(rng.integers(0, len(pool), size=20))
+    idx[7] = idx[6]                                   # a repeated operator
+    seqs = [idx[:k] for k in range(1, 21)] + [idx[:10] + [idx[3]] + idx[11:]]
+    th_all = rng.uniform(-0.4, 0.4, size=20)
+    try:
+        for seq in seqs:
+            ops = [pool.ops[i] for i in seq]
+            th = th_all[:len(seq)].copy()
+            th[-1] = 0.0                              # a new operator starts at theta = 0
+            N.call("hsv_set_tuning", b"sweep_incr", 1)
+            e1, g1 = eng.energy_and_gradient(ops, th)
+            N.call("hsv_set_tuning", b"sweep_incr", 0)
+            e0, g0 = eng.energy_and_gradient(ops[:1], th[:1])   # another plan in between
+            e0, g0 = eng.energy_and_gradient(ops, th)
+            assert e1 == e0 and np.array_equal(g1, g0), len(seq)
+    finally:
+        N.call("hsv_set_tuning", b"sweep_incr", 1)

@@ -1,0 +1,61 @@
+#!/usr/bin/env python3
+"""Per-call wall time of the deep H12 ADAPT leg (bench.py adapt_deep): every
+energy_and_gradient / screen / energy call is timed, the same resumed
+iterations run twice, so one-off costs (first-use loads, pool growth) show up
+as a difference between the passes:
+
+  python tools/iter_probe.py --depth 400 --iters 6
+"""
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+import paper_2604_01176_b200 as hsv  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--depth", type=int, default=400)
+    ap.add_argument("--iters", type=int, default=6)
+    ap.add_argument("--passes", type=int, default=2)
+    args = ap.parse_args()
+    tr = np.load(ROOT / "tests" / "golden" / "trace_h12_416.npz")
+    sysm = hsv.MolecularSystem.bundled("h12")
+    eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
+    pool = hsv.build_qeb_pool(sysm.n_qubits, sysm.integrals.nelec)
+    sel = [int(i) for i in tr["selected"]]
+    ops = [pool.ops[i] for i in sel]
+    k = args.depth
+    log = []
+    for name in ("energy_and_gradient", "screen", "energy", "prepare"):
+        fn = getattr(eng, name, None)
+        if fn is None:
+            continue
+
+        def wrap(*a, _fn=fn, _name=name, **kw):
+            t0 = time.perf_counter()
+            r = _fn(*a, **kw)
+            log.append((_name, len(a[0]) if _name == "energy_and_gradient" else -1,
+                        (time.perf_counter() - t0) * 1e3))
+            return r
+        setattr(eng, name, wrap)
+    init = (ops[:k], tr[f"thetas_at_{k}"])
+    for p in range(args.passes):
+        log.clear()
+        res = hsv.run_adapt(hsv.AdaptConfig(engine="sv", eps_grad=float(tr["eps"]),
+                                            max_iter=k + args.iters),
+                            sysm, engine=eng, replay=sel, initial=init)
+        wall = np.diff([r.wall_elapsed for r in res.records]) * 1e3
+        print(json.dumps({"pass": p, "iter_ms": [round(float(x), 2) for x in wall],
+                          "calls": [(n, d, round(t, 2)) for n, d, t in log]}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
