@@ -266,13 +266,13 @@ def run_hsv(args):
     M = dpool.n
     nnz_struct = op.nnz                       # structural nonzeros (== reference CSR nnz)
     psi_vals = s1_values(dim)
-    val_pinned = torch.from_numpy(psi_vals).pin_memory()
     st = hsv.svengine.DeviceState(basis)
 
     def upload():
-        # the binding's transfer of a SparseVector with full support (DeviceState.from_sparse):
-        # values only, in reference position order
-        N.call("hsv_state_set_dense", st.handle, N.C.cast(val_pinned.data_ptr(), N.P_dbl), None)
+        # exactly the binding's transfer of a SparseVector with full support
+        # (DeviceState.from_sparse): values only, in reference position order, from the
+        # caller's PAGEABLE numpy buffer (no pinned staging the API would not have)
+        N.call("hsv_state_set_dense", st.handle, N.ptr_f64(psi_vals), None)
 
     upload()
     n_alpha_strings = basis._sector.n_alpha_strings
@@ -355,7 +355,7 @@ def run_hsv(args):
         barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
-        upload()                               # H2D: amplitudes (pinned)
+        upload()                               # H2D: amplitudes (pageable numpy)
         if world > 1:
             res = step_device().cpu().numpy()             # D2H
             e_host.value, g_host[:] = res[0], res[2:2 + M]

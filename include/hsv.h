@@ -77,8 +77,9 @@ HSV_API void* hsv_get_stream(void);
 HSV_API int64_t hsv_launch_count(int reset);
 /* Device work counters of the ADAPT evaluation kernels (8 slots): [0] rotation
  * pairs processed by forward sweeps, [1] by adjoint sweeps, [2] rows computed by
- * the support-restricted H application (K1r).  Synchronizes when out != NULL;
- * reset != 0 zeroes them (stream-ordered). */
+ * the support-restricted H application (K1r); [6] / [7] (host-read, not reset)
+ * the device memory pool's reserved / used bytes.  Synchronizes when
+ * out != NULL; reset != 0 zeroes the device counters (stream-ordered). */
 HSV_API int hsv_stats(int64_t* out, int reset);
 HSV_API int hsv_synchronize(void);
 

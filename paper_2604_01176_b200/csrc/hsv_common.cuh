@@ -70,7 +70,8 @@ struct Context {
   // evaluation kernels, for the bench's algorithmic-byte accounting
   unsigned long long* d_stats = nullptr;
 };
-enum StatKey { kStatPairsFwd = 0, kStatPairsAdj = 1, kStatRowsK1r = 2, kStatCount = 8 };
+enum StatKey { kStatPairsFwd = 0, kStatPairsAdj = 1, kStatRowsK1r = 2, kStatPoolReserved = 6,
+               kStatPoolUsed = 7, kStatCount = 8 };
 Context& ctx();
 int ensure_init();
 inline cudaStream_t stream() { return ctx().stream; }

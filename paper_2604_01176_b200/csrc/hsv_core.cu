@@ -223,6 +223,14 @@ int hsv_stats(int64_t* out, int reset) {
     HSV_TRY(stream_sync());
     HSV_TRY_CUDA(cudaMemcpy(out, g_ctx.d_stats, kStatCount * sizeof(int64_t),
                             cudaMemcpyDeviceToHost));
+    // host-side slots: the stream-ordered pool's reserved / used bytes
+    cudaMemPool_t pool;
+    HSV_TRY_CUDA(cudaDeviceGetDefaultMemPool(&pool, g_ctx.device));
+    uint64_t v = 0;
+    HSV_TRY_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &v));
+    out[kStatPoolReserved] = (int64_t)v;
+    HSV_TRY_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &v));
+    out[kStatPoolUsed] = (int64_t)v;
   }
   if (reset)
     HSV_TRY_CUDA(cudaMemsetAsync(g_ctx.d_stats, 0, kStatCount * sizeof(unsigned long long),

@@ -500,9 +500,13 @@ __global__ void __launch_bounds__(256, 1) k_bsweep(const BSweepArgs a) {   // on
   // block: no serial descriptor load between a grid barrier and the next batch
   __shared__ __align__(16) BatchDev sB[kBChunk];
   const int lane = threadIdx.x & 31;
-  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  // logical warp gw: consecutive warps of a batch's orbit list sit on
+  // different SMs (a batch of a few thousand orbits would otherwise load all
+  // its amplitudes through the first ~20 SMs' LSUs)
+  const int64_t gw = (int64_t)(threadIdx.x >> 5) * gridDim.x + blockIdx.x;
+  const int64_t gt = gw * 32 + lane;
   const int64_t nt = (int64_t)gridDim.x * blockDim.x;
-  const int64_t gw = gt >> 5, nw = nt >> 5;
+  const int64_t nw = nt >> 5;
   OrbitRec next{};
   bool have_next = false;
   for (int bi = 0; bi < a.n_batches; ++bi) {
