@@ -77,11 +77,15 @@ HSV_API void* hsv_get_stream(void);
 HSV_API int64_t hsv_launch_count(int reset);
 /* Device work counters of the ADAPT evaluation kernels (8 slots): [0] rotation
  * pairs processed by forward sweeps, [1] by adjoint sweeps, [2] rows computed by
- * the support-restricted H application (K1r); [6] / [7] (host-read, not reset)
- * the device memory pool's reserved / used bytes.  Synchronizes when
- * out != NULL; reset != 0 zeroes the device counters (stream-ordered). */
+ * the support-restricted H application (K1r); host-read, not reset: [4] idle
+ * bytes held by the library's allocation cache, [5] cache misses (driver
+ * allocations) so far, [6] / [7] the device memory pool's reserved / used bytes.
+ * Synchronizes when out != NULL; reset != 0 zeroes the device counters. */
 HSV_API int hsv_stats(int64_t* out, int reset);
 HSV_API int hsv_synchronize(void);
+/* Return the library's cached idle device blocks (and the stream-ordered pool's
+ * idle memory) to the driver.  Scratch is otherwise kept for reuse. */
+HSV_API int hsv_mem_trim(void);
 
 /* ---- sector: replaces CiBasis / enumerate_basis (cibasis.py:98-181) ---- */
 HSV_API int hsv_sector_create(int n_qubits, int n_alpha, int n_beta, int ordering,

@@ -40,6 +40,7 @@ _SIGNATURES = {
     "hsv_get_stream": (vp, []),
     "hsv_launch_count": (i64, [C.c_int]),
     "hsv_stats": (C.c_int, [P_i64, C.c_int]),
+    "hsv_mem_trim": (C.c_int, []),
     "hsv_synchronize": (C.c_int, []),
     "hsv_sector_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
     "hsv_sector_destroy": (C.c_int, [vp]),

@@ -426,11 +426,14 @@ static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_wa
   const int64_t units1_full = (a.a_hi - a.a_lo) * a.upr;
   const int64_t units1 = LM ? list_units : units1_full;
   const size_t smem = RM == 1 ? (size_t)a.rb0_n * sizeof(uint32_t) : 0;
-  if (smem > 48 * 1024)
-    HSV_TRY_CUDA(cudaFuncSetAttribute(k_apply<W, SH, R, MINB, RM, LM>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
-  HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<W, SH, R, MINB, RM, LM>, 256, smem));
+  {
+    HostWatch hw("k_apply attributes");
+    if (smem > 48 * 1024)
+      HSV_TRY_CUDA(cudaFuncSetAttribute(k_apply<W, SH, R, MINB, RM, LM>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<W, SH, R, MINB, RM, LM>, 256, smem));
+  }
   occ = std::max(occ, 1);
   const int64_t max_warps = (int64_t)ctx().num_sms * occ * 8;
   // Split the bucket range of each row unit.  Split-major unit order keeps the
@@ -486,6 +489,7 @@ static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_wa
     HSV_TRY_CUDA(cudaMemsetAsync(a.out + a.a_lo * a.Nb, 0, rows * sizeof(double2), stream()));
   {
     ProfScope prof(LM ? "apply_rows" : "apply");
+    HostWatch hw("k_apply launch");
     k_apply<W, SH, R, MINB, RM, LM><<<(unsigned)grid, 256, smem, stream()>>>(a);
     if (ypart && LM)
       launch_combine_splits_map(ypart, S, rows, a.out, a.a_lo * a.Nb, smap, a.peer_rows,

@@ -70,29 +70,43 @@ struct Context {
   // evaluation kernels, for the bench's algorithmic-byte accounting
   unsigned long long* d_stats = nullptr;
 };
-enum StatKey { kStatPairsFwd = 0, kStatPairsAdj = 1, kStatRowsK1r = 2, kStatPoolReserved = 6,
-               kStatPoolUsed = 7, kStatCount = 8 };
+enum StatKey { kStatPairsFwd = 0, kStatPairsAdj = 1, kStatRowsK1r = 2, kStatCacheIdle = 4,
+               kStatCacheMisses = 5, kStatPoolReserved = 6, kStatPoolUsed = 7, kStatCount = 8 };
 Context& ctx();
 int ensure_init();
 inline cudaStream_t stream() { return ctx().stream; }
 inline void count_launch(int n = 1) { ctx().launches += n; }
 
-// stream-ordered allocation from the device pool
+// Host-stall watch (diagnostics): with HSV_WATCH_MS=t in the environment, a
+// watched host call that takes longer than t ms is reported on stderr with its
+// label (allocations, synchronizations, copies and launches on the ADAPT path).
+class HostWatch {
+ public:
+  explicit HostWatch(const char* what, int64_t bytes = -1);
+  ~HostWatch();
+ private:
+  const char* what_;
+  int64_t bytes_;
+  int64_t t0_ = -1;
+};
+
+// Device scratch allocation, stream-ordered on the library stream, through a
+// caching layer (hsv_core.cu): freed blocks stay mapped and are reused by
+// later requests of up to their size (best fit, at most 2x), so the ADAPT loop
+// does not go back to the driver once warm.  cudaMallocAsync's own pool remaps
+// physical pages between requests of changing sizes, and on the GPU boxes a
+// 210 MB request from an unchanged 736 MB reservation took 10-550 ms (HSV_WATCH_MS
+// logs, profiles/r02/alloc_stalls.txt).
+int cache_alloc(void** p, size_t bytes);
+void cache_free(void* p);
 template <typename T>
 int dalloc(T** p, size_t n) {
   if (n == 0) n = 1;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(p), n * sizeof(T), stream());
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    set_error(HSV_ERR_OOM, "device allocation of %zu bytes failed: %s", n * sizeof(T),
-              cudaGetErrorString(e));
-    return HSV_ERR_OOM;
-  }
-  return HSV_OK;
+  return cache_alloc(reinterpret_cast<void**>(p), n * sizeof(T));
 }
 template <typename T>
 void dfree(T* p) {
-  if (p) cudaFreeAsync(p, stream());
+  if (p) cache_free(const_cast<void*>(reinterpret_cast<const void*>(p)));
 }
 int stream_sync();   // stream sync + error mapping
 

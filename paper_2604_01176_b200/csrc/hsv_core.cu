@@ -3,7 +3,12 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <unordered_map>
+
+#include <chrono>
+#include <cstdlib>
 
 #include "hsv_common.cuh"
 #include "hsv_kernels.cuh"
@@ -36,7 +41,114 @@ int ensure_init() {
   return hsv_init(dev);
 }
 
+static int64_t watch_ms() {
+  static const int64_t v = [] {
+    const char* e = getenv("HSV_WATCH_MS");
+    return e ? (int64_t)atoll(e) : (int64_t)-1;
+  }();
+  return v;
+}
+static int64_t now_us() {
+  return std::chrono::duration_cast<std::chrono::microseconds>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+HostWatch::HostWatch(const char* what, int64_t bytes) : what_(what), bytes_(bytes) {
+  if (watch_ms() >= 0) t0_ = now_us();
+}
+HostWatch::~HostWatch() {
+  if (t0_ < 0) return;
+  const int64_t dt = now_us() - t0_;
+  if (dt < watch_ms() * 1000) return;
+  if (bytes_ >= 0) {
+    cudaMemPool_t pool;
+    uint64_t res = 0;
+    if (cudaDeviceGetDefaultMemPool(&pool, ctx().device) == cudaSuccess)
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+    fprintf(stderr, "[hsv watch] %s %.3f ms (%lld bytes, pool reserved %llu MB)\n", what_, dt * 1e-3,
+            (long long)bytes_, (unsigned long long)(res >> 20));
+  } else {
+    fprintf(stderr, "[hsv watch] %s %.3f ms\n", what_, dt * 1e-3);
+  }
+}
+
+// ------------------------------------------------------ allocation cache
+namespace {
+struct AllocCache {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_blocks;       // size -> block
+  std::unordered_map<void*, size_t> live;         // block -> size
+  size_t cached = 0, in_use = 0;
+  int64_t hits = 0, misses = 0;
+};
+AllocCache& cache() {
+  static AllocCache c;
+  return c;
+}
+// free every cached block (stream-ordered), e.g. before retrying a failed request
+void cache_trim_locked(AllocCache& c) {
+  for (auto& kv : c.free_blocks) cudaFreeAsync(kv.second, stream());
+  c.free_blocks.clear();
+  c.cached = 0;
+}
+}  // namespace
+
+int cache_alloc(void** p, size_t bytes) {
+  HostWatch hw("device allocation", (int64_t)bytes);
+  // size classes above 64 KB: the top 4 significant bits (steps of 1/8 of a
+  // power of two), so a buffer that grows a little per ADAPT iteration (sweep
+  // plan rows) keeps hitting its class instead of missing every time
+  bytes = (bytes + 511) & ~(size_t)511;
+  if (bytes > (64u << 10)) {
+    int sh = 63 - __builtin_clzll((unsigned long long)bytes) - 3;
+    const size_t step = (size_t)1 << sh;
+    bytes = (bytes + step - 1) & ~(step - 1);
+  }
+  AllocCache& c = cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto it = c.free_blocks.lower_bound(bytes);
+  if (it != c.free_blocks.end() && it->first <= 2 * bytes) {
+    *p = it->second;
+    c.live[*p] = it->first;
+    c.cached -= it->first;
+    c.in_use += it->first;
+    c.free_blocks.erase(it);
+    ++c.hits;
+    return HSV_OK;
+  }
+  cudaError_t e = cudaMallocAsync(p, bytes, stream());
+  if (e != cudaSuccess) {   // give the cached blocks back and retry once
+    cudaGetLastError();
+    cache_trim_locked(c);
+    e = cudaMallocAsync(p, bytes, stream());
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error(HSV_ERR_OOM, "device allocation of %zu bytes failed: %s", bytes,
+              cudaGetErrorString(e));
+    return HSV_ERR_OOM;
+  }
+  c.live[*p] = bytes;
+  c.in_use += bytes;
+  ++c.misses;
+  return HSV_OK;
+}
+
+void cache_free(void* p) {
+  AllocCache& c = cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto it = c.live.find(p);
+  if (it == c.live.end()) {   // not from the cache
+    cudaFreeAsync(p, stream());
+    return;
+  }
+  c.free_blocks.emplace(it->second, p);
+  c.cached += it->second;
+  c.in_use -= it->second;
+  c.live.erase(it);
+}
+
 int stream_sync() {
+  HostWatch hw("cudaStreamSynchronize");
   cudaError_t e = cudaStreamSynchronize(stream());
   if (e != cudaSuccess) {
     set_error(HSV_ERR_CUDA, "CUDA error during stream synchronize: %s", cudaGetErrorString(e));
@@ -231,6 +343,10 @@ int hsv_stats(int64_t* out, int reset) {
     out[kStatPoolReserved] = (int64_t)v;
     HSV_TRY_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &v));
     out[kStatPoolUsed] = (int64_t)v;
+    AllocCache& c = cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    out[kStatCacheIdle] = (int64_t)c.cached;
+    out[kStatCacheMisses] = c.misses;
   }
   if (reset)
     HSV_TRY_CUDA(cudaMemsetAsync(g_ctx.d_stats, 0, kStatCount * sizeof(unsigned long long),
@@ -240,6 +356,9 @@ int hsv_stats(int64_t* out, int reset) {
 
 int hsv_set_stream(void* s) {
   HSV_TRY(ensure_init());
+  // blocks freed on the old stream may still be in use by its queued work:
+  // drain it before they can be handed to work on the new one
+  HSV_TRY(stream_sync());
   g_ctx.stream = s ? reinterpret_cast<cudaStream_t>(s) : g_ctx.own;
   return HSV_OK;
 }
@@ -252,6 +371,20 @@ int64_t hsv_launch_count(int reset) {
   if (reset) g_ctx.launches = 0;
   return n;
 }
+int hsv_mem_trim(void) {
+  HSV_TRY(ensure_init());
+  {
+    AllocCache& c = cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    cache_trim_locked(c);
+  }
+  HSV_TRY(stream_sync());
+  cudaMemPool_t pool;
+  HSV_TRY_CUDA(cudaDeviceGetDefaultMemPool(&pool, g_ctx.device));
+  HSV_TRY_CUDA(cudaMemPoolTrimTo(pool, 0));
+  return HSV_OK;
+}
+
 int hsv_synchronize(void) {
   HSV_TRY(ensure_init());
   return stream_sync();

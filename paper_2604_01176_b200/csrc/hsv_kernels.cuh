@@ -17,6 +17,9 @@ struct Tuning {
   int push_keys = 32;     // auto: push while nnz(psi) * (1 + groups) <= push_keys * rows - 2^20
   int sweep = 2;          // adjoint/forward sweeps: 2 batched (orbits of kBatch rotations per
                           // grid barrier, hsv_sweep.cu), 1 one barrier per rotation, 0 launch per op
+  int sweep_bar = 0;      // batched sweep barrier: 0 grid.sync(), 1 counting (release/acquire;
+                          // measured equal at H12 depth 100/400, profiles/r02/sweep_probe_bar.jsonl)
+  int sweep_threads = 256;   // batched sweep block size (128 or 256)
   int sweep_grid = 0;     // sweep blocks: 0 = min(co-resident, work items)
   int sweep_incr = 1;     // sweep plans: 1 refilter only the batches an operator list change
                           // touched (ADAPT appends), 0 refilter every batch

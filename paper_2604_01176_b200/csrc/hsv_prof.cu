@@ -101,6 +101,12 @@ int hsv_set_tuning(const char* key, int64_t value) {
   } else if (k == "staged") {
     HSV_REQUIRE(value == 0 || value == 1, HSV_ERR_INVALID, "staged must be 0 or 1");
     g_tuning.staged = (int)value;
+  } else if (k == "sweep_bar") {
+    HSV_REQUIRE(value == 0 || value == 1, HSV_ERR_INVALID, "sweep_bar must be 0 or 1");
+    g_tuning.sweep_bar = (int)value;
+  } else if (k == "sweep_threads") {
+    HSV_REQUIRE(value == 128 || value == 256, HSV_ERR_INVALID, "sweep_threads must be 128 or 256");
+    g_tuning.sweep_threads = (int)value;
   } else if (k == "sweep_grid") {
     HSV_REQUIRE(value >= 0 && value <= (1 << 20), HSV_ERR_INVALID, "sweep_grid out of range");
     g_tuning.sweep_grid = (int)value;

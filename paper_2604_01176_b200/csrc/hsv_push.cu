@@ -319,6 +319,7 @@ static int push_t(const hsv_op_s* op, const ApplyArgs& a0, bool* done, int64_t* 
     HSV_PUSH_ALLOC(&keys, guess * per_src);
     p.keys = keys;
     HSV_TRY(launch_keys(true));
+    HostWatch hw("push count D2H");
     HSV_TRY_CUDA(cudaMemcpyAsync(h, cnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                                  stream()));
     HSV_TRY(stream_sync());

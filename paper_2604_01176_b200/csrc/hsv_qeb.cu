@@ -858,8 +858,11 @@ int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
   }
   static thread_local std::vector<double> h;
   h.resize(k + 2);
-  HSV_TRY_CUDA(cudaMemcpyAsync(h.data(), d_grad, (k + 2) * sizeof(double),
-                               cudaMemcpyDeviceToHost, stream()));
+  {
+    HostWatch hw("gradients D2H");
+    HSV_TRY_CUDA(cudaMemcpyAsync(h.data(), d_grad, (k + 2) * sizeof(double),
+                                 cudaMemcpyDeviceToHost, stream()));
+  }
   const int rc = sc.check();
   dfree(pl.la); dfree(pl.lb);
   sc.release();

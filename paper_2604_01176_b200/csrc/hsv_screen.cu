@@ -295,6 +295,7 @@ extern "C" {
 static int energy_screen_dev(hsv_op op, hsv_state psi, const hsv_pool_s* pool, int64_t a_lo,
                              int64_t a_hi, double* d_out) {
   const hsv_sector_s* s = op->sec;
+  ProfScope prof_all("es_all");
   double2* w = nullptr;
   HSV_TRY(dalloc(&w, s->dim));
   const int nw = apply_warps(op);
@@ -302,9 +303,15 @@ static int energy_screen_dev(hsv_op op, hsv_state psi, const hsv_pool_s* pool, i
   HSV_TRY(dalloc(&epart, 2 * (int64_t)nw));
   HSV_TRY_CUDA(cudaMemsetAsync(epart, 0, 2 * sizeof(double) * nw, stream()));
   int64_t used = 0;
-  HSV_TRY(state_arow_async(psi));
-  HSV_TRY(launch_apply(op, psi->d_amp, w, epart, a_lo, a_hi, 0.0, 0, &used, psi->d_arow,
-                       &psi->dense_hint));
+  {
+    ProfScope prof("es_arow");
+    HSV_TRY(state_arow_async(psi));
+  }
+  {
+    ProfScope prof("es_k1");
+    HSV_TRY(launch_apply(op, psi->d_amp, w, epart, a_lo, a_hi, 0.0, 0, &used, psi->d_arow,
+                         &psi->dense_hint));
+  }
   if (used == 1)   // already reduced to one (re, im) pair (dynamic schedule, push path)
     HSV_TRY_CUDA(cudaMemcpyAsync(d_out, epart, 2 * sizeof(double), cudaMemcpyDeviceToDevice,
                                  stream()));
@@ -318,6 +325,7 @@ static int energy_screen_dev(hsv_op op, hsv_state psi, const hsv_pool_s* pool, i
     HSV_TRY(arow_flags_async(w + a_lo * s->Nb, a_hi - a_lo, s->Nb, wrow + a_lo));
   }
   // psi found sparse by K1 (push path taken, dense_hint still clear): pivot on psi rows
+  ProfScope prof_k4("es_k4");
   HSV_TRY(launch_screen(op, psi->d_amp, w, pool, a_lo, a_hi, d_out + 2, psi->d_arow, wrow,
                         !psi->dense_hint));
   dfree(wrow);

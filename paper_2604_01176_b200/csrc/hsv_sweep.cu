@@ -83,6 +83,7 @@ struct BSweepArgs {
   double* err_val;
   unsigned long long* stats;   // pairs processed (kStatPairsFwd / kStatPairsAdj)
   uint32_t* ver;               // barrier-free sweep: writes completed per row (zeroed)
+  unsigned* bar;               // barrier sweep: counting-barrier word (zeroed), nullptr: grid.sync
   // barrier-free sweep: the plan's global (padded) orbit arrays, chunk maps
   const uint32_t* rows;
   const uint4* masks;
@@ -109,6 +110,32 @@ __device__ __forceinline__ bool is_src(uint32_t sa, uint32_t sb, uint32_t oa, ui
 }
 
 __device__ __forceinline__ void grid_sync() { cooperative_groups::this_grid().sync(); }
+
+// Counting grid barrier for the batched sweep (co-residency from the
+// cooperative launch): arrivals on one monotone counter, zeroed before the
+// launch; barrier e completes when e * gridDim.x blocks have arrived.  The
+// release add / acquire poll pair replaces grid.sync()'s fence + atomic + fence
+// (microbenchmark, 148 blocks with an L2 round trip between barriers: 1.73 vs
+// 2.07 us, tools/micro/gbar_probe.cu).
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void count_barrier(unsigned* ctr, unsigned& epoch) {
+  ++epoch;
+  if (!ctr) {
+    grid_sync();
+    return;
+  }
+  __syncthreads();   // the block's writes are ordered before thread 0's release
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+    const unsigned target = epoch * gridDim.x;
+    while ((int)(ld_acquire_u32(ctr) - target) < 0) {}
+  }
+  __syncthreads();
+}
 
 // i-th string (ascending) with occ set, virt clear and `ones` electrons on the
 // remaining orbitals of nmask (binomials bt[n * 32 + k]).
@@ -494,7 +521,7 @@ __device__ __forceinline__ OrbitRec load_orbit(const BatchDev& B, int64_t it) {
 }
 
 template <int MODE>
-__global__ void __launch_bounds__(256, 1) k_bsweep(const BSweepArgs a) {   // one block per SM (launch_bsweep)
+__global__ void __launch_bounds__(256, 1) k_bsweep(const BSweepArgs a) {   // <= one block per SM (launch_bsweep)
   constexpr int NV = MODE == kAdj ? 3 : 2;
   // batch descriptors staged in shared memory kBChunk at a time by the whole
   // block: no serial descriptor load between a grid barrier and the next batch
@@ -509,6 +536,7 @@ __global__ void __launch_bounds__(256, 1) k_bsweep(const BSweepArgs a) {   // on
   const int64_t nw = nt >> 5;
   OrbitRec next{};
   bool have_next = false;
+  unsigned epoch = 0;
   for (int bi = 0; bi < a.n_batches; ++bi) {
     if (bi % kBChunk == 0) {
       __syncthreads();
@@ -553,7 +581,7 @@ __global__ void __launch_bounds__(256, 1) k_bsweep(const BSweepArgs a) {   // on
         have_next = true;
       }
     }
-    grid_sync();   // batch bi+1 reads rows batch bi wrote
+    count_barrier(a.bar, epoch);   // batch bi+1 reads rows batch bi wrote
   }
   // per-rotation totals: one rotation per warp, warps summed in a fixed order
   // (warps whose first orbit index is past the batch wrote nothing: skipped)
@@ -571,7 +599,7 @@ __global__ void __launch_bounds__(256, 1) k_bsweep(const BSweepArgs a) {   // on
       if (lane == 0) a.red[(int64_t)(B.op0 + j) * NV + q] = x;
     }
   }
-  grid_sync();
+  count_barrier(a.bar, epoch);
   norm_chain<MODE, NV>(a);
 }
 
@@ -770,6 +798,7 @@ struct Plan {
   uint4* masks = nullptr;
   uint32_t* ranks = nullptr;   // barrier-free sweep: per element write rank | writers << 16
   uint32_t* ver = nullptr;     // per-row versions (dim), zeroed before each barrier-free sweep
+  unsigned* bar = nullptr;     // counting-barrier word of the barrier sweep
   int* chunk_batch = nullptr;  // physical 32-orbit chunk -> batch
   uint32_t* chunk_rev = nullptr;   // adjoint order: chunks of the batches in reverse
   int64_t* chunk_off = nullptr;    // batch -> first chunk
@@ -797,8 +826,10 @@ struct Plan {
     dfree(smap);
     dfree(ver);
     dfree(added);
+    dfree(bar);
     smap = nullptr;
     ver = nullptr;
+    bar = nullptr;
     added = nullptr;
     hf_row = -1;
   }
@@ -887,9 +918,9 @@ int build_batch(const hsv_sector_s* sec, PlanBatch& pb) {
   return HSV_OK;
 }
 
-int coop_grid(const void* fn, int64_t want) {
+int coop_grid(const void* fn, int64_t want, int threads = 256) {
   int occ = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 256, 0) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, 0) != cudaSuccess) {
     cudaGetLastError();
     occ = 1;
   }
@@ -1233,12 +1264,17 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
   const int64_t want = tuning().sweep_grid > 0 ? tuning().sweep_grid
                        : p2p ? (int64_t)ctx().num_sms
                              : std::min<int64_t>(ctx().num_sms, (P.max_live + 255) / 256);
-  const int grid = coop_grid(fn, std::max<int64_t>(want, 1));
+  const int threads = p2p ? 256 : tuning().sweep_threads;
+  const int grid = coop_grid(fn, std::max<int64_t>(want * 256 / threads, 1), threads);
   const int NV = mode == kAdj ? 3 : 2;
   double *part = nullptr, *red = nullptr;
   // barrier version: [batch][block][rotation][NV]; barrier-free: [batch][warp][...]
-  HSV_TRY(dalloc(&part, (p2p ? std::max<int64_t>(P.n_chunks, 1) : (int64_t)nb * grid * 8) *
-                            kBatch * NV));
+  HSV_TRY(dalloc(&part, (p2p ? std::max<int64_t>(P.n_chunks, 1)
+                              : (int64_t)nb * grid * (threads / 32)) * kBatch * NV));
+  if (!p2p && tuning().sweep_bar == 1) {
+    if (!P.bar) HSV_TRY(dalloc(&P.bar, 1));
+    HSV_TRY_CUDA(cudaMemsetAsync(P.bar, 0, sizeof(unsigned), stream()));
+  }
   if (p2p) {
     if (!P.ver) HSV_TRY(dalloc(&P.ver, sec->dim));
     HSV_TRY_CUDA(cudaMemsetAsync(P.ver, 0, sec->dim * sizeof(uint32_t), stream()));
@@ -1253,14 +1289,16 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
   a.norm2 = norm2; a.grads = d_grads; a.err = err; a.err_val = err_val;
   a.stats = ctx().d_stats;
   a.ver = P.ver;
+  a.bar = (!p2p && tuning().sweep_bar == 1) ? P.bar : nullptr;
   a.rows = P.rows; a.masks = P.masks; a.ranks = P.ranks;
   a.n_chunks = P.n_chunks; a.chunk_batch = P.chunk_batch; a.chunk_off = P.chunk_off;
   a.chunk_order = mode == kFwd ? nullptr : P.chunk_rev;
   void* params[] = {&a};
   {
     ProfScope prof(mode == kFwd ? "qeb" : "adjoint");
-    HSV_TRY_CUDA(cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3(256), params, 0,
-                                             stream()));
+    HostWatch hw("k_bsweep cooperative launch");
+    HSV_TRY_CUDA(cudaLaunchCooperativeKernel(fn, dim3((unsigned)grid), dim3((unsigned)threads),
+                                             params, 0, stream()));
   }
   count_launch();
   dfree(d_b);

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--iters", type=int, default=6)
     ap.add_argument("--passes", type=int, default=2)
     ap.add_argument("--sync", type=int, default=1, help="synchronize after every call")
+    ap.add_argument("--tune", nargs="*", default=[], help="KEY=V library tuning keys")
     args = ap.parse_args()
     tr = np.load(ROOT / "tests" / "golden" / "trace_h12_416.npz")
     sysm = hsv.MolecularSystem.bundled("h12")
@@ -39,27 +40,41 @@ def main():
     import gc
     scopes = ("apply", "apply_rows", "qeb", "adjoint", "screen", "push", "push_collect",
               "sweep_plan")
+    extra = ("es_all", "es_arow", "es_k1", "es_k4")
     N.call("hsv_prof_enable", 1)
+
+    from cuda.bindings import runtime as rt
+    N.init(0)
+    for kv in args.tune:
+        key, v = kv.split("=")
+        N.call("hsv_set_tuning", key.encode(), int(v))
+    ev0 = rt.cudaEventCreate()[1]
+    ev1 = rt.cudaEventCreate()[1]
 
     def pool():
         st = (N.i64 * 8)()
         N.call("hsv_stats", st, 0)
         return st[6] >> 20, st[7] >> 20
 
-    def dev_ms():
+    def dev_ms(each=False):
         N.call("hsv_prof_collect")
-        tot = 0.0
-        for kn in scopes:
+        tot, d = 0.0, {}
+        for kn in scopes + extra:
             t, c = N.dbl(), N.i64()
             N.call("hsv_prof_get", kn.encode(), N.C.byref(t), N.C.byref(c))
-            tot += t.value
-        return tot
+            if kn in scopes:
+                tot += t.value
+            d[kn] = t.value
+        return d if each else tot
     for name in ("energy_and_gradient", "screen", "energy", "rebuild", "state_size"):
         fn = getattr(eng, name, None)
         if fn is None:
             continue
 
         def wrap(*a, _fn=fn, _name=name, **kw):
+            stream = N.lib().hsv_get_stream()
+            rt.cudaEventRecord(ev0, stream)
+            e0 = dev_ms(True)
             d0 = dev_ms()
             p0 = pool()
             c0 = time.process_time()
@@ -68,9 +83,13 @@ def main():
             if args.sync:
                 N.call("hsv_synchronize")
             t1 = time.perf_counter()
+            rt.cudaEventRecord(ev1, stream)
+            rt.cudaEventSynchronize(ev1)
+            span = rt.cudaEventElapsedTime(ev0, ev1)[1]
             log.append((_name, len(a[0]) if _name == "energy_and_gradient" else -1,
                         round((t1 - t0) * 1e3, 2), round((time.process_time() - c0) * 1e3, 2),
-                        round(dev_ms() - d0, 2), p0, pool()))
+                        round(dev_ms() - d0, 2), p0, pool(), round(span, 2),
+                        {k: round(v - e0[k], 2) for k, v in dev_ms(True).items() if v - e0[k] > 0.5}))
             return r
         setattr(eng, name, wrap)
     init = (ops[:k], tr[f"thetas_at_{k}"])

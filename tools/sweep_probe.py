@@ -65,7 +65,8 @@ def main():
             for key, v in kv:   # back to defaults
                 N.call("hsv_set_tuning", key.encode(),
                        {"sweep": 2, "restrict_rows": -1, "push": -1, "sweep_p2p": 0,
-                        "apply_v": 0, "apply_t": 0, "sweep_grid": 0}.get(key, -1))
+                        "apply_v": 0, "apply_t": 0, "sweep_grid": 0,
+                        "sweep_bar": 0, "sweep_threads": 256}.get(key, -1))
 
 
 if __name__ == "__main__":
