@@ -78,13 +78,14 @@ HSV_API int64_t hsv_launch_count(int reset);
 /* Device work counters of the ADAPT evaluation kernels (8 slots): [0] rotation
  * pairs processed by forward sweeps, [1] by adjoint sweeps, [2] rows computed by
  * the support-restricted H application (K1r); host-read, not reset: [4] idle
- * bytes held by the library's allocation cache, [5] cache misses (driver
- * allocations) so far, [6] / [7] the device memory pool's reserved / used bytes.
+ * bytes of the library's device arena, [5] arena chunks taken from the driver
+ * so far, [6] / [7] the CUDA default pool's reserved / used bytes.
  * Synchronizes when out != NULL; reset != 0 zeroes the device counters. */
 HSV_API int hsv_stats(int64_t* out, int reset);
 HSV_API int hsv_synchronize(void);
-/* Return the library's cached idle device blocks (and the stream-ordered pool's
- * idle memory) to the driver.  Scratch is otherwise kept for reuse. */
+/* Return the wholly idle chunks of the library's device arena (and the CUDA
+ * default pool's idle memory) to the driver; synchronizes.  Freed scratch is
+ * otherwise kept for reuse. */
 HSV_API int hsv_mem_trim(void);
 
 /* ---- sector: replaces CiBasis / enumerate_basis (cibasis.py:98-181) ---- */

@@ -90,13 +90,9 @@ class HostWatch {
   int64_t t0_ = -1;
 };
 
-// Device scratch allocation, stream-ordered on the library stream, through a
-// caching layer (hsv_core.cu): freed blocks stay mapped and are reused by
-// later requests of up to their size (best fit, at most 2x), so the ADAPT loop
-// does not go back to the driver once warm.  cudaMallocAsync's own pool remaps
-// physical pages between requests of changing sizes, and on the GPU boxes a
-// 210 MB request from an unchanged 736 MB reservation took 10-550 ms (HSV_WATCH_MS
-// logs, profiles/r02/alloc_stalls.txt).
+// Device scratch allocation, stream-ordered on the library stream, from the
+// library's device arena (hsv_core.cu): large chunks taken from the driver once
+// and sub-allocated, so the ADAPT loop does not go back to the driver once warm.
 int cache_alloc(void** p, size_t bytes);
 void cache_free(void* p);
 template <typename T>
@@ -305,6 +301,17 @@ class ProfScope {
   const char* name_;
   cudaEvent_t a_ = nullptr;
   bool active_ = false;
+};
+
+// RAII host-time scope, accumulated under "h:<name>" next to the kernel
+// scopes while profiling is enabled (hsv_prof_get("h:eg_fwd", ...)).
+class HostProf {
+ public:
+  explicit HostProf(const char* name);
+  ~HostProf();
+ private:
+  const char* name_;
+  int64_t t0_ = -1;
 };
 
 int reduce_sum_f64(const double* d_in, int64_t n, int64_t stride, int64_t count,

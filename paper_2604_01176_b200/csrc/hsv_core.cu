@@ -60,91 +60,130 @@ HostWatch::~HostWatch() {
   const int64_t dt = now_us() - t0_;
   if (dt < watch_ms() * 1000) return;
   if (bytes_ >= 0) {
-    cudaMemPool_t pool;
-    uint64_t res = 0;
-    if (cudaDeviceGetDefaultMemPool(&pool, ctx().device) == cudaSuccess)
-      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
-    fprintf(stderr, "[hsv watch] %s %.3f ms (%lld bytes, pool reserved %llu MB)\n", what_, dt * 1e-3,
-            (long long)bytes_, (unsigned long long)(res >> 20));
+    fprintf(stderr, "[hsv watch] %s %.3f ms (%lld bytes)\n", what_, dt * 1e-3, (long long)bytes_);
   } else {
     fprintf(stderr, "[hsv watch] %s %.3f ms\n", what_, dt * 1e-3);
   }
 }
 
-// ------------------------------------------------------ allocation cache
+// ------------------------------------------------------ device arena
+// Scratch and states are carved from large chunks the library owns (cudaMalloc
+// once, kept): best-fit free ranges with splitting and coalescing inside a
+// chunk, stream-ordered like cudaMallocAsync (one library stream; a block freed
+// by earlier work is handed to later work on the same stream).  On the GPU
+// boxes every trip to the driver -- cudaMallocAsync pool growth, and even pool
+// remaps of an unchanged reservation -- cost 3-550 ms (profiles/r02/alloc_stalls.txt),
+// so the ADAPT loop must not make any once warm.
 namespace {
-struct AllocCache {
+constexpr size_t kAlign = 512;
+constexpr size_t kChunk = (size_t)512 << 20;   // new chunks: max(request, 512 MB)
+struct Arena {
   std::mutex mu;
-  std::multimap<size_t, void*> free_blocks;       // size -> block
-  std::unordered_map<void*, size_t> live;         // block -> size
-  size_t cached = 0, in_use = 0;
-  int64_t hits = 0, misses = 0;
+  struct Chunk { char* base; size_t size; };
+  std::vector<Chunk> chunks;
+  std::multimap<size_t, char*> free_by_size;        // size -> start
+  std::map<char*, std::pair<size_t, int>> free_by_addr;   // start -> (size, chunk)
+  std::unordered_map<char*, std::pair<size_t, int>> live;  // start -> (size, chunk)
+  size_t reserved = 0, in_use = 0;
+  int64_t driver_allocs = 0;
 };
-AllocCache& cache() {
-  static AllocCache c;
-  return c;
+Arena& arena() {
+  static Arena a;
+  return a;
 }
-// free every cached block (stream-ordered), e.g. before retrying a failed request
-void cache_trim_locked(AllocCache& c) {
-  for (auto& kv : c.free_blocks) cudaFreeAsync(kv.second, stream());
-  c.free_blocks.clear();
-  c.cached = 0;
+void erase_free(Arena& A, std::map<char*, std::pair<size_t, int>>::iterator it) {
+  auto r = A.free_by_size.equal_range(it->second.first);
+  for (auto q = r.first; q != r.second; ++q)
+    if (q->second == it->first) { A.free_by_size.erase(q); break; }
+  A.free_by_addr.erase(it);
+}
+void insert_free(Arena& A, char* p, size_t n, int chunk) {
+  // coalesce with the free neighbours of the same chunk
+  auto nx = A.free_by_addr.lower_bound(p);
+  if (nx != A.free_by_addr.end() && nx->second.second == chunk && p + n == nx->first) {
+    n += nx->second.first;
+    erase_free(A, nx);
+  }
+  auto pv = A.free_by_addr.lower_bound(p);
+  if (pv != A.free_by_addr.begin()) {
+    --pv;
+    if (pv->second.second == chunk && pv->first + pv->second.first == p) {
+      p = pv->first;
+      n += pv->second.first;
+      erase_free(A, pv);
+    }
+  }
+  A.free_by_addr[p] = {n, chunk};
+  A.free_by_size.emplace(n, p);
+}
+// give wholly free chunks back to the driver (synchronizes)
+int arena_trim_locked(Arena& A) {
+  if (cudaStreamSynchronize(stream()) != cudaSuccess) cudaGetLastError();
+  for (size_t c = 0; c < A.chunks.size(); ++c) {
+    auto it = A.free_by_addr.find(A.chunks[c].base);
+    if (A.chunks[c].base && it != A.free_by_addr.end() && it->second.first == A.chunks[c].size) {
+      erase_free(A, it);
+      cudaFree(A.chunks[c].base);
+      A.reserved -= A.chunks[c].size;
+      A.chunks[c] = {nullptr, 0};
+    }
+  }
+  return HSV_OK;
 }
 }  // namespace
 
 int cache_alloc(void** p, size_t bytes) {
   HostWatch hw("device allocation", (int64_t)bytes);
-  // size classes above 64 KB: the top 4 significant bits (steps of 1/8 of a
-  // power of two), so a buffer that grows a little per ADAPT iteration (sweep
-  // plan rows) keeps hitting its class instead of missing every time
-  bytes = (bytes + 511) & ~(size_t)511;
-  if (bytes > (64u << 10)) {
-    int sh = 63 - __builtin_clzll((unsigned long long)bytes) - 3;
-    const size_t step = (size_t)1 << sh;
-    bytes = (bytes + step - 1) & ~(step - 1);
+  bytes = (bytes + kAlign - 1) & ~(kAlign - 1);
+  Arena& A = arena();
+  std::lock_guard<std::mutex> lk(A.mu);
+  auto it = A.free_by_size.lower_bound(bytes);
+  if (it == A.free_by_size.end()) {   // new chunk
+    size_t csz = std::max(bytes, kChunk);
+    char* base = nullptr;
+    cudaError_t e = cudaMalloc(&base, csz);
+    if (e != cudaSuccess && csz > bytes) {   // no room for a full chunk: exact size
+      cudaGetLastError();
+      csz = bytes;
+      e = cudaMalloc(&base, csz);
+    }
+    if (e != cudaSuccess) {   // return wholly free chunks, retry once
+      cudaGetLastError();
+      arena_trim_locked(A);
+      e = cudaMalloc(&base, csz);
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      set_error(HSV_ERR_OOM, "device allocation of %zu bytes failed: %s", bytes,
+                cudaGetErrorString(e));
+      return HSV_ERR_OOM;
+    }
+    A.chunks.push_back({base, csz});
+    A.reserved += csz;
+    ++A.driver_allocs;
+    insert_free(A, base, csz, (int)A.chunks.size() - 1);
+    it = A.free_by_size.lower_bound(bytes);
   }
-  AllocCache& c = cache();
-  std::lock_guard<std::mutex> lk(c.mu);
-  auto it = c.free_blocks.lower_bound(bytes);
-  if (it != c.free_blocks.end() && it->first <= 2 * bytes) {
-    *p = it->second;
-    c.live[*p] = it->first;
-    c.cached -= it->first;
-    c.in_use += it->first;
-    c.free_blocks.erase(it);
-    ++c.hits;
-    return HSV_OK;
-  }
-  cudaError_t e = cudaMallocAsync(p, bytes, stream());
-  if (e != cudaSuccess) {   // give the cached blocks back and retry once
-    cudaGetLastError();
-    cache_trim_locked(c);
-    e = cudaMallocAsync(p, bytes, stream());
-  }
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    set_error(HSV_ERR_OOM, "device allocation of %zu bytes failed: %s", bytes,
-              cudaGetErrorString(e));
-    return HSV_ERR_OOM;
-  }
-  c.live[*p] = bytes;
-  c.in_use += bytes;
-  ++c.misses;
+  char* start = it->second;
+  auto fa = A.free_by_addr.find(start);
+  const size_t have = fa->second.first;
+  const int chunk = fa->second.second;
+  erase_free(A, fa);
+  if (have > bytes) insert_free(A, start + bytes, have - bytes, chunk);   // split off the tail
+  A.live[start] = {bytes, chunk};
+  A.in_use += bytes;
+  *p = start;
   return HSV_OK;
 }
 
 void cache_free(void* p) {
-  AllocCache& c = cache();
-  std::lock_guard<std::mutex> lk(c.mu);
-  auto it = c.live.find(p);
-  if (it == c.live.end()) {   // not from the cache
-    cudaFreeAsync(p, stream());
-    return;
-  }
-  c.free_blocks.emplace(it->second, p);
-  c.cached += it->second;
-  c.in_use -= it->second;
-  c.live.erase(it);
+  Arena& A = arena();
+  std::lock_guard<std::mutex> lk(A.mu);
+  auto it = A.live.find(static_cast<char*>(p));
+  if (it == A.live.end()) return;   // not an arena block (never happens: dalloc is the only source)
+  A.in_use -= it->second.first;
+  insert_free(A, it->first, it->second.first, it->second.second);
+  A.live.erase(it);
 }
 
 int stream_sync() {
@@ -343,10 +382,10 @@ int hsv_stats(int64_t* out, int reset) {
     out[kStatPoolReserved] = (int64_t)v;
     HSV_TRY_CUDA(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &v));
     out[kStatPoolUsed] = (int64_t)v;
-    AllocCache& c = cache();
-    std::lock_guard<std::mutex> lk(c.mu);
-    out[kStatCacheIdle] = (int64_t)c.cached;
-    out[kStatCacheMisses] = c.misses;
+    Arena& A = arena();
+    std::lock_guard<std::mutex> lk(A.mu);
+    out[kStatCacheIdle] = (int64_t)(A.reserved - A.in_use);
+    out[kStatCacheMisses] = A.driver_allocs;
   }
   if (reset)
     HSV_TRY_CUDA(cudaMemsetAsync(g_ctx.d_stats, 0, kStatCount * sizeof(unsigned long long),
@@ -374,11 +413,10 @@ int64_t hsv_launch_count(int reset) {
 int hsv_mem_trim(void) {
   HSV_TRY(ensure_init());
   {
-    AllocCache& c = cache();
-    std::lock_guard<std::mutex> lk(c.mu);
-    cache_trim_locked(c);
+    Arena& A = arena();
+    std::lock_guard<std::mutex> lk(A.mu);
+    arena_trim_locked(A);
   }
-  HSV_TRY(stream_sync());
   cudaMemPool_t pool;
   HSV_TRY_CUDA(cudaDeviceGetDefaultMemPool(&pool, g_ctx.device));
   HSV_TRY_CUDA(cudaMemPoolTrimTo(pool, 0));

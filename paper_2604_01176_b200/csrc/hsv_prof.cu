@@ -1,5 +1,6 @@
 // Live per-kernel timing (CUDA events on the launching stream) and the
 // persistent device operator pool used by the screen kernel.
+#include <chrono>
 #include <map>
 #include <string>
 #include <vector>
@@ -32,6 +33,20 @@ static cudaEvent_t take_event() {
   cudaEvent_t e = g_prof.free_ev.back();
   g_prof.free_ev.pop_back();
   return e;
+}
+
+static int64_t host_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+HostProf::HostProf(const char* name) : name_(name) {
+  if (g_prof.on) t0_ = host_ns();
+}
+HostProf::~HostProf() {
+  if (t0_ < 0) return;
+  auto& slot = g_prof.acc[std::string("h:") + name_];
+  slot.first += (host_ns() - t0_) * 1e-6;
+  slot.second += 1;
 }
 
 ProfScope::ProfScope(const char* name) : name_(name) {

@@ -748,6 +748,7 @@ static int take_pending_drift(hsv_state psi) {
 int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const uint64_t* virt,
                          const double* cs, const double* sn, int64_t k, int64_t a_lo,
                          int64_t a_hi, hsv_state psi, hsv_state w) {
+  HostProf hp("eg_fwd");
   HSV_TRY(check_eg_args(op, occ, virt, cs, sn, k));
   HSV_REQUIRE(psi && w && psi != w && psi->sec == op->sec && w->sec == op->sec,
               HSV_ERR_INVALID, "bad state argument");
@@ -761,8 +762,12 @@ int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const 
   // (the support map closes over every rotation, theta = 0 included, in the
   // batched sweep only)
   const bool rows_only = tuning().restrict_rows != 0 && tuning().sweep == 2;
-  HSV_TRY(forward_psi(sec, hf_key, occ, virt, cs, sn, k, psi, sc, pl, rows_only));
+  {
+    HostProf hf("fwd_psi");
+    HSV_TRY(forward_psi(sec, hf_key, occ, virt, cs, sn, k, psi, sc, pl, rows_only));
+  }
   int64_t used = 0;
+  HostProf hk("k1r_launch");
   if (rows_only && psi->smap_valid)
     HSV_TRY(launch_apply_rows(op, psi->d_amp, w->d_amp, a_lo, a_hi, psi->d_arow, psi->d_smap,
                               sweep_plan_support(sec)));
@@ -809,6 +814,7 @@ int hsv_ansatz_state(hsv_sector s, uint64_t hf_key, const uint64_t* occ, const u
 int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
                     const uint64_t* virt, const double* cs, const double* sn, int64_t k,
                     double* energy, double* grads) {
+  HostProf hp("eg_bwd");
   HSV_TRY(check_eg_args(op, occ, virt, cs, sn, k));
   HSV_REQUIRE(energy && (k == 0 || grads), HSV_ERR_INVALID, "null output");
   HSV_REQUIRE(psi && w && psi != w && psi->sec == op->sec && w->sec == op->sec,
@@ -860,6 +866,7 @@ int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
   h.resize(k + 2);
   {
     HostWatch hw("gradients D2H");
+    HostProf hs("bwd_wait");
     HSV_TRY_CUDA(cudaMemcpyAsync(h.data(), d_grad, (k + 2) * sizeof(double),
                                  cudaMemcpyDeviceToHost, stream()));
   }

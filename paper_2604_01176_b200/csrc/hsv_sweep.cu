@@ -1223,7 +1223,10 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
   const int k = (int)ops.size();
   std::vector<std::vector<int>> parts;
   bool ok = true;
-  HSV_TRY(get_plan(sec, mode == kFwd ? hf_row : -1, ops, parts, &ok));
+  {
+    HostProf hp("get_plan");
+    HSV_TRY(get_plan(sec, mode == kFwd ? hf_row : -1, ops, parts, &ok));
+  }
   if (!ok) {
     *used = false;
     return HSV_OK;

@@ -431,3 +431,23 @@ def test_complex_state_energy_is_real_and_gradients_consistent(hsv, systems, rng
         t = hsv.apply_generator(pool[k], st).to_dense()
         assert abs(g[k] - 2.0 * np.real(np.vdot(w, t))) <= 1e-12
     assert abs(re.value - np.real(np.vdot(v, w))) <= 1e-12
+
+
+def test_complex_apply_is_the_reference_matrix_and_exactly_linear(hsv, systems, rng):
+    """complex128 H|psi> (no complex reference output exists: the reference's
+    molecular path is real) anchored twice: against the reference's own CSR
+    (golden ref_h6, bitwise equal to the materialized matrix above) applied on
+    the host to the complex vector, and by exact linearity -- H(i psi) is i H psi
+    bit for bit, since every product and sum is mirrored under re <-> -im."""
+    s, m, _, _ = systems["h6"]
+    ref = load_golden("ref_h6")
+    import scipy.sparse
+    A = scipy.sparse.csr_matrix((ref["csr_v"], ref["csr_ci"], ref["csr_ro"]))
+    n = len(s.basis)
+    v = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    v /= np.linalg.norm(v)
+    w = m.apply_state(hsv.SvState(s.basis, hsv.SparseVector(n, np.arange(n), v))).to_sparse().to_dense()
+    want = A @ v
+    assert np.max(np.abs(w - want)) <= 1e-12 * max(1.0, np.max(np.abs(want)))
+    wi = m.apply_state(hsv.SvState(s.basis, hsv.SparseVector(n, np.arange(n), 1j * v))).to_sparse().to_dense()
+    assert np.array_equal(wi.real, -w.imag) and np.array_equal(wi.imag, w.real)
