@@ -121,10 +121,11 @@ def ncu_traffic(kernel):
         return None
 
 
-def step_roofline(sysm, ops, nnz, dim, ms, hbm):
-    """Whole-step roofline: algorithmic bytes of <psi|H|psi> (16 P + 24 N) plus the
-    pool gradients (16 * sum_k matches_k + 24 N), SURVEY.md 8(d).  matches_k =
-    rows in source or target pattern of operator k = 2 * C_alpha * C_beta."""
+def step_roofline(sysm, ops, nnz, dim, ms, hbm, apply_bytes=None):
+    """Whole-step roofline: bytes of <psi|H|psi> (the apply kernel's: streamed
+    slots for K1a, else the algorithmic 16 P + 24 N) plus the pool gradients
+    (16 * sum_k matches_k + 24 N), SURVEY.md 8(d).  matches_k = rows in source or
+    target pattern of operator k = 2 * C_alpha * C_beta."""
     from math import comb
     b = sysm.basis
     norb = sysm.n_qubits // 2
@@ -141,7 +142,7 @@ def step_roofline(sysm, ops, nnz, dim, ms, hbm):
         va = [q for q in op.virt if q in set(range(0, sysm.n_qubits, 2))]
         vb = [q for q in op.virt if q not in va]
         matches += 2 * cnt(b.n_alpha, oa, va) * cnt(b.n_beta, ob, vb)
-    by = 16.0 * nnz + 24.0 * dim + 16.0 * matches + 24.0 * dim
+    by = (apply_bytes if apply_bytes else 16.0 * nnz + 24.0 * dim) + 16.0 * matches + 24.0 * dim
     ach = by / (ms * 1e-3) / 1e9
     return {"bytes": by, "matches": matches, "achieved": ach, "peak": hbm, "frac": ach / hbm,
             "unit": "GB/s"}
@@ -414,10 +415,20 @@ def run_hsv(args):
         # algorithmic bytes of one H application over the rank's rows:
         # 16 B per nonzero matrix element (one complex128 gather) + 24 B per row
         # (stream psi_b and write w_b ... key + amplitude) -- SURVEY.md 8(d)
-        bytes_apply = (16.0 * nnz_struct + 24.0 * dim) * rows_local / dim
+        # K1a (assembled rows, built on the warm-up step when they fit): the kernel
+        # STREAMS 12 B per stored slot (column + element, sliced-ELL padding
+        # included) and reads psi_b, the diagonal and writes w_b (40 B per row);
+        # the psi gathers hit L2/L1 (psi is 13.7 MB at H12)
+        slots, nsplit = N.i64(), N.i64()
+        N.call("hsv_op_sell_info", op.handle, a_lo, a_hi, N.C.byref(slots), N.C.byref(nsplit))
+        assembled = slots.value > 0
+        if assembled:
+            bytes_apply = 12.0 * slots.value + 40.0 * rows_local
+        else:
+            bytes_apply = (16.0 * nnz_struct + 24.0 * dim) * rows_local / dim
         achieved = bytes_apply / (apply_ms * 1e-3) / 1e9
         screen_ms = prof["screen"][0] / max(prof["screen"][1], 1)
-        traffic = ncu_traffic("k_apply")
+        traffic = ncu_traffic("k_apply_sell" if assembled else "k_apply")
         dram_gbs = traffic / (apply_ms * 1e-3) / 1e9 if traffic else None
         line = {
             "metric": METRIC if cfg == CONFIG else METRIC.replace("H12", cfg.upper()),
@@ -433,23 +444,39 @@ def run_hsv(args):
                        "parallelism": f"owner-computes alpha rows x{world}",
                        "exchange": exchange},
             "energy": energy,
-            "roofline": {"bound": "hbm", "kernel": "k_apply (H|psi>, K1)",
-                         "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "peak_kind": pk_kind,
-                         "frac_basis": "ALGORITHMIC bytes (16 B per nonzero matrix element "
-                                       "+ 24 B per row, SURVEY 8d) / K1 time, against the "
-                                       "HBM copy peak",
-                         "traffic": traffic,
-                         "dram_achieved": dram_gbs,
-                         "dram_frac": dram_gbs / hbm if dram_gbs else None,
-                         "limiter": "instruction issue / L1 (ncu: issue-active ~46%, "
-                                    "L2 hit ~95%); psi (13.7 MB) is L2-resident at H12, so "
-                                    "real DRAM traffic is ~0.5% of peak and frac is a "
-                                    "bytes-equivalent figure, not DRAM utilisation",
-                         "apply_ms": apply_ms,
-                         "bytes_per_launch": bytes_apply},
+            "roofline": ({"bound": "hbm", "kernel": "k_apply_sell (H|psi>, K1a: assembled "
+                                                    "sliced-ELL rows)",
+                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                          "frac": achieved / hbm, "peak_kind": pk_kind,
+                          "frac_basis": "STREAMED bytes: 12 B per stored slot (column + "
+                                        "element, padding included) + 40 B per row (psi_b, "
+                                        "diagonal, w_b) / K1a time, against the HBM copy peak",
+                          "stored_slots": slots.value, "nnz": nnz_struct,
+                          "traffic": traffic,
+                          "dram_achieved": dram_gbs,
+                          "dram_frac": dram_gbs / hbm if dram_gbs else None,
+                          "limiter": "HBM stream of the assembled rows (the psi gathers "
+                                     "hit L2/L1)",
+                          "apply_ms": apply_ms,
+                          "bytes_per_launch": bytes_apply} if assembled else
+                         {"bound": "hbm", "kernel": "k_apply (H|psi>, K1)",
+                          "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                          "frac": achieved / hbm, "peak_kind": pk_kind,
+                          "frac_basis": "ALGORITHMIC bytes (16 B per nonzero matrix element "
+                                        "+ 24 B per row, SURVEY 8d) / K1 time, against the "
+                                        "HBM copy peak",
+                          "traffic": traffic,
+                          "dram_achieved": dram_gbs,
+                          "dram_frac": dram_gbs / hbm if dram_gbs else None,
+                          "limiter": "instruction issue / L1 (ncu: issue-active ~46%, "
+                                     "L2 hit ~95%); psi is L2-resident at H12, so real "
+                                     "DRAM traffic is ~0.5% of peak and frac is a "
+                                     "bytes-equivalent figure, not DRAM utilisation",
+                          "apply_ms": apply_ms,
+                          "bytes_per_launch": bytes_apply}),
             "kernels_ms": {"apply": apply_ms, "screen": screen_ms},
-            "step_roofline": step_roofline(sysm, pool_ops, nnz_struct, dim, ms_per_step, hbm),
+            "step_roofline": step_roofline(sysm, pool_ops, nnz_struct, dim, ms_per_step, hbm,
+                                           apply_bytes=bytes_apply * dim / max(rows_local, 1)),
             "e2e": {"value": e2e_value, "unit": UNIT, "ms_per_step": e2e_t,
                     "h2d_bytes_per_step": dim * 8, "d2h_bytes_per_step": (2 + M) * 8},
             "gpu_launches": launches,
@@ -504,7 +531,7 @@ def adapt_deep(world, iters=DEEP_ITERS, depths=DEEP_DEPTHS):
     pk, _ = peaks()
     hbm = float(pk.get("hbm_gbs", 6650.0))
     kern = ("apply_rows", "qeb", "adjoint", "apply", "screen", "push", "push_collect",
-            "sweep_plan")
+            "sweep_plan", "sup_build")
     out = {}
     for k in depths:
         if f"thetas_at_{k}" not in tr.files or k + iters > len(sel):

@@ -110,6 +110,12 @@ HSV_API int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const i
 HSV_API int hsv_op_destroy(hsv_op op);
 /* n_terms, n_groups (distinct x incl. diagonal), number of in-sector nonzero
  * matrix elements is not stored (matrix-free). */
+/* K1a: stored slots (elements incl. sliced-ELL padding; 12 B each) and split
+ * count of the assembled rows for alpha rows [a_lo, a_hi), 0 if not assembled
+ * (K1a is built on the first H application of a range whose rows fit
+ * sell_budget_mb; the matrix-free K1 runs otherwise). */
+HSV_API int hsv_op_sell_info(hsv_op op, int64_t a_lo, int64_t a_hi, int64_t* slots,
+                             int64_t* splits);
 HSV_API int hsv_op_info(hsv_op op, int64_t* n_terms, int64_t* n_groups, int64_t* n_active_groups);
 /* Number of structurally nonzero matrix elements (== reference CSR nnz). */
 HSV_API int hsv_op_count_nnz(hsv_op op, int64_t* nnz);

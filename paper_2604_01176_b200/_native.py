@@ -41,6 +41,7 @@ _SIGNATURES = {
     "hsv_launch_count": (i64, [C.c_int]),
     "hsv_stats": (C.c_int, [P_i64, C.c_int]),
     "hsv_mem_trim": (C.c_int, []),
+    "hsv_op_sell_info": (C.c_int, [vp, i64, i64, P_i64, P_i64]),
     "hsv_synchronize": (C.c_int, []),
     "hsv_sector_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
     "hsv_sector_destroy": (C.c_int, [vp]),

@@ -134,8 +134,12 @@ __global__ void k_csr_rows(const uint32_t* __restrict__ Sa, const uint32_t* __re
 // IEEE rounding is symmetric under negation) and h a per-group perfect
 // multiply-shift hash of the in-sector patterns of b on x.  Other groups
 // (singles carrying number-operator Z's) run the sequential term loop.
-template <typename W, int SH, int R, int MINB, int RM, int LM>
+template <typename W, int SH, int R, int MINB, int RM, int LM, int EM = 0>
 __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
+  // EM (SELL build): 0 accumulate; 1 count the (row, split) entries with a
+  // nonzero matrix element; 2 write them -- (partner row, element) in exactly
+  // the order the accumulation adds them
+  static_assert(EM == 0 || LM == 0, "the SELL build runs over the full row range");
   constexpr bool RS = RM == 1;
   static_assert(!(LM && RM == 2), "row-list mode reads partner ranks from Rb0");
   const int lane = threadIdx.x & 31;
@@ -206,6 +210,7 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
     W s[R];
     uint32_t sb[R];
     double2 acc[R];
+    uint64_t epos[R];   // EM: entry count (1) or next slot (2) of the lane's (row, split)
     unsigned live = 0u, inrm = 0u;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
@@ -214,6 +219,14 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
       if (LM) inrm |= inr ? (1u << k) : 0u;
       sb[k] = inr ? __ldg(a.Sb + rb) : 0u;
       s[k] = (W)sa | ((W)sb[k] << SH);
+      if (EM) {
+        live |= inr ? (1u << k) : 0u;
+        const uint64_t rl = (uint64_t)(rowbase + rb - (uint32_t)a.a_lo * Nb);
+        epos[k] = EM == 1 ? 0ull
+                          : (inr ? __ldg(a.sell_off + (rl >> 5) * (uint64_t)a.nsplit + sp) + (rl & 31u)
+                                 : 0ull);
+        continue;
+      }
       const double2 pv = inr ? a.psi[rowbase + rb] : make_double2(0.0, 0.0);
       const bool lv = inr && (!a.energy_only || pv.x != 0.0 || pv.y != 0.0);
       const double d = (a.diag && lv && sp == 0) ? a.diag[rowbase + rb] : 0.0;
@@ -247,6 +260,18 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
             const double amp = __hiloint2double(__double2hiint(A) ^ sgn, __double2loint(A));
             const uint32_t rk = RM == 2 ? __ldg(a.bperm + (cur.pad0 + rb0 + k * 32))
                                 : RS ? rb0_sh[sb[k] ^ xb] : __ldg(a.Rb0 + (uint32_t)(sb[k] ^ xb));
+            if (EM) {   // out-of-sector partners and cancelled sums hold A = 0: no entry
+              if (A != 0.0 && ((live >> k) & 1u)) {
+                if (EM == 2) {
+                  a.sell_cols[epos[k]] = rowoff + rk;
+                  a.sell_amps[epos[k]] = amp;
+                  epos[k] += 32;
+                } else {
+                  ++epos[k];
+                }
+              }
+              continue;
+            }
             const double2 p = a.psi[rowoff + rk];
             acc[k].x = fma(amp, p.x, acc[k].x);
             acc[k].y = fma(amp, p.y, acc[k].y);
@@ -303,6 +328,18 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
 #pragma unroll
           for (int k = 0; k < R; ++k) {
             if ((v >> k) & 1u) {
+              if (EM) {
+                if (amp[k] != 0.0) {
+                  if (EM == 2) {
+                    a.sell_cols[epos[k]] = rowoff + __ldg(a.Rb + (sb[k] ^ xb));
+                    a.sell_amps[epos[k]] = amp[k];
+                    epos[k] += 32;
+                  } else {
+                    ++epos[k];
+                  }
+                }
+                continue;
+              }
               const double2 p = a.psi[rowoff + __ldg(a.Rb + (sb[k] ^ xb))];
               acc[k].x = fma(amp[k], p.x, acc[k].x);
               acc[k].y = fma(amp[k], p.y, acc[k].y);
@@ -311,6 +348,14 @@ __global__ void __launch_bounds__(256, MINB) k_apply(const ApplyArgs a) {
         }
       }
     }
+    if (EM == 1) {
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+        if (rb0 + k * 32 < Nb)
+          a.sell_cnt[(uint64_t)(rowbase + rb0 + k * 32 - (uint32_t)a.a_lo * Nb) * a.nsplit + sp] =
+              (uint32_t)epos[k];
+    }
+    if (EM) continue;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       if (LM ? !((inrm >> k) & 1u) : rb0 + k * 32 >= Nb) continue;
@@ -415,7 +460,7 @@ void use_split_table(const hsv_op_s* op, int St, ApplyArgs& a) {
   a.split_bk = op->d_splits + T.cut_off;
 }
 
-template <typename W, int SH, int R, int MINB, int RM = 0, int LM = 0>
+template <typename W, int SH, int R, int MINB, int RM = 0, int LM = 0, int EM = 0>
 static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_warps_out,
                           const uint8_t* smap = nullptr, int64_t list_units = 0) {
   ApplyArgs a = a0;
@@ -430,9 +475,9 @@ static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_wa
   {
     HostWatch hw("k_apply attributes");
     if (smem > 48 * 1024)
-      HSV_TRY_CUDA(cudaFuncSetAttribute(k_apply<W, SH, R, MINB, RM, LM>,
+      HSV_TRY_CUDA(cudaFuncSetAttribute(k_apply<W, SH, R, MINB, RM, LM, EM>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<W, SH, R, MINB, RM, LM>, 256, smem));
+    HSV_TRY_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_apply<W, SH, R, MINB, RM, LM, EM>, 256, smem));
   }
   occ = std::max(occ, 1);
   const int64_t max_warps = (int64_t)ctx().num_sms * occ * 8;
@@ -488,9 +533,9 @@ static int launch_apply_t(const hsv_op_s* op, const ApplyArgs& a0, int64_t* n_wa
   if (LM && a.out && !ypart)   // rows outside the list are exact zeros
     HSV_TRY_CUDA(cudaMemsetAsync(a.out + a.a_lo * a.Nb, 0, rows * sizeof(double2), stream()));
   {
-    ProfScope prof(LM ? "apply_rows" : "apply");
+    ProfScope prof(EM ? "sell_build" : LM ? "apply_rows" : "apply");
     HostWatch hw("k_apply launch");
-    k_apply<W, SH, R, MINB, RM, LM><<<(unsigned)grid, 256, smem, stream()>>>(a);
+    k_apply<W, SH, R, MINB, RM, LM, EM><<<(unsigned)grid, 256, smem, stream()>>>(a);
     if (ypart && LM)
       launch_combine_splits_map(ypart, S, rows, a.out, a.a_lo * a.Nb, smap, a.peer_rows,
                                 a.n_peer_rows);
@@ -536,6 +581,440 @@ int k1_default_split(const hsv_op_s* op, int64_t a_lo, int64_t a_hi, bool has_ou
   return S;
 }
 
+// ------------------------------------------------------ K1a (assembled rows)
+// The matrix-free K1 recomputes every element each launch: x-local hash,
+// sign, partner rank, out-of-sector partners adding exact zeros (issue-bound,
+// 1,455 instructions per row at H12).  Where the rows fit in HBM, they are
+// enumerated ONCE by K1 itself (EM count and emit modes: same buckets, same
+// groups, same order) into a sliced ELL matrix, and every later H application
+// streams it: 12 B per stored element, coalesced, plus the psi gather.  Each
+// lane replays K1's per-split FMA chain (diagonal first in split 0, elements
+// in K1's order, exact zeros dropped -- adding +-0 changes nothing but the
+// sign of a zero) and sums the split partials in split order, so rows are
+// bit-identical to K1's.
+__global__ void k_sell_len(const uint32_t* __restrict__ cnt, int64_t rows, int S, int64_t n_chunks,
+                           uint32_t* __restrict__ len, uint64_t* __restrict__ sz) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;   // (chunk, split)
+  if (i >= n_chunks * S) return;
+  const int64_t c = i / S;
+  const int sp = (int)(i - c * S);
+  uint32_t m = 0;
+  for (int l = 0; l < 32; ++l) {
+    const int64_t r = c * 32 + l;
+    if (r < rows) m = max(m, __ldg(cnt + r * S + sp));
+  }
+  len[i] = m;
+  sz[i] = 32ull * m;
+}
+
+struct SellArgs {
+  const uint32_t* cols;
+  const double* amps;
+  const uint64_t* off;
+  const uint32_t* len;
+  int64_t n_chunks, rows, row0;   // rows of the range (K1s: of the list), first internal row
+  const uint32_t* rlist;          // K1s: local rows of the list (nullptr: rows in order)
+  int S;
+  const double2* psi;
+  const double* diag;
+  double2* out;
+  double prune;
+  int energy_only;
+  double* cpart;                  // [chunk][2] energy partials or nullptr
+  double2* const* peer_rows;
+  int n_peer_rows;
+};
+
+template <int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_apply_sell(const SellArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = gw; c < a.n_chunks; c += nw) {
+    const int64_t li = c * 32 + lane;
+    const bool inr = li < a.rows;
+    const int64_t row = a.row0 + (a.rlist ? (inr ? (int64_t)__ldg(a.rlist + li) : 0) : li);
+    const double2 pv = inr ? a.psi[row] : make_double2(0.0, 0.0);
+    if (a.energy_only && !__any_sync(0xffffffffu, pv.x != 0.0 || pv.y != 0.0)) {
+      if (lane == 0 && a.cpart) { a.cpart[2 * c] = 0.0; a.cpart[2 * c + 1] = 0.0; }
+      continue;
+    }
+    const double d = (a.diag && inr) ? a.diag[row] : 0.0;
+    double2 y = make_double2(0.0, 0.0);
+    for (int sp = 0; sp < a.S; ++sp) {
+      const double ds = sp == 0 ? d : 0.0;
+      double2 acc = make_double2(ds * pv.x, ds * pv.y);
+      const uint32_t L = __ldg(a.len + c * a.S + sp);
+      const uint64_t base = __ldg(a.off + c * a.S + sp) + lane;
+      const uint32_t* __restrict__ cp = a.cols + base;
+      const double* __restrict__ ap = a.amps + base;
+      // software pipeline: the next U slots' (column, element) loads are in
+      // flight while this group's psi gathers return (the stream and the
+      // gathers would otherwise serialize: ncu, 91 % of cycles without an
+      // eligible warp at U = 4 unpipelined).  12 B per slot: an 8 B form
+      // (column + code into a value table) read 8.0 instead of 10.1 GB but was
+      // slower (1.69 vs 1.58 ms): the extra gather made it L1-bound (91 %).
+      const uint32_t Lu = L / U * U;
+      uint32_t q[U];
+      double m[U];
+      if (Lu > 0) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          q[u] = __ldcs(cp + (uint64_t)u * 32);
+          m[u] = __ldcs(ap + (uint64_t)u * 32);
+        }
+      }
+      for (uint32_t j = 0; j < Lu; j += U) {
+        double2 p[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) p[u] = a.psi[q[u]];
+        uint32_t qn[U];
+        double mn[U];
+        const bool more = j + U < Lu;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          qn[u] = more ? __ldcs(cp + (uint64_t)(j + U + u) * 32) : 0u;
+          mn[u] = more ? __ldcs(ap + (uint64_t)(j + U + u) * 32) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          acc.x = fma(m[u], p[u].x, acc.x);
+          acc.y = fma(m[u], p[u].y, acc.y);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) { q[u] = qn[u]; m[u] = mn[u]; }
+      }
+      for (uint32_t j = Lu; j < L; ++j) {
+        const uint32_t qq = __ldcs(cp + (uint64_t)j * 32);
+        const double mm = __ldcs(ap + (uint64_t)j * 32);
+        const double2 pp = a.psi[qq];
+        acc.x = fma(mm, pp.x, acc.x);
+        acc.y = fma(mm, pp.y, acc.y);
+      }
+      if (sp == 0) {
+        y = acc;
+      } else {
+        y.x += acc.x;
+        y.y += acc.y;
+      }
+    }
+    if (inr && a.out && !a.energy_only) {
+      double2 v = y;
+      if (a.prune > 0.0 && sqrt(v.x * v.x + v.y * v.y) < a.prune) v = make_double2(0.0, 0.0);
+      put_row(a.out, a.peer_rows, a.n_peer_rows, row, v);
+    }
+    if (a.cpart) {   // this chunk's <psi|H psi> share, summed in chunk order
+      double er = 0.0, ei = 0.0;
+      if (inr) {
+        er = pv.x * y.x + pv.y * y.y;
+        ei = pv.x * y.y - pv.y * y.x;
+      }
+      er = warp_sum(er);
+      ei = warp_sum(ei);
+      if (lane == 0) { a.cpart[2 * c] = er; a.cpart[2 * c + 1] = ei; }
+    }
+  }
+}
+
+static void free_sell(hsv_op_s::Sell& m) {
+  dfree(m.cols); dfree(m.amps); dfree(m.off); dfree(m.len);
+  m.cols = nullptr; m.amps = nullptr; m.off = nullptr; m.len = nullptr;
+}
+
+static void drop_sells(hsv_op_s* op) {
+  for (auto& m : op->sells) free_sell(m);
+  op->sells.clear();
+  op->sell_declined.clear();
+  free_sell(op->sup);
+  dfree(op->sup_rows);
+  op->sup_rows = nullptr;
+  op->sup_version = 0;
+}
+
+// Enumerate rows [a0.a_lo, a0.a_hi) with K1's EM modes into m (m.cols == nullptr:
+// declined, over the budget left after `held` bytes of other ranges).
+template <typename W, int SH>
+static int build_sell_t(hsv_op_s* op, const ApplyArgs& a0, int S, int64_t held,
+                        hsv_op_s::Sell& m) {
+  const hsv_sector_s* s = op->sec;
+  const int64_t rows = (a0.a_hi - a0.a_lo) * s->Nb;
+  const int64_t n_chunks = (rows + 31) / 32;
+  const int64_t nl = n_chunks * S;
+  uint32_t* cnt = nullptr;
+  uint64_t* sz = nullptr;
+  HSV_TRY(dalloc(&cnt, rows * S));
+  HSV_TRY(dalloc(&m.len, nl));
+  HSV_TRY(dalloc(&m.off, nl + 1));
+  HSV_TRY(dalloc(&sz, nl + 1));
+  ApplyArgs a = a0;
+  a.psi = nullptr; a.out = nullptr; a.epart = nullptr; a.arow = nullptr; a.diag = nullptr;
+  a.peer_rows = nullptr; a.n_peer_rows = 0; a.prune = 0.0; a.energy_only = 0;
+  a.nsplit = S;
+  a.sell_cnt = cnt;
+  const bool bp = op->d_bperm && tuning().bperm != 0 && !s->wide;
+  a.bperm = op->d_bperm;   // (launch_apply sets it only on its own K1 branch)
+  a.rb0_n = 0;
+  if (bp) HSV_TRY((launch_apply_t<W, SH, 8, 2, 2, 0, 1>(op, a, nullptr)));
+  else HSV_TRY((launch_apply_t<W, SH, 8, 2, 0, 0, 1>(op, a, nullptr)));
+  k_sell_len<<<(unsigned)((nl + 255) / 256), 256, 0, stream()>>>(cnt, rows, S, n_chunks, m.len, sz);
+  HSV_TRY_CUDA(cudaMemsetAsync(sz + nl, 0, sizeof(uint64_t), stream()));
+  count_launch();
+  size_t tb = 0;
+  HSV_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, sz, m.off, nl + 1, stream()));
+  unsigned char* tmp = nullptr;
+  HSV_TRY(dalloc(&tmp, std::max<size_t>(tb, 1)));
+  HSV_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, sz, m.off, nl + 1, stream()));
+  uint64_t total = 0;
+  HSV_TRY_CUDA(cudaMemcpyAsync(&total, m.off + nl, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                               stream()));
+  HSV_TRY(stream_sync());
+  dfree(tmp); dfree(sz); dfree(cnt);
+  const int64_t bytes = (int64_t)total * 12;
+  if (held + bytes > tuning().sell_budget_mb * (1ll << 20) ||
+      dalloc(&m.cols, std::max<uint64_t>(total, 1)) != HSV_OK ||
+      dalloc(&m.amps, std::max<uint64_t>(total, 1)) != HSV_OK) {
+    free_sell(m);
+    return HSV_OK;
+  }
+  // padding slots: column 0, element 0.0 (fma(0, psi, acc) == acc up to the sign of a zero)
+  HSV_TRY_CUDA(cudaMemsetAsync(m.cols, 0, total * sizeof(uint32_t), stream()));
+  HSV_TRY_CUDA(cudaMemsetAsync(m.amps, 0, total * sizeof(double), stream()));
+  a.sell_cnt = nullptr;
+  a.sell_off = m.off;
+  a.sell_cols = m.cols;
+  a.sell_amps = m.amps;
+  if (bp) HSV_TRY((launch_apply_t<W, SH, 8, 2, 2, 0, 2>(op, a, nullptr)));
+  else HSV_TRY((launch_apply_t<W, SH, 8, 2, 0, 0, 2>(op, a, nullptr)));
+  m.lo = a0.a_lo;
+  m.hi = a0.a_hi;
+  m.chunks = n_chunks;
+  m.entries = (int64_t)total;
+  m.S = S;
+  return HSV_OK;
+}
+
+// The range's assembled rows, built on first use when they fit (nullptr: not
+// assembled -- over the budget, declined before, or K1a off).
+static int get_sell(hsv_op_s* op, const ApplyArgs& a, int S, hsv_op_s::Sell** out) {
+  *out = nullptr;
+  if (tuning().sell == 0 || a.a_hi <= a.a_lo) return HSV_OK;
+  const hsv_sector_s* s = op->sec;
+  for (const int4& d : op->sell_declined)
+    if (d.x == (int)a.a_lo && d.y == (int)a.a_hi && d.z == S) return HSV_OK;
+  for (auto& x : op->sells)
+    if (x.lo == a.a_lo && x.hi == a.a_hi && x.S == S) {
+      *out = &x;
+      return HSV_OK;
+    }
+  const int64_t rows = (a.a_hi - a.a_lo) * s->Nb;
+  const double budget = (double)tuning().sell_budget_mb * (double)(1ll << 20);
+  // cheap bound first (every (row, active group) pair stored), then the exact count
+  if ((double)rows * (double)op->n_active * 12.0 > 4.0 * budget) {
+    op->sell_declined.push_back(make_int4((int)a.a_lo, (int)a.a_hi, S, 0));
+    return HSV_OK;
+  }
+  while (op->sells.size() >= 2) {   // keep at most two ranges: drop the oldest
+    free_sell(op->sells.front());
+    op->sells.erase(op->sells.begin());
+  }
+  int64_t held = 0;
+  for (auto& x : op->sells) held += x.entries * 12;
+  hsv_op_s::Sell nm;
+  if (s->wide) HSV_TRY((build_sell_t<uint64_t, 32>(op, a, S, held, nm)));
+  else HSV_TRY((build_sell_t<uint32_t, 16>(op, a, S, held, nm)));
+  if (!nm.cols) {
+    op->sell_declined.push_back(make_int4((int)a.a_lo, (int)a.a_hi, S, 0));
+    return HSV_OK;
+  }
+  op->sells.push_back(nm);
+  *out = &op->sells.back();
+  return HSV_OK;
+}
+
+static int run_sell(const hsv_op_s* op, const hsv_op_s::Sell& m, const ApplyArgs& a, int S,
+                    const uint32_t* rlist, int64_t list_n, const char* scope) {
+  SellArgs g{};
+  g.cols = m.cols; g.amps = m.amps; g.off = m.off; g.len = m.len;
+  g.n_chunks = m.chunks;
+  g.rows = rlist ? list_n : (a.a_hi - a.a_lo) * op->sec->Nb;
+  g.row0 = a.a_lo * op->sec->Nb;
+  g.rlist = rlist;
+  g.S = S;
+  g.psi = a.psi; g.diag = a.diag; g.out = a.out; g.prune = a.prune; g.energy_only = a.energy_only;
+  g.peer_rows = a.peer_rows; g.n_peer_rows = a.n_peer_rows;
+  double* cpart = nullptr;
+  if (a.epart) {
+    HSV_TRY(dalloc(&cpart, 2 * std::max<int64_t>(g.n_chunks, 1)));
+    g.cpart = cpart;
+  }
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((g.n_chunks + 7) / 8,
+                                                              (int64_t)ctx().num_sms * 16));
+  {
+    ProfScope prof(scope);
+    switch (tuning().sell_kernel) {   // (elements per pipeline stage, blocks per SM)
+      case 1: k_apply_sell<4, 6><<<(unsigned)grid, 256, 0, stream()>>>(g); break;
+      case 2: k_apply_sell<8, 3><<<(unsigned)grid, 256, 0, stream()>>>(g); break;
+      case 3: k_apply_sell<8, 4><<<(unsigned)grid, 256, 0, stream()>>>(g); break;
+      case 4: k_apply_sell<2, 8><<<(unsigned)grid, 256, 0, stream()>>>(g); break;
+      default: k_apply_sell<4, 4><<<(unsigned)grid, 256, 0, stream()>>>(g); break;
+    }
+  }
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  if (cpart) HSV_TRY(reduce_sum_f64(cpart, g.n_chunks, 2, 2, a.epart));
+  dfree(cpart);
+  return HSV_OK;
+}
+
+// K1a: run the assembled rows when they exist (or can be built) for this row
+// range and split count; *done = false leaves the launch to K1.
+static int launch_apply_sell(const hsv_op_s* cop, const ApplyArgs& a, int S, int64_t* n_warps,
+                             bool* done) {
+  *done = false;
+  if (!a.out && !a.epart) return HSV_OK;
+  hsv_op_s* op = const_cast<hsv_op_s*>(cop);
+  hsv_op_s::Sell* m = nullptr;
+  HSV_TRY(get_sell(op, a, S, &m));
+  if (!m) return HSV_OK;
+  HSV_TRY(run_sell(op, *m, a, S, nullptr, 0, "apply"));
+  if (n_warps) *n_warps = 1;   // epart[0..1] holds the total
+  *done = true;
+  return HSV_OK;
+}
+
+// ------------------------------------------------------ K1s (support rows)
+// One thread per support row: count (EMIT = false) or copy (true) the row's
+// elements whose partner is in the support map, split by split, in order.
+template <bool EMIT>
+__global__ void k_sup_rows(const uint32_t* __restrict__ list, int64_t n_s, int S,
+                           const uint32_t* __restrict__ cols, const double* __restrict__ amps,
+                           const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
+                           const uint8_t* __restrict__ smap, uint32_t* __restrict__ cnt,
+                           const uint64_t* __restrict__ off2, uint32_t* __restrict__ cols2,
+                           double* __restrict__ amps2) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n_s) return;
+  const uint32_t rl = __ldg(list + i);
+  const uint64_t c = rl >> 5, l = rl & 31u;
+  for (int sp = 0; sp < S; ++sp) {
+    const uint32_t L = __ldg(len + c * S + sp);
+    const uint64_t base = __ldg(off + c * S + sp) + l;
+    uint64_t o = EMIT ? __ldg(off2 + (uint64_t)(i >> 5) * S + sp) + (uint64_t)(i & 31) : 0;
+    uint32_t n = 0;
+    for (uint32_t j = 0; j < L; ++j) {
+      const uint64_t idx = base + (uint64_t)j * 32;
+      const double v = __ldg(amps + idx);
+      if (v == 0.0) continue;                  // padding
+      const uint32_t q = __ldg(cols + idx);
+      if (!__ldg(smap + q)) continue;          // partner outside the map: psi is 0 there
+      if (EMIT) {
+        cols2[o] = q;
+        amps2[o] = v;
+        o += 32;
+      } else {
+        ++n;
+      }
+    }
+    if (!EMIT) cnt[(uint64_t)i * S + sp] = n;
+  }
+}
+
+static int build_sup(hsv_op_s* op, const hsv_op_s::Sell& m, const ApplyArgs& a, int S,
+                     const uint8_t* smap, uint64_t version, int64_t held) {
+  hsv_op_s::Sell& u = op->sup;
+  free_sell(u);
+  dfree(op->sup_rows);
+  op->sup_rows = nullptr;
+  op->sup_version = 0;
+  const int64_t Nb = op->sec->Nb;
+  const int64_t rows = (a.a_hi - a.a_lo) * Nb;
+  const int64_t row0 = a.a_lo * Nb;
+  int* d_n = nullptr;
+  HSV_TRY(dalloc(&op->sup_rows, std::max<int64_t>(rows, 1)));
+  HSV_TRY(dalloc(&d_n, 1));
+  size_t tb = 0;
+  cub::CountingInputIterator<uint32_t> it(0);
+  HSV_TRY_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, smap + row0, op->sup_rows, d_n,
+                                          (int)rows, stream()));
+  unsigned char* tmp = nullptr;
+  HSV_TRY(dalloc(&tmp, std::max<size_t>(tb, 1)));
+  HSV_TRY_CUDA(cub::DeviceSelect::Flagged(tmp, tb, it, smap + row0, op->sup_rows, d_n,
+                                          (int)rows, stream()));
+  int n_s = 0;
+  HSV_TRY_CUDA(cudaMemcpyAsync(&n_s, d_n, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+  HSV_TRY(stream_sync());
+  dfree(tmp); dfree(d_n);
+  const int64_t chunks = (n_s + 31) / 32;
+  const int64_t nl = chunks * S;
+  uint32_t* cnt = nullptr;
+  uint64_t* sz = nullptr;
+  HSV_TRY(dalloc(&cnt, std::max<int64_t>((int64_t)n_s * S, 1)));
+  HSV_TRY(dalloc(&u.len, std::max<int64_t>(nl, 1)));
+  HSV_TRY(dalloc(&u.off, nl + 1));
+  HSV_TRY(dalloc(&sz, nl + 1));
+  const unsigned gb = (unsigned)std::max<int64_t>(1, (n_s + 255) / 256);
+  if (n_s)
+    k_sup_rows<false><<<gb, 256, 0, stream()>>>(op->sup_rows, n_s, S, m.cols, m.amps, m.off,
+                                                 m.len, smap, cnt, nullptr, nullptr, nullptr);
+  if (nl)
+    k_sell_len<<<(unsigned)((nl + 255) / 256), 256, 0, stream()>>>(cnt, n_s, S, chunks, u.len, sz);
+  HSV_TRY_CUDA(cudaMemsetAsync(sz + nl, 0, sizeof(uint64_t), stream()));
+  tb = 0;
+  HSV_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, sz, u.off, nl + 1, stream()));
+  HSV_TRY(dalloc(&tmp, std::max<size_t>(tb, 1)));
+  HSV_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, sz, u.off, nl + 1, stream()));
+  uint64_t total = 0;
+  HSV_TRY_CUDA(cudaMemcpyAsync(&total, u.off + nl, sizeof(uint64_t), cudaMemcpyDeviceToHost,
+                               stream()));
+  HSV_TRY(stream_sync());
+  dfree(tmp); dfree(sz); dfree(cnt);
+  if (held + (int64_t)total * 12 > tuning().sell_budget_mb * (1ll << 20) ||
+      dalloc(&u.cols, std::max<uint64_t>(total, 1)) != HSV_OK ||
+      dalloc(&u.amps, std::max<uint64_t>(total, 1)) != HSV_OK) {
+    free_sell(u);
+    return HSV_OK;
+  }
+  HSV_TRY_CUDA(cudaMemsetAsync(u.cols, 0, total * sizeof(uint32_t), stream()));
+  HSV_TRY_CUDA(cudaMemsetAsync(u.amps, 0, total * sizeof(double), stream()));
+  if (n_s)
+    k_sup_rows<true><<<gb, 256, 0, stream()>>>(op->sup_rows, n_s, S, m.cols, m.amps, m.off,
+                                                m.len, smap, nullptr, u.off, u.cols, u.amps);
+  count_launch(n_s ? 3 : 1);
+  HSV_CHECK_LAUNCH();
+  u.lo = a.a_lo; u.hi = a.a_hi; u.S = S; u.chunks = chunks; u.entries = (int64_t)total;
+  op->sup_n = n_s;
+  op->sup_version = version;
+  return HSV_OK;
+}
+
+// K1s: K1r from the support-compacted assembled rows; *done = false leaves the
+// launch to the matrix-free K1r.
+static int launch_apply_sup(const hsv_op_s* cop, const ApplyArgs& a, int S, const uint8_t* smap,
+                            uint64_t version, bool* done) {
+  *done = false;
+  hsv_op_s* op = const_cast<hsv_op_s*>(cop);
+  if (!smap || !version || !a.out || a.n_peer_rows > 0) return HSV_OK;
+  hsv_op_s::Sell* m = nullptr;
+  HSV_TRY(get_sell(op, a, S, &m));
+  if (!m) return HSV_OK;
+  hsv_op_s::Sell& u = op->sup;
+  if (op->sup_version != version || u.lo != a.a_lo || u.hi != a.a_hi || u.S != S || !u.cols) {
+    ProfScope prof("sup_build");
+    int64_t held = 0;
+    for (auto& x : op->sells) held += x.entries * 12;
+    HSV_TRY(build_sup(op, *m, a, S, smap, version, held));
+    if (!u.cols) return HSV_OK;
+  }
+  const int64_t rows = (a.a_hi - a.a_lo) * op->sec->Nb;
+  // rows outside the support are exact zeros (K1r's contract)
+  HSV_TRY_CUDA(cudaMemsetAsync(a.out + a.a_lo * op->sec->Nb, 0, rows * sizeof(double2), stream()));
+  ApplyArgs b = a;
+  b.epart = nullptr;
+  HSV_TRY(run_sell(op, u, b, S, op->sup_rows, op->sup_n, "apply_rows"));
+  *done = true;
+  return HSV_OK;
+}
+
 int apply_warps(const hsv_op_s* op) {
   // upper bound on the warps the apply kernel uses (energy-partial sizing):
   // 256-thread blocks, at most 8 resident per SM
@@ -566,6 +1045,11 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
   if (tuning().push != 0) {   // sparse psi: scatter + sort-reduce (hsv_push.cu)
     bool done = false;
     HSV_TRY(launch_push(op, a, &done, n_warps, dense_hint));
+    if (done) return HSV_OK;
+  }
+  {   // K1a: assembled rows (built on first use where they fit)
+    bool done = false;
+    HSV_TRY(launch_apply_sell(op, a, k1_default_split(op, a_lo, a_hi, true), n_warps, &done));
     if (done) return HSV_OK;
   }
   if (tuning().staged != 1) {   // K1t: alpha tiles (hsv_apply_t.cu)
@@ -728,7 +1212,7 @@ void RowList::release() {
 
 int launch_apply_rows(const hsv_op_s* op, const double2* psi, double2* out, int64_t a_lo,
                       int64_t a_hi, const uint32_t* arow, const uint8_t* smap,
-                      int64_t support_rows) {
+                      int64_t support_rows, uint64_t smap_version) {
   const hsv_sector_s* s = op->sec;
   HSV_REQUIRE(s->dim < ((int64_t)1 << 32), HSV_ERR_UNSUPPORTED,
               "sector dimension %lld exceeds the 32-bit row index of the apply kernel",
@@ -749,6 +1233,11 @@ int launch_apply_rows(const hsv_op_s* op, const double2* psi, double2* out, int6
   // rows per lane: 8 while the full row range gives a 256-row unit to every
   // resident warp (the full kernel's rule), else 4
   const int S = k1_default_split(op, a_lo, a_hi, true);
+  {   // K1s: the support-compacted assembled rows (built once per support map)
+    bool done = false;
+    HSV_TRY(launch_apply_sup(op, a, S, smap, smap_version, &done));
+    if (done) return HSV_OK;
+  }
   {   // K1v over the support rows (hsv_apply_v.cu)
     bool done = false;
     ApplyArgs av = a;
@@ -1483,7 +1972,18 @@ int hsv_op_destroy(hsv_op op) {
   dfree(op->d_vl);
   dfree(op->d_vloff);
   dfree(op->d_vgslot);
+  drop_sells(op);
   delete op;
+  return HSV_OK;
+}
+
+int hsv_op_sell_info(hsv_op op, int64_t a_lo, int64_t a_hi, int64_t* slots, int64_t* splits) {
+  HSV_REQUIRE(op, HSV_ERR_INVALID, "null operator");
+  int64_t n = 0, S = 0;
+  for (const auto& m : op->sells)
+    if (m.lo == a_lo && m.hi == a_hi) { n = m.entries; S = m.S; }
+  if (slots) *slots = n;
+  if (splits) *splits = S;
   return HSV_OK;
 }
 

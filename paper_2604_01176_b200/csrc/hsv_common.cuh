@@ -213,6 +213,28 @@ struct hsv_op_s {
   // host copies of the active group table (for CSR materialization)
   std::vector<int4> buckets, groups;
   std::vector<Term> terms;
+  // K1a: alpha-string rows [lo, hi) assembled once as a sliced ELL matrix
+  // (chunks of 32 rows, entry j of a chunk's lane at off + 32 j), one segment
+  // per bucket split in K1's accumulation order (hsv_apply.cu build_sell).
+  // A few row ranges are kept (a rank's shard and the full range); declined
+  // ranges (over the budget) are remembered so they are not counted again.
+  struct Sell {
+    int64_t lo = 0, hi = 0, chunks = 0, entries = 0;
+    int S = 1;
+    uint32_t* cols = nullptr;
+    double* amps = nullptr;
+    uint64_t* off = nullptr;   // [chunk][split]
+    uint32_t* len = nullptr;   // [chunk][split] entries per lane
+  };
+  std::vector<Sell> sells;
+  std::vector<int4> sell_declined;   // {lo, hi, S, 0}
+  // K1s: the support rows of one sweep plan's map, with only the elements whose
+  // partner is in the map (psi is exactly zero elsewhere), compacted from the
+  // range's K1a rows; rebuilt when the map changes (once per ADAPT iteration)
+  Sell sup;
+  uint32_t* sup_rows = nullptr;      // local rows of the support, ascending
+  int64_t sup_n = 0;
+  uint64_t sup_version = 0;
 };
 
 struct hsv_pool_s {

@@ -17,6 +17,11 @@ struct Tuning {
   int push_keys = 32;     // auto: push while nnz(psi) * (1 + groups) <= push_keys * rows - 2^20
   int sweep = 2;          // adjoint/forward sweeps: 2 batched (orbits of kBatch rotations per
                           // grid barrier, hsv_sweep.cu), 1 one barrier per rotation, 0 launch per op
+  int sell = -1;          // K1a (assembled sliced-ELL rows, built once per operator and
+                          // row range when it fits sell_budget_mb): -1/1 on, 0 off
+  int64_t sell_budget_mb = 32768;
+  int sell_kernel = 3;    // K1a variant (elements per stage, blocks per SM): 0 (4,4) 1 (4,6)
+                          // 2 (8,3) 3 (8,4) 4 (2,8); H12: 1.74 1.70 1.72 1.58 1.85 ms
   int sweep_bar = 0;      // batched sweep barrier: 0 grid.sync(), 1 counting (release/acquire;
                           // measured equal at H12 depth 100/400, profiles/r02/sweep_probe_bar.jsonl)
   int sweep_threads = 256;   // batched sweep block size (128 or 256)
@@ -104,6 +109,12 @@ struct ApplyArgs {
   int vl_chunk, vl_nchunks;
   const uint8_t* smap;     // K1v row-restricted mode: rows outside the map are skipped
   const uint32_t* vgslot;  // K1v: per group, its list's offset slot
+  // K1 enumeration modes (SELL build, hsv_apply.cu): per (row, split) entry
+  // counts, or the entries themselves at their sliced-ELL slots
+  uint32_t* sell_cnt;        // [row - a_lo*Nb][split]
+  const uint64_t* sell_off;  // [chunk][split] first slot (lane 0) of the segment
+  uint32_t* sell_cols;
+  double* sell_amps;
 };
 
 // K1r: row lists of the rows marked in smap (or, smap == nullptr, of the
@@ -196,7 +207,7 @@ int launch_apply(const hsv_op_s* op, const double2* psi, double2* out, double* e
 // 0 on every other row of [a_lo, a_hi); no energy partials.
 int launch_apply_rows(const hsv_op_s* op, const double2* psi, double2* out, int64_t a_lo,
                       int64_t a_hi, const uint32_t* arow, const uint8_t* smap,
-                      int64_t support_rows = -1);
+                      int64_t support_rows = -1, uint64_t smap_version = 0);
 
 // Compressed QEB masks of one excitation operator.
 struct OpMasks {
@@ -221,6 +232,8 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
 int smap_arow_async(const hsv_sector_s* sec, const uint8_t* smap, uint32_t* flags);
 // rows of the cached plan's support map (-1: no plan for this sector)
 int64_t sweep_plan_support(const hsv_sector_s* s);
+// identity of the cached plan's support map contents (0: none)
+uint64_t sweep_plan_version(const hsv_sector_s* s);
 // drop the cached sweep plan (of sector s only, when s != nullptr)
 void release_sweep_plans(const hsv_sector_s* s = nullptr);
 

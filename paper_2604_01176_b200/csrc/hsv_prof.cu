@@ -116,6 +116,15 @@ int hsv_set_tuning(const char* key, int64_t value) {
   } else if (k == "staged") {
     HSV_REQUIRE(value == 0 || value == 1, HSV_ERR_INVALID, "staged must be 0 or 1");
     g_tuning.staged = (int)value;
+  } else if (k == "sell") {
+    HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "sell must be -1, 0 or 1");
+    g_tuning.sell = (int)value;
+  } else if (k == "sell_kernel") {
+    HSV_REQUIRE(value >= 0 && value <= 4, HSV_ERR_INVALID, "sell_kernel must be 0..4");
+    g_tuning.sell_kernel = (int)value;
+  } else if (k == "sell_budget_mb") {
+    HSV_REQUIRE(value >= 0, HSV_ERR_INVALID, "sell_budget_mb must be >= 0");
+    g_tuning.sell_budget_mb = value;
   } else if (k == "sweep_bar") {
     HSV_REQUIRE(value == 0 || value == 1, HSV_ERR_INVALID, "sweep_bar must be 0 or 1");
     g_tuning.sweep_bar = (int)value;

@@ -770,7 +770,7 @@ int hsv_eg_forward_async(hsv_op op, uint64_t hf_key, const uint64_t* occ, const 
   HostProf hk("k1r_launch");
   if (rows_only && psi->smap_valid)
     HSV_TRY(launch_apply_rows(op, psi->d_amp, w->d_amp, a_lo, a_hi, psi->d_arow, psi->d_smap,
-                              sweep_plan_support(sec)));
+                              sweep_plan_support(sec), sweep_plan_version(sec)));
   else
     HSV_TRY(launch_apply(op, psi->d_amp, w->d_amp, nullptr, a_lo, a_hi, 0.0, 0, &used,
                          psi->d_arow, &psi->dense_hint));

@@ -804,6 +804,7 @@ struct Plan {
   int64_t* chunk_off = nullptr;    // batch -> first chunk
   int64_t n_chunks = 0;
   int64_t support_rows = 0;    // rows of the support map (HF closure)
+  uint64_t version = 0;        // changes whenever the support map does (K1s caches on it)
   uint32_t* added = nullptr;   // rows each batch added to the map, batch after batch (dim)
   std::vector<int64_t> added_end;   // per batch: rows added by batches <= it
   bool has_ranks = false;
@@ -1074,6 +1075,8 @@ int filter_plan(Plan& P, int first) {
     P.max_live = std::max<int64_t>(P.max_live, hl[q]);
   }
   P.support_rows = 1 + P.added_end.back();   // HF + the rows the batches added
+  static uint64_t g_version = 0;
+  P.version = ++g_version;
   const int64_t n_live = cmp[nn];
   const int64_t keep_slots = P.live_off[first];
   const int64_t n_slots = P.live_off[nb];
@@ -1313,6 +1316,11 @@ int launch_bsweep(const hsv_sector_s* sec, int mode, int64_t hf_row,
 int64_t sweep_plan_support(const hsv_sector_s* s) {
   const Plan& P = plan();
   return P.sec == s && P.filtered ? P.support_rows : -1;
+}
+
+uint64_t sweep_plan_version(const hsv_sector_s* s) {
+  const Plan& P = plan();
+  return P.sec == s && P.filtered ? P.version : 0;
 }
 
 void release_sweep_plans(const hsv_sector_s* s) {

@@ -1,0 +1,97 @@
+"""K1a (assembled sliced-ELL rows, csrc/hsv_apply.cu k_apply_sell) against the
+matrix-free K1 it is enumerated from: H|psi> rows bit for bit (same split
+partials, same FMA order, exact zeros dropped), on dense real and complex
+states, on alpha-row shards, with the drop rule, and through the ADAPT screen;
+energies to rounding (the partial sums are grouped per 32-row chunk)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def hsv():
+    import paper_2604_01176_b200 as hsv
+    return hsv
+
+
+@pytest.fixture()
+def N():
+    from paper_2604_01176_b200 import _native as N
+    yield N
+    N.call("hsv_set_tuning", b"sell", -1)
+
+
+def dense(hsv, basis, v):
+    n = len(basis)
+    return hsv.SvState(basis, hsv.SparseVector(n, np.arange(n), v))
+
+
+def both(N, fn):
+    N.call("hsv_set_tuning", b"sell", 0)
+    r0 = fn()
+    N.call("hsv_set_tuning", b"sell", 1)
+    r1 = fn()
+    return r0, r1
+
+
+@pytest.mark.parametrize("name", ["h4", "h6", "h8", "h10", "h12"])
+@pytest.mark.parametrize("cplx", [False, True])
+def test_sell_rows_bitwise_equal_k1(hsv, N, name, cplx):
+    sysm = hsv.MolecularSystem.bundled(name)
+    op = hsv.assemble_subspace_hamiltonian(sysm.hamiltonian, sysm.basis)
+    rng = np.random.default_rng(5)
+    n = len(sysm.basis)
+    v = rng.standard_normal(n) + (1j * rng.standard_normal(n) if cplx else 0.0)
+    v /= np.linalg.norm(v)
+    st = dense(hsv, sysm.basis, v)
+    (w0, e0), (w1, e1) = both(N, lambda: (op.apply_state(st).to_sparse().to_dense(), op.expect(st)))
+    assert np.array_equal(w0, w1)
+    assert abs(e1 - e0) <= 1e-13 * max(1.0, abs(e0))
+    # the drop rule on the combined rows
+    thr = float(np.quantile(np.abs(w0), 0.3))
+    p0, p1 = both(N, lambda: op.apply_state(st, prune=thr).to_sparse())
+    assert np.array_equal(p0.indices, p1.indices) and np.array_equal(p0.values, p1.values)
+
+
+@pytest.mark.parametrize("name", ["h8", "h12"])
+def test_sell_alpha_shards_and_screen(hsv, N, name):
+    """Rank shards (alpha-row ranges, the multi-GPU owner-computes split) build
+    their own assembled rows; the screen's gradients are bitwise equal."""
+    from paper_2604_01176_b200.svengine import DeviceState
+    sysm = hsv.MolecularSystem.bundled(name)
+    op = hsv.assemble_subspace_hamiltonian(sysm.hamiltonian, sysm.basis)
+    na = sysm.basis._sector.n_alpha_strings
+    rng = np.random.default_rng(9)
+    n = len(sysm.basis)
+    v = rng.standard_normal(n)
+    v /= np.linalg.norm(v)
+    st = dense(hsv, sysm.basis, v)
+    cuts = [0, na // 3, na // 3 + 1, na]
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        def shard():
+            out = DeviceState(sysm.basis)
+            N.call("hsv_apply_h_rows_async", op.handle, st.device.handle, out.handle, lo, hi, 0.0)
+            N.call("hsv_synchronize")
+            return out.to_sparse().to_dense()
+        r0, r1 = both(N, shard)
+        assert np.array_equal(r0, r1), (lo, hi)
+    pool = hsv.build_qeb_pool(sysm.n_qubits, sysm.integrals.nelec)
+    eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
+    (ea, ga), (eb, gb) = both(N, lambda: eng.energy_and_screen(st, pool))
+    assert np.array_equal(ga, gb)
+    assert abs(ea - eb) <= 1e-13 * max(1.0, abs(ea))
+
+
+def test_sell_declines_over_budget(hsv, N):
+    """Over the budget nothing is built and K1 runs (same rows)."""
+    sysm = hsv.MolecularSystem.bundled("h8")
+    op = hsv.assemble_subspace_hamiltonian(sysm.hamiltonian, sysm.basis)
+    n = len(sysm.basis)
+    st = dense(hsv, sysm.basis, np.full(n, 1.0 / np.sqrt(n)))
+    N.call("hsv_set_tuning", b"sell_budget_mb", 0)
+    try:
+        (w0, _), (w1, _) = both(N, lambda: (op.apply_state(st).to_sparse().to_dense(), 0))
+        assert np.array_equal(w0, w1)
+    finally:
+        N.call("hsv_set_tuning", b"sell_budget_mb", 32768)

@@ -18,7 +18,7 @@ sys.path.insert(0, str(ROOT))
 import paper_2604_01176_b200 as hsv  # noqa: E402
 from paper_2604_01176_b200 import _native as N  # noqa: E402
 
-KERNELS = ("qeb", "adjoint", "apply_rows", "apply", "push", "push_collect",
+KERNELS = ("qeb", "adjoint", "apply_rows", "apply", "push", "push_collect", "sup_build",
            "h:eg_fwd", "h:fwd_psi", "h:get_plan", "h:k1r_launch", "h:eg_bwd", "h:bwd_wait")
 
 
