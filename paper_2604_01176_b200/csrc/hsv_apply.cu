@@ -717,8 +717,8 @@ __global__ void __launch_bounds__(256, MINB) k_apply_sell(const SellArgs a) {
 }
 
 static void free_sell(hsv_op_s::Sell& m) {
-  dfree(m.cols); dfree(m.amps); dfree(m.off); dfree(m.len);
-  m.cols = nullptr; m.amps = nullptr; m.off = nullptr; m.len = nullptr;
+  dfree(m.cols); dfree(m.amps); dfree(m.rcnt); dfree(m.off); dfree(m.len);
+  m.cols = nullptr; m.amps = nullptr; m.rcnt = nullptr; m.off = nullptr; m.len = nullptr;
 }
 
 static void drop_sells(hsv_op_s* op) {
@@ -768,7 +768,8 @@ static int build_sell_t(hsv_op_s* op, const ApplyArgs& a0, int S, int64_t held,
   HSV_TRY_CUDA(cudaMemcpyAsync(&total, m.off + nl, sizeof(uint64_t), cudaMemcpyDeviceToHost,
                                stream()));
   HSV_TRY(stream_sync());
-  dfree(tmp); dfree(sz); dfree(cnt);
+  dfree(tmp); dfree(sz);
+  m.rcnt = cnt;   // kept: the K1s build skips the padding by it
   const int64_t bytes = (int64_t)total * 12;
   if (held + bytes > tuning().sell_budget_mb * (1ll << 20) ||
       dalloc(&m.cols, std::max<uint64_t>(total, 1)) != HSV_OK ||
@@ -883,39 +884,74 @@ static int launch_apply_sell(const hsv_op_s* cop, const ApplyArgs& a, int S, int
 }
 
 // ------------------------------------------------------ K1s (support rows)
-// One thread per support row: count (EMIT = false) or copy (true) the row's
-// elements whose partner is in the support map, split by split, in order.
+// Warp per 32-row chunk of the range's assembled rows (coalesced): the rows in
+// the support map keep, split by split and in order, the elements whose partner
+// is in the map (psi is exactly zero elsewhere).  Pass 1 lists the support rows
+// and counts; pass 2 copies into the compacted sliced-ELL rows (list order, so
+// a chunk's rows land in one or two compacted chunks).
+__global__ void k_sup_chunk_count(const uint8_t* __restrict__ smap, int64_t row0, int64_t rows,
+                                  int64_t n_chunks, uint32_t* __restrict__ ccount) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (c >= n_chunks) return;
+  const int64_t rl = c * 32 + lane;
+  const unsigned b = __ballot_sync(0xffffffffu, rl < rows && smap[row0 + rl] != 0);
+  if (lane == 0) ccount[c] = __popc(b);
+}
+
 template <bool EMIT>
-__global__ void k_sup_rows(const uint32_t* __restrict__ list, int64_t n_s, int S,
-                           const uint32_t* __restrict__ cols, const double* __restrict__ amps,
-                           const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
-                           const uint8_t* __restrict__ smap, uint32_t* __restrict__ cnt,
-                           const uint64_t* __restrict__ off2, uint32_t* __restrict__ cols2,
-                           double* __restrict__ amps2) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n_s) return;
-  const uint32_t rl = __ldg(list + i);
-  const uint64_t c = rl >> 5, l = rl & 31u;
-  for (int sp = 0; sp < S; ++sp) {
-    const uint32_t L = __ldg(len + c * S + sp);
-    const uint64_t base = __ldg(off + c * S + sp) + l;
-    uint64_t o = EMIT ? __ldg(off2 + (uint64_t)(i >> 5) * S + sp) + (uint64_t)(i & 31) : 0;
-    uint32_t n = 0;
-    for (uint32_t j = 0; j < L; ++j) {
-      const uint64_t idx = base + (uint64_t)j * 32;
-      const double v = __ldg(amps + idx);
-      if (v == 0.0) continue;                  // padding
-      const uint32_t q = __ldg(cols + idx);
-      if (!__ldg(smap + q)) continue;          // partner outside the map: psi is 0 there
-      if (EMIT) {
-        cols2[o] = q;
-        amps2[o] = v;
-        o += 32;
-      } else {
-        ++n;
+__global__ void __launch_bounds__(256) k_sup_pass(
+    const uint8_t* __restrict__ smap, int64_t row0, int64_t rows, int64_t n_chunks, int S,
+    const uint32_t* __restrict__ cprefix, const uint32_t* __restrict__ cols,
+    const double* __restrict__ amps, const uint32_t* __restrict__ rcnt,
+    const uint64_t* __restrict__ off, const uint32_t* __restrict__ len,
+    uint32_t* __restrict__ list, uint32_t* __restrict__ cnt2, const uint64_t* __restrict__ off2,
+    uint32_t* __restrict__ cols2, double* __restrict__ amps2) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = gw; c < n_chunks; c += nw) {
+    const int64_t rl = c * 32 + lane;
+    const bool act = rl < rows && smap[row0 + rl] != 0;
+    const unsigned b = __ballot_sync(0xffffffffu, act);
+    if (!b) continue;
+    const uint32_t lidx = __ldg(cprefix + c) + __popc(b & ((1u << lane) - 1u));
+    if (!EMIT && act) list[lidx] = (uint32_t)rl;
+    for (int sp = 0; sp < S; ++sp) {
+      const uint32_t L = __ldg(len + c * S + sp);
+      const uint64_t base = __ldg(off + c * S + sp) + lane;
+      const uint32_t rc = act ? __ldg(rcnt + (uint64_t)rl * S + sp) : 0u;
+      uint64_t o = EMIT && act ? __ldg(off2 + (uint64_t)(lidx >> 5) * S + sp) + (lidx & 31u) : 0;
+      uint32_t n = 0;
+      // groups of 8 slots: the column loads, then the map gathers, are
+      // independent within a group (8 round trips in flight, not 1)
+      for (uint32_t j0 = 0; j0 < L; j0 += 8) {
+        uint32_t q[8];
+        double v[8];
+        bool ok[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          ok[u] = j0 + u < rc;
+          const uint64_t idx = base + (uint64_t)(j0 + u) * 32;
+          q[u] = ok[u] ? __ldcs(cols + idx) : 0u;
+          v[u] = (EMIT && ok[u]) ? __ldcs(amps + idx) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) ok[u] = ok[u] && __ldg(smap + q[u]) != 0;   // partner in the map
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (!ok[u]) continue;
+          if (EMIT) {
+            cols2[o] = q[u];
+            amps2[o] = v[u];
+            o += 32;
+          } else {
+            ++n;
+          }
+        }
       }
+      if (!EMIT && act) cnt2[(uint64_t)lidx * S + sp] = n;
     }
-    if (!EMIT) cnt[(uint64_t)i * S + sp] = n;
   }
 }
 
@@ -929,33 +965,39 @@ static int build_sup(hsv_op_s* op, const hsv_op_s::Sell& m, const ApplyArgs& a, 
   const int64_t Nb = op->sec->Nb;
   const int64_t rows = (a.a_hi - a.a_lo) * Nb;
   const int64_t row0 = a.a_lo * Nb;
-  int* d_n = nullptr;
-  HSV_TRY(dalloc(&op->sup_rows, std::max<int64_t>(rows, 1)));
-  HSV_TRY(dalloc(&d_n, 1));
+  const int64_t nc = m.chunks;
+  ProfScope pa("sup_list");
+  uint32_t *ccount = nullptr, *cprefix = nullptr;
+  HSV_TRY(dalloc(&ccount, nc + 1));
+  HSV_TRY(dalloc(&cprefix, nc + 1));
+  HSV_TRY_CUDA(cudaMemsetAsync(ccount + nc, 0, sizeof(uint32_t), stream()));
+  k_sup_chunk_count<<<(unsigned)((nc * 32 + 255) / 256), 256, 0, stream()>>>(smap, row0, rows, nc,
+                                                                            ccount);
   size_t tb = 0;
-  cub::CountingInputIterator<uint32_t> it(0);
-  HSV_TRY_CUDA(cub::DeviceSelect::Flagged(nullptr, tb, it, smap + row0, op->sup_rows, d_n,
-                                          (int)rows, stream()));
+  HSV_TRY_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, ccount, cprefix, nc + 1, stream()));
   unsigned char* tmp = nullptr;
   HSV_TRY(dalloc(&tmp, std::max<size_t>(tb, 1)));
-  HSV_TRY_CUDA(cub::DeviceSelect::Flagged(tmp, tb, it, smap + row0, op->sup_rows, d_n,
-                                          (int)rows, stream()));
-  int n_s = 0;
-  HSV_TRY_CUDA(cudaMemcpyAsync(&n_s, d_n, sizeof(int), cudaMemcpyDeviceToHost, stream()));
+  HSV_TRY_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, ccount, cprefix, nc + 1, stream()));
+  uint32_t n_s = 0;
+  HSV_TRY_CUDA(cudaMemcpyAsync(&n_s, cprefix + nc, sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                               stream()));
   HSV_TRY(stream_sync());
-  dfree(tmp); dfree(d_n);
-  const int64_t chunks = (n_s + 31) / 32;
+  dfree(tmp);
+  const int64_t chunks = ((int64_t)n_s + 31) / 32;
   const int64_t nl = chunks * S;
   uint32_t* cnt = nullptr;
   uint64_t* sz = nullptr;
+  HSV_TRY(dalloc(&op->sup_rows, std::max<int64_t>(n_s, 1)));
   HSV_TRY(dalloc(&cnt, std::max<int64_t>((int64_t)n_s * S, 1)));
   HSV_TRY(dalloc(&u.len, std::max<int64_t>(nl, 1)));
   HSV_TRY(dalloc(&u.off, nl + 1));
   HSV_TRY(dalloc(&sz, nl + 1));
-  const unsigned gb = (unsigned)std::max<int64_t>(1, (n_s + 255) / 256);
-  if (n_s)
-    k_sup_rows<false><<<gb, 256, 0, stream()>>>(op->sup_rows, n_s, S, m.cols, m.amps, m.off,
-                                                 m.len, smap, cnt, nullptr, nullptr, nullptr);
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((nc + 7) / 8,
+                                                              (int64_t)ctx().num_sms * 16));
+  ProfScope pb("sup_count");
+  k_sup_pass<false><<<(unsigned)grid, 256, 0, stream()>>>(
+      smap, row0, rows, nc, S, cprefix, m.cols, m.amps, m.rcnt, m.off, m.len, op->sup_rows, cnt,
+      nullptr, nullptr, nullptr);
   if (nl)
     k_sell_len<<<(unsigned)((nl + 255) / 256), 256, 0, stream()>>>(cnt, n_s, S, chunks, u.len, sz);
   HSV_TRY_CUDA(cudaMemsetAsync(sz + nl, 0, sizeof(uint64_t), stream()));
@@ -972,15 +1014,21 @@ static int build_sup(hsv_op_s* op, const hsv_op_s::Sell& m, const ApplyArgs& a, 
       dalloc(&u.cols, std::max<uint64_t>(total, 1)) != HSV_OK ||
       dalloc(&u.amps, std::max<uint64_t>(total, 1)) != HSV_OK) {
     free_sell(u);
+    dfree(ccount); dfree(cprefix);
     return HSV_OK;
   }
-  HSV_TRY_CUDA(cudaMemsetAsync(u.cols, 0, total * sizeof(uint32_t), stream()));
-  HSV_TRY_CUDA(cudaMemsetAsync(u.amps, 0, total * sizeof(double), stream()));
-  if (n_s)
-    k_sup_rows<true><<<gb, 256, 0, stream()>>>(op->sup_rows, n_s, S, m.cols, m.amps, m.off,
-                                                m.len, smap, nullptr, u.off, u.cols, u.amps);
-  count_launch(n_s ? 3 : 1);
+  {
+    ProfScope pc("sup_memset");
+    HSV_TRY_CUDA(cudaMemsetAsync(u.cols, 0, total * sizeof(uint32_t), stream()));
+    HSV_TRY_CUDA(cudaMemsetAsync(u.amps, 0, total * sizeof(double), stream()));
+  }
+  ProfScope pd("sup_emit");
+  k_sup_pass<true><<<(unsigned)grid, 256, 0, stream()>>>(
+      smap, row0, rows, nc, S, cprefix, m.cols, m.amps, m.rcnt, m.off, m.len, nullptr, nullptr,
+      u.off, u.cols, u.amps);
+  count_launch(4);
   HSV_CHECK_LAUNCH();
+  dfree(ccount); dfree(cprefix);
   u.lo = a.a_lo; u.hi = a.a_hi; u.S = S; u.chunks = chunks; u.entries = (int64_t)total;
   op->sup_n = n_s;
   op->sup_version = version;
@@ -990,10 +1038,15 @@ static int build_sup(hsv_op_s* op, const hsv_op_s::Sell& m, const ApplyArgs& a, 
 // K1s: K1r from the support-compacted assembled rows; *done = false leaves the
 // launch to the matrix-free K1r.
 static int launch_apply_sup(const hsv_op_s* cop, const ApplyArgs& a, int S, const uint8_t* smap,
-                            uint64_t version, bool* done) {
+                            uint64_t version, int64_t support_rows, bool* done) {
   *done = false;
   hsv_op_s* op = const_cast<hsv_op_s*>(cop);
-  if (!smap || !version || !a.out || a.n_peer_rows > 0) return HSV_OK;
+  if (!smap || !version || !a.out || a.n_peer_rows > 0 || tuning().sup == 0) return HSV_OK;
+  // auto: a sparse support changes with nearly every appended operator and its
+  // K1r is cheap already; the compacted rows pay from ~8 % of the rows up
+  if (tuning().sup < 0 && support_rows >= 0 &&
+      support_rows * 100 < 8 * (a.a_hi - a.a_lo) * op->sec->Nb)
+    return HSV_OK;
   hsv_op_s::Sell* m = nullptr;
   HSV_TRY(get_sell(op, a, S, &m));
   if (!m) return HSV_OK;
@@ -1235,7 +1288,7 @@ int launch_apply_rows(const hsv_op_s* op, const double2* psi, double2* out, int6
   const int S = k1_default_split(op, a_lo, a_hi, true);
   {   // K1s: the support-compacted assembled rows (built once per support map)
     bool done = false;
-    HSV_TRY(launch_apply_sup(op, a, S, smap, smap_version, &done));
+    HSV_TRY(launch_apply_sup(op, a, S, smap, smap_version, support_rows, &done));
     if (done) return HSV_OK;
   }
   {   // K1v over the support rows (hsv_apply_v.cu)

@@ -223,6 +223,7 @@ struct hsv_op_s {
     int S = 1;
     uint32_t* cols = nullptr;
     double* amps = nullptr;
+    uint32_t* rcnt = nullptr;  // [row][split] stored elements (before padding; full ranges)
     uint64_t* off = nullptr;   // [chunk][split]
     uint32_t* len = nullptr;   // [chunk][split] entries per lane
   };

@@ -139,7 +139,11 @@ int cache_alloc(void** p, size_t bytes) {
   std::lock_guard<std::mutex> lk(A.mu);
   auto it = A.free_by_size.lower_bound(bytes);
   if (it == A.free_by_size.end()) {   // new chunk
-    size_t csz = std::max(bytes, kChunk);
+    // 25 % headroom: a buffer rebuilt a little larger each ADAPT iteration
+    // (support-compacted rows) reuses its chunk after coalescing instead of
+    // taking a new one from the driver every time
+    size_t csz = std::max(((bytes + bytes / 4) + ((size_t)2 << 20) - 1) & ~(((size_t)2 << 20) - 1),
+                          kChunk);
     char* base = nullptr;
     cudaError_t e = cudaMalloc(&base, csz);
     if (e != cudaSuccess && csz > bytes) {   // no room for a full chunk: exact size

@@ -20,6 +20,14 @@ struct Tuning {
   int sell = -1;          // K1a (assembled sliced-ELL rows, built once per operator and
                           // row range when it fits sell_budget_mb): -1/1 on, 0 off
   int64_t sell_budget_mb = 32768;
+  int sup = 0;            // K1s (support-compacted assembled rows in the ADAPT evaluation):
+                          // 1 on, -1 auto (when the support map holds >= 8 % of the rows), 0 off.
+                          // Off by default: exact, and the evaluation's H application drops
+                          // from 1.39 to 0.82 ms at H12 depth 400, but the map grows with
+                          // nearly every appended operator and the rebuild (count + copy of
+                          // the in-map elements, 6.4 ms, write-bound) costs more than the 7
+                          // evaluations save (26.3 vs 23.2 ms per iteration; depth 200 15.6
+                          // vs 15.8 ms; tools/sup_probe.py)
   int sell_kernel = 3;    // K1a variant (elements per stage, blocks per SM): 0 (4,4) 1 (4,6)
                           // 2 (8,3) 3 (8,4) 4 (2,8); H12: 1.74 1.70 1.72 1.58 1.85 ms
   int sweep_bar = 0;      // batched sweep barrier: 0 grid.sync(), 1 counting (release/acquire;

@@ -1075,8 +1075,6 @@ int filter_plan(Plan& P, int first) {
     P.max_live = std::max<int64_t>(P.max_live, hl[q]);
   }
   P.support_rows = 1 + P.added_end.back();   // HF + the rows the batches added
-  static uint64_t g_version = 0;
-  P.version = ++g_version;
   const int64_t n_live = cmp[nn];
   const int64_t keep_slots = P.live_off[first];
   const int64_t n_slots = P.live_off[nb];
@@ -1184,6 +1182,17 @@ int get_plan(const hsv_sector_s* sec, int64_t hf_row, const std::vector<OpMasks>
                          (hf_row < 0 || hf_row == P.hf_row) && P.filtered;
   if (unchanged) return HSV_OK;
   if (hf_row < 0) { *ok = false; return HSV_OK; }
+  // the new list extends the old one (ADAPT appends): its support map contains
+  // the old map, so an unchanged row count means an unchanged map and the
+  // map's version (K1s caches on it) stays
+  bool extends = P.filtered && hf_row == P.hf_row;
+  size_t pos = 0;
+  for (const auto& pb : P.b)
+    for (const auto& m : pb.m) {
+      extends = extends && pos < ops.size() && same(m, ops[pos]);
+      ++pos;
+    }
+  const int64_t old_rows = P.support_rows;
   // incremental replan (the common ADAPT case: an appended operator changes the
   // last batch or adds one): drop the support rows the replaced batches added,
   // keep the prefix's live orbits, filter only the new batches
@@ -1208,7 +1217,10 @@ int get_plan(const hsv_sector_s* sec, int64_t hf_row, const std::vector<OpMasks>
     P.b.push_back(pb);
   }
   P.hf_row = hf_row;
-  return filter_plan(P, first);
+  HSV_TRY(filter_plan(P, first));
+  static uint64_t g_version = 0;
+  if (!(extends && P.support_rows == old_rows && P.version)) P.version = ++g_version;
+  return HSV_OK;
 }
 
 }  // namespace

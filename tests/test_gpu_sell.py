@@ -95,3 +95,31 @@ def test_sell_declines_over_budget(hsv, N):
         assert np.array_equal(w0, w1)
     finally:
         N.call("hsv_set_tuning", b"sell_budget_mb", 32768)
+
+
+@pytest.mark.parametrize("name", ["h8", "h10"])
+def test_support_compacted_rows_along_a_growing_list(hsv, N, name):
+    """K1s (support rows of the assembled matrix, in-map elements only) against
+    the matrix-free K1r: energies and gradients bitwise along a growing operator
+    list (the map grows, stays, is rebuilt) and after a replaced operator."""
+    sysm = hsv.MolecularSystem.bundled(name)
+    eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
+    pool = hsv.build_qeb_pool(sysm.n_qubits, sysm.integrals.nelec)
+    rng = np.random.default_rng(17)
+    idx = list(rng.integers(0, len(pool), size=24))
+    th_all = rng.uniform(-0.4, 0.4, size=24)
+    seqs = [idx[:k] for k in (1, 2, 5, 9, 10, 16, 24)] + [idx[:12] + [idx[2]] + idx[13:]]
+    try:
+        for seq in seqs:
+            ops = [pool.ops[i] for i in seq]
+            th = th_all[:len(seq)].copy()
+            th[-1] = 0.0
+            N.call("hsv_set_tuning", b"sup", 1)
+            e1, g1 = eng.energy_and_gradient(ops, th)
+            e1b, g1b = eng.energy_and_gradient(ops, th)    # the cached compacted rows
+            N.call("hsv_set_tuning", b"sup", 0)
+            e0, g0 = eng.energy_and_gradient(ops, th)
+            assert e1 == e0 and np.array_equal(g1, g0), len(seq)
+            assert e1b == e0 and np.array_equal(g1b, g0), len(seq)
+    finally:
+        N.call("hsv_set_tuning", b"sup", 0)
