@@ -411,7 +411,9 @@ def run_hsv(args):
         pk, pk_kind = peaks()
         hbm = float(pk.get("hbm_gbs", 6650.0))
         rows_local = (a_hi - a_lo) * (dim // n_alpha_strings)
-        apply_ms = prof["apply"][0] / max(prof["apply"][1], 1)
+        # per step: the H application runs as screen_overlap phases (K4 on a second
+        # stream overlaps the next phase), so the per-launch mean is not a step's
+        apply_ms = prof["apply"][0] / max(args.steps, 1)
         # algorithmic bytes of one H application over the rank's rows:
         # 16 B per nonzero matrix element (one complex128 gather) + 24 B per row
         # (stream psi_b and write w_b ... key + amplitude) -- SURVEY.md 8(d)
@@ -427,7 +429,7 @@ def run_hsv(args):
         else:
             bytes_apply = (16.0 * nnz_struct + 24.0 * dim) * rows_local / dim
         achieved = bytes_apply / (apply_ms * 1e-3) / 1e9
-        screen_ms = prof["screen"][0] / max(prof["screen"][1], 1)
+        screen_ms = prof["screen"][0] / max(args.steps, 1)
         traffic = ncu_traffic("k_apply_sell" if assembled else "k_apply")
         dram_gbs = traffic / (apply_ms * 1e-3) / 1e9 if traffic else None
         line = {

@@ -613,6 +613,7 @@ struct SellArgs {
   const uint64_t* off;
   const uint32_t* len;
   int64_t n_chunks, rows, row0;   // rows of the range (K1s: of the list), first internal row
+  int64_t chunk_lo, chunk_hi;      // chunks this launch processes
   const uint32_t* rlist;          // K1s: local rows of the list (nullptr: rows in order)
   int S;
   const double2* psi;
@@ -630,7 +631,7 @@ __global__ void __launch_bounds__(256, MINB) k_apply_sell(const SellArgs a) {
   const int lane = threadIdx.x & 31;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t c = gw; c < a.n_chunks; c += nw) {
+  for (int64_t c = a.chunk_lo + gw; c < a.chunk_hi; c += nw) {
     const int64_t li = c * 32 + lane;
     const bool inr = li < a.rows;
     const int64_t row = a.row0 + (a.rlist ? (inr ? (int64_t)__ldg(a.rlist + li) : 0) : li);
@@ -833,22 +834,32 @@ static int get_sell(hsv_op_s* op, const ApplyArgs& a, int S, hsv_op_s::Sell** ou
 }
 
 static int run_sell(const hsv_op_s* op, const hsv_op_s::Sell& m, const ApplyArgs& a, int S,
-                    const uint32_t* rlist, int64_t list_n, const char* scope) {
+                    const uint32_t* rlist, int64_t list_n, const char* scope,
+                    int64_t c0 = 0, int64_t c1 = -1, double* cpart_ext = nullptr) {
   SellArgs g{};
   g.cols = m.cols; g.amps = m.amps; g.off = m.off; g.len = m.len;
   g.n_chunks = m.chunks;
+  g.chunk_lo = c0;
+  g.chunk_hi = c1 < 0 ? m.chunks : c1;
   g.rows = rlist ? list_n : (a.a_hi - a.a_lo) * op->sec->Nb;
   g.row0 = a.a_lo * op->sec->Nb;
   g.rlist = rlist;
   g.S = S;
   g.psi = a.psi; g.diag = a.diag; g.out = a.out; g.prune = a.prune; g.energy_only = a.energy_only;
   g.peer_rows = a.peer_rows; g.n_peer_rows = a.n_peer_rows;
+  const int64_t nch = g.chunk_hi - g.chunk_lo;
+  if (nch <= 0) {
+    if (a.epart && !cpart_ext) HSV_TRY_CUDA(cudaMemsetAsync(a.epart, 0, 2 * sizeof(double), stream()));
+    return HSV_OK;
+  }
   double* cpart = nullptr;
-  if (a.epart) {
+  if (cpart_ext) {
+    g.cpart = cpart_ext;
+  } else if (a.epart) {
     HSV_TRY(dalloc(&cpart, 2 * std::max<int64_t>(g.n_chunks, 1)));
     g.cpart = cpart;
   }
-  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((g.n_chunks + 7) / 8,
+  const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((nch + 7) / 8,
                                                               (int64_t)ctx().num_sms * 16));
   {
     ProfScope prof(scope);
@@ -881,6 +892,46 @@ static int launch_apply_sell(const hsv_op_s* cop, const ApplyArgs& a, int S, int
   if (n_warps) *n_warps = 1;   // epart[0..1] holds the total
   *done = true;
   return HSV_OK;
+}
+
+static ApplyArgs sell_args(const hsv_op_s* op, const double2* psi, double2* out, int64_t a_lo,
+                           int64_t a_hi) {
+  const hsv_sector_s* s = op->sec;
+  ApplyArgs a{};
+  a.split_bk = op->d_splits;
+  a.dim_bytes = s->dim * (int64_t)sizeof(double2);
+  a.Sa = s->d_Sa; a.Sb = s->d_Sb; a.Ra = s->d_Ra; a.Rb = s->d_Rb; a.Rb0 = s->d_Rb0;
+  a.buckets = op->d_buckets; a.n_buckets = (int)op->n_buckets;
+  a.groups = op->d_groups; a.terms = op->d_terms; a.diag = op->d_diag;
+  a.tabs = op->d_tabs; a.recs = op->d_recs; a.n_buckets_h = (int)op->n_buckets_h;
+  a.gsz = op->d_gsz; a.szt = op->d_szt; a.gxa = op->d_gxa; a.g_hashed = (int)op->g_hashed;
+  a.peer_rows = out ? ctx().peer_rows : nullptr;
+  a.n_peer_rows = out ? ctx().n_peer_rows : 0;
+  a.psi = psi; a.out = out;
+  a.Nb = s->Nb; a.a_lo = a_lo; a.a_hi = a_hi;
+  return a;
+}
+
+int sell_chunks(const hsv_op_s* cop, int64_t a_lo, int64_t a_hi, int64_t* chunks) {
+  *chunks = 0;
+  if (tuning().sell == 0 || a_hi <= a_lo) return HSV_OK;
+  hsv_op_s* op = const_cast<hsv_op_s*>(cop);
+  const int S = k1_default_split(op, a_lo, a_hi, true);
+  hsv_op_s::Sell* m = nullptr;
+  HSV_TRY(get_sell(op, sell_args(op, nullptr, nullptr, a_lo, a_hi), S, &m));
+  if (m) *chunks = m->chunks;
+  return HSV_OK;
+}
+
+int sell_apply_chunks(const hsv_op_s* cop, const double2* psi, double2* out, int64_t a_lo,
+                      int64_t a_hi, int64_t c0, int64_t c1, double* cpart) {
+  hsv_op_s* op = const_cast<hsv_op_s*>(cop);
+  const int S = k1_default_split(op, a_lo, a_hi, true);
+  hsv_op_s::Sell* m = nullptr;
+  const ApplyArgs a = sell_args(op, psi, out, a_lo, a_hi);
+  HSV_TRY(get_sell(op, a, S, &m));
+  HSV_REQUIRE(m, HSV_ERR_INVALID, "assembled rows missing for the range");
+  return run_sell(op, *m, a, S, nullptr, 0, "apply", c0, c1, cpart);
 }
 
 // ------------------------------------------------------ K1s (support rows)

@@ -69,6 +69,9 @@ struct Context {
   // device work counters (hsv_stats): exact units processed by the ADAPT
   // evaluation kernels, for the bench's algorithmic-byte accounting
   unsigned long long* d_stats = nullptr;
+  // second stream (K4 phases overlapped with the K1a stream) and its events
+  cudaStream_t aux = nullptr;
+  std::vector<cudaEvent_t> aux_ev;
 };
 enum StatKey { kStatPairsFwd = 0, kStatPairsAdj = 1, kStatRowsK1r = 2, kStatCacheIdle = 4,
                kStatCacheMisses = 5, kStatPoolReserved = 6, kStatPoolUsed = 7, kStatCount = 8 };
@@ -318,10 +321,11 @@ __device__ __forceinline__ double warp_max(double v) {
 // RAII CUDA-event pair around a launch when profiling is enabled.
 class ProfScope {
  public:
-  explicit ProfScope(const char* name);
+  explicit ProfScope(const char* name, cudaStream_t st = nullptr);   // nullptr: stream()
   ~ProfScope();
  private:
   const char* name_;
+  cudaStream_t st_ = nullptr;
   cudaEvent_t a_ = nullptr;
   bool active_ = false;
 };

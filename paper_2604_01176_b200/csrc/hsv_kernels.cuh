@@ -20,6 +20,11 @@ struct Tuning {
   int sell = -1;          // K1a (assembled sliced-ELL rows, built once per operator and
                           // row range when it fits sell_budget_mb): -1/1 on, 0 off
   int64_t sell_budget_mb = 32768;
+  int screen_wsmem = 0;   // K4: the CTA's own w row staged in shared memory (Nb * 16 B <= 48 KB)
+  int screen_overlap = 2; // energy + screen with K1a: K4 on alpha-row phases, on a second
+                          // stream, as the K1a stream finishes their rows (0/1: serial).
+                          // H12 step 2.509 (serial) / 2.435 (2) / 2.494 (4) / 2.561 ms (8):
+                          // K1a and K4 contend for L1 and issue, little overlaps
   int sup = 0;            // K1s (support-compacted assembled rows in the ADAPT evaluation):
                           // 1 on, -1 auto (when the support map holds >= 8 % of the rows), 0 off.
                           // Off by default: exact, and the evaluation's H application drops
@@ -245,6 +250,13 @@ uint64_t sweep_plan_version(const hsv_sector_s* s);
 // drop the cached sweep plan (of sector s only, when s != nullptr)
 void release_sweep_plans(const hsv_sector_s* s = nullptr);
 
+// K1a by chunk ranges (the overlapped energy + screen, hsv_screen.cu): the
+// range's assembled rows if built (*chunks = their 32-row chunk count, 0: not
+// assembled -- the caller runs the serial path); rows of chunks [c0, c1) into
+// out, their energy partials into cpart[2 c] (reduced by the caller in chunk order)
+int sell_chunks(const hsv_op_s* op, int64_t a_lo, int64_t a_hi, int64_t* chunks);
+int sell_apply_chunks(const hsv_op_s* op, const double2* psi, double2* out, int64_t a_lo,
+                      int64_t a_hi, int64_t c0, int64_t c1, double* cpart);
 int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
                   const hsv_pool_s* pool, int64_t a_lo, int64_t a_hi, double* d_grads,
                   const uint32_t* psi_arow = nullptr, const uint32_t* w_arow = nullptr,

@@ -49,16 +49,17 @@ HostProf::~HostProf() {
   slot.second += 1;
 }
 
-ProfScope::ProfScope(const char* name) : name_(name) {
+ProfScope::ProfScope(const char* name, cudaStream_t st) : name_(name), st_(st) {
   if (!g_prof.on) return;
+  if (!st_) st_ = stream();
   a_ = take_event();
-  cudaEventRecord(a_, stream());
+  cudaEventRecord(a_, st_);
   active_ = true;
 }
 ProfScope::~ProfScope() {
   if (!active_) return;
   cudaEvent_t b = take_event();
-  cudaEventRecord(b, stream());
+  cudaEventRecord(b, st_);
   g_prof.pending.push_back(ProfPair{name_, a_, b});
 }
 
@@ -119,6 +120,12 @@ int hsv_set_tuning(const char* key, int64_t value) {
   } else if (k == "sell") {
     HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "sell must be -1, 0 or 1");
     g_tuning.sell = (int)value;
+  } else if (k == "screen_wsmem") {
+    HSV_REQUIRE(value == 0 || value == 1, HSV_ERR_INVALID, "screen_wsmem must be 0 or 1");
+    g_tuning.screen_wsmem = (int)value;
+  } else if (k == "screen_overlap") {
+    HSV_REQUIRE(value >= 0 && value <= 64, HSV_ERR_INVALID, "screen_overlap must be 0..64");
+    g_tuning.screen_overlap = (int)value;
   } else if (k == "sup") {
     HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "sup must be -1, 0 or 1");
     g_tuning.sup = (int)value;

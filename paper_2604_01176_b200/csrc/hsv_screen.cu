@@ -63,13 +63,21 @@ __device__ __forceinline__ double re_conj_mul(double2 a, double2 b) {
 // outside [a_lo, a_hi) or where w is zero).  The same (w row, psi row, beta
 // list) triples are summed, grouped by psi row: CTAs of empty psi rows write
 // zeros and leave, so the cost follows the support of psi.
-template <int D, bool PIVOT>
+template <int D, bool PIVOT, bool WS = false>
 __global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t rloc = blockIdx.y;
   const int64_t rc = PIVOT ? rloc : a.a_lo + rloc;   // the CTA's row: w (own) or psi
   const uint32_t sc = __ldg(a.Sa + rc);
   const double2* __restrict__ crow = (PIVOT ? a.psi : a.w) + rc * a.Nb;
+  // WS: the CTA's own w row staged in shared memory once (every warp's w
+  // gathers hit it; the L1 keeps the psi partner rows)
+  extern __shared__ double2 wsh[];
+  if (WS) {
+    for (int64_t j = threadIdx.x; j < a.Nb; j += blockDim.x) wsh[j] = crow[j];
+    __syncthreads();
+    crow = wsh;
+  }
   const int stride = a.slices * kScreenWarps;
   const bool c_zero = PIVOT ? (a.psi_arow && !__ldg(a.psi_arow + rc))
                             : (a.w_arow && !__ldg(a.w_arow + rc));
@@ -238,6 +246,42 @@ int pool_prepare(hsv_pool_s* p) {
   return HSV_OK;
 }
 
+// K4 partials of owned alpha rows [r0, r1) (no pivot) into part rows
+// [r0 - part_row0, r1 - part_row0) on stream st.
+static int launch_screen_rows(const hsv_op_s* op, const double2* psi, const double2* w,
+                              const hsv_pool_s* pool, int64_t r0, int64_t r1, double* part,
+                              const uint32_t* psi_arow, cudaStream_t st) {
+  const hsv_sector_s* s = op->sec;
+  const int n_ops = (int)pool->n;
+  const int64_t rows = r1 - r0;
+  if (n_ops <= 0 || rows <= 0) return HSV_OK;
+  HSV_REQUIRE(rows <= 65535, HSV_ERR_UNSUPPORTED, "too many alpha rows for one launch");
+  const int64_t want = (int64_t)ctx().num_sms * 8 * 4;
+  int slices = (int)std::min<int64_t>((want + rows - 1) / rows,
+                                      (n_ops + kScreenWarps - 1) / kScreenWarps);
+  slices = std::max(slices, 1);
+  ScreenArgs a{};
+  a.Sa = s->d_Sa; a.Ra = s->d_Ra;
+  a.ops = pool->d; a.order = pool->d_order; a.opl = pool->d_opl; a.blist = pool->d_blist;
+  a.qa = pool->d_qa; a.qn = pool->d_qn;
+  a.n_ops = n_ops; a.psi = psi; a.w = w; a.Nb = s->Nb; a.a_lo = r0; a.a_hi = r1;
+  a.slices = slices;
+  a.part = part;
+  a.psi_arow = psi_arow;
+  a.w_arow = nullptr;
+  const dim3 grid((unsigned)slices, (unsigned)rows);
+  const bool big = 2 * s->dim * (int64_t)sizeof(double2) > ctx().l2_bytes;
+  const size_t ws = (size_t)s->Nb * sizeof(double2);
+  if (tuning().screen_wsmem != 0 && ws <= 48 * 1024 && !big)
+    k_screen<2, false, true><<<grid, kScreenBlock, ws, st>>>(a);
+  else
+    big ? k_screen<4, false><<<grid, kScreenBlock, 0, st>>>(a)
+        : k_screen<2, false><<<grid, kScreenBlock, 0, st>>>(a);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  return HSV_OK;
+}
+
 int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
                   const hsv_pool_s* pool, int64_t a_lo, int64_t a_hi, double* d_grads,
                   const uint32_t* psi_arow, const uint32_t* w_arow, bool sparse_psi) {
@@ -272,9 +316,12 @@ int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
     ProfScope prof("screen");
     const dim3 grid((unsigned)slices, (unsigned)rows);
     const bool big = 2 * s->dim * (int64_t)sizeof(double2) > ctx().l2_bytes;
+    const size_t ws = (size_t)s->Nb * sizeof(double2);
     if (pivot)
       big ? k_screen<4, true><<<grid, kScreenBlock, 0, stream()>>>(a)
           : k_screen<2, true><<<grid, kScreenBlock, 0, stream()>>>(a);
+    else if (tuning().screen_wsmem != 0 && ws <= 48 * 1024 && !big)
+      k_screen<2, false, true><<<grid, kScreenBlock, ws, stream()>>>(a);
     else
       big ? k_screen<4, false><<<grid, kScreenBlock, 0, stream()>>>(a)
           : k_screen<2, false><<<grid, kScreenBlock, 0, stream()>>>(a);
@@ -292,9 +339,73 @@ using namespace hsv;
 
 extern "C" {
 
+// Energy + screen with the assembled rows, overlapped: K1a runs phase after
+// phase (alpha-row ranges, chunk-aligned) on the library stream, and K4 works on
+// each finished range on a second stream while K1a streams the next one (K1a
+// is HBM-bound, K4 L1-bound on L2-resident data).  The K4 partials and the K1a
+// energy partials are reduced once, in the serial path's order: bitwise equal.
+static int energy_screen_overlap(hsv_op op, hsv_state psi, const hsv_pool_s* pool, int64_t a_lo,
+                                 int64_t a_hi, double* d_out, bool* done) {
+  *done = false;
+  const int P = tuning().screen_overlap;
+  if (P <= 1 || !psi->dense_hint || pool->n <= 0 || a_hi - a_lo < 2 * P) return HSV_OK;
+  int64_t nc = 0;
+  HSV_TRY(sell_chunks(op, a_lo, a_hi, &nc));
+  if (nc == 0) return HSV_OK;
+  const hsv_sector_s* s = op->sec;
+  Context& C = ctx();
+  if (!C.aux) HSV_TRY_CUDA(cudaStreamCreateWithFlags(&C.aux, cudaStreamNonBlocking));
+  while ((int)C.aux_ev.size() < P + 1) {
+    cudaEvent_t e;
+    HSV_TRY_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    C.aux_ev.push_back(e);
+  }
+  const int n_ops = (int)pool->n;
+  const int64_t rows = a_hi - a_lo;
+  double2* w = nullptr;
+  double *cpart = nullptr, *part = nullptr;
+  HSV_TRY(dalloc(&w, s->dim));
+  HSV_TRY(dalloc(&cpart, 2 * nc));
+  HSV_TRY(dalloc(&part, rows * n_ops));
+  HSV_TRY(state_arow_async(psi));
+  const int64_t Nb = s->Nb;
+  int64_t c_prev = 0, done_rows = a_lo;
+  for (int r = 0; r < P; ++r) {
+    // phase r: chunks up to the one holding the end of alpha row ra1 - 1 ...
+    const int64_t ra1 = a_lo + rows * (r + 1) / P;
+    const int64_t c1 = r == P - 1 ? nc : ((ra1 - a_lo) * Nb) / 32;
+    HSV_TRY(sell_apply_chunks(op, psi->d_amp, w, a_lo, a_hi, c_prev, c1, cpart));
+    HSV_TRY_CUDA(cudaEventRecord(C.aux_ev[r], stream()));
+    // ... and K4 on the alpha rows those chunks completed
+    const int64_t ra_done = r == P - 1 ? a_hi : a_lo + (c1 * 32) / Nb;
+    if (ra_done > done_rows) {
+      HSV_TRY_CUDA(cudaStreamWaitEvent(C.aux, C.aux_ev[r], 0));
+      ProfScope prof("screen", C.aux);
+      HSV_TRY(launch_screen_rows(op, psi->d_amp, w, pool, done_rows, ra_done,
+                                 part + (done_rows - a_lo) * n_ops, psi->d_arow, C.aux));
+      done_rows = ra_done;
+    }
+    c_prev = c1;
+  }
+  HSV_TRY_CUDA(cudaEventRecord(C.aux_ev[P], C.aux));
+  HSV_TRY_CUDA(cudaStreamWaitEvent(stream(), C.aux_ev[P], 0));
+  HSV_TRY(reduce_sum_f64(cpart, nc, 2, 2, d_out));
+  HSV_TRY(reduce_sum_f64(part, rows, n_ops, n_ops, d_out + 2));
+  dfree(part);
+  dfree(cpart);
+  dfree(w);
+  *done = true;
+  return HSV_OK;
+}
+
 static int energy_screen_dev(hsv_op op, hsv_state psi, const hsv_pool_s* pool, int64_t a_lo,
                              int64_t a_hi, double* d_out) {
   const hsv_sector_s* s = op->sec;
+  {
+    bool done = false;
+    HSV_TRY(energy_screen_overlap(op, psi, pool, a_lo, a_hi, d_out, &done));
+    if (done) return HSV_OK;
+  }
   ProfScope prof_all("es_all");
   double2* w = nullptr;
   HSV_TRY(dalloc(&w, s->dim));

@@ -123,3 +123,28 @@ def test_support_compacted_rows_along_a_growing_list(hsv, N, name):
             assert e1b == e0 and np.array_equal(g1b, g0), len(seq)
     finally:
         N.call("hsv_set_tuning", b"sup", 0)
+
+
+@pytest.mark.parametrize("name", ["h10", "h12"])
+def test_overlapped_energy_screen_bitwise_equal_serial(hsv, N, name):
+    """K4 phases on a second stream under the K1a stream (screen_overlap) give
+    the serial path's energy and gradients bit for bit (same partials, same
+    reduction order); also on an alpha-row shard."""
+    sysm = hsv.MolecularSystem.bundled(name)
+    eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
+    pool = hsv.build_qeb_pool(sysm.n_qubits, sysm.integrals.nelec)
+    n = len(sysm.basis)
+    rng = np.random.default_rng(23)
+    v = rng.standard_normal(n)
+    v /= np.linalg.norm(v)
+    st = dense(hsv, sysm.basis, v)
+    eng.energy_and_screen(st, pool)                 # marks psi dense, builds the rows
+    try:
+        out = {}
+        for ov in (0, 4, 3):
+            N.call("hsv_set_tuning", b"screen_overlap", ov)
+            out[ov] = eng.energy_and_screen(st, pool)
+        for ov in (4, 3):
+            assert out[ov][0] == out[0][0] and np.array_equal(out[ov][1], out[0][1]), ov
+    finally:
+        N.call("hsv_set_tuning", b"screen_overlap", 2)
