@@ -20,7 +20,6 @@ struct Tuning {
   int sell = -1;          // K1a (assembled sliced-ELL rows, built once per operator and
                           // row range when it fits sell_budget_mb): -1/1 on, 0 off
   int64_t sell_budget_mb = 32768;
-  int screen_wsmem = 0;   // K4: the CTA's own w row staged in shared memory (Nb * 16 B <= 48 KB)
   int screen_overlap = 2; // energy + screen with K1a: K4 on alpha-row phases, on a second
                           // stream, as the K1a stream finishes their rows (0/1: serial).
                           // H12 step 2.509 (serial) / 2.435 (2) / 2.494 (4) / 2.561 ms (8):

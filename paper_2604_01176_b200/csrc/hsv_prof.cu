@@ -120,9 +120,6 @@ int hsv_set_tuning(const char* key, int64_t value) {
   } else if (k == "sell") {
     HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "sell must be -1, 0 or 1");
     g_tuning.sell = (int)value;
-  } else if (k == "screen_wsmem") {
-    HSV_REQUIRE(value == 0 || value == 1, HSV_ERR_INVALID, "screen_wsmem must be 0 or 1");
-    g_tuning.screen_wsmem = (int)value;
   } else if (k == "screen_overlap") {
     HSV_REQUIRE(value >= 0 && value <= 64, HSV_ERR_INVALID, "screen_overlap must be 0..64");
     g_tuning.screen_overlap = (int)value;

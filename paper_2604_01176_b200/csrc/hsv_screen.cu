@@ -63,21 +63,13 @@ __device__ __forceinline__ double re_conj_mul(double2 a, double2 b) {
 // outside [a_lo, a_hi) or where w is zero).  The same (w row, psi row, beta
 // list) triples are summed, grouped by psi row: CTAs of empty psi rows write
 // zeros and leave, so the cost follows the support of psi.
-template <int D, bool PIVOT, bool WS = false>
+template <int D, bool PIVOT>
 __global__ void __launch_bounds__(kScreenBlock) k_screen(const ScreenArgs a) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t rloc = blockIdx.y;
   const int64_t rc = PIVOT ? rloc : a.a_lo + rloc;   // the CTA's row: w (own) or psi
   const uint32_t sc = __ldg(a.Sa + rc);
   const double2* __restrict__ crow = (PIVOT ? a.psi : a.w) + rc * a.Nb;
-  // WS: the CTA's own w row staged in shared memory once (every warp's w
-  // gathers hit it; the L1 keeps the psi partner rows)
-  extern __shared__ double2 wsh[];
-  if (WS) {
-    for (int64_t j = threadIdx.x; j < a.Nb; j += blockDim.x) wsh[j] = crow[j];
-    __syncthreads();
-    crow = wsh;
-  }
   const int stride = a.slices * kScreenWarps;
   const bool c_zero = PIVOT ? (a.psi_arow && !__ldg(a.psi_arow + rc))
                             : (a.w_arow && !__ldg(a.w_arow + rc));
@@ -271,12 +263,8 @@ static int launch_screen_rows(const hsv_op_s* op, const double2* psi, const doub
   a.w_arow = nullptr;
   const dim3 grid((unsigned)slices, (unsigned)rows);
   const bool big = 2 * s->dim * (int64_t)sizeof(double2) > ctx().l2_bytes;
-  const size_t ws = (size_t)s->Nb * sizeof(double2);
-  if (tuning().screen_wsmem != 0 && ws <= 48 * 1024 && !big)
-    k_screen<2, false, true><<<grid, kScreenBlock, ws, st>>>(a);
-  else
-    big ? k_screen<4, false><<<grid, kScreenBlock, 0, st>>>(a)
-        : k_screen<2, false><<<grid, kScreenBlock, 0, st>>>(a);
+  big ? k_screen<4, false><<<grid, kScreenBlock, 0, st>>>(a)
+      : k_screen<2, false><<<grid, kScreenBlock, 0, st>>>(a);
   count_launch();
   HSV_CHECK_LAUNCH();
   return HSV_OK;
@@ -316,12 +304,9 @@ int launch_screen(const hsv_op_s* op, const double2* psi, const double2* w,
     ProfScope prof("screen");
     const dim3 grid((unsigned)slices, (unsigned)rows);
     const bool big = 2 * s->dim * (int64_t)sizeof(double2) > ctx().l2_bytes;
-    const size_t ws = (size_t)s->Nb * sizeof(double2);
     if (pivot)
       big ? k_screen<4, true><<<grid, kScreenBlock, 0, stream()>>>(a)
           : k_screen<2, true><<<grid, kScreenBlock, 0, stream()>>>(a);
-    else if (tuning().screen_wsmem != 0 && ws <= 48 * 1024 && !big)
-      k_screen<2, false, true><<<grid, kScreenBlock, ws, stream()>>>(a);
     else
       big ? k_screen<4, false><<<grid, kScreenBlock, 0, stream()>>>(a)
           : k_screen<2, false><<<grid, kScreenBlock, 0, stream()>>>(a);
