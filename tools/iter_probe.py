@@ -92,7 +92,7 @@ def main():
                         {k: round(v - e0[k], 2) for k, v in dev_ms(True).items() if v - e0[k] > 0.5}))
             return r
         setattr(eng, name, wrap)
-    init = (ops[:k], tr[f"thetas_at_{k}"])
+    init = (ops[:k], tr[f"thetas_at_{k}"]) if k > 0 else None
     for p in range(args.passes):
         log.clear()
         if p == args.passes - 1 and args.passes > 1:
