@@ -193,6 +193,7 @@ __device__ __forceinline__ double rec_amp(const Rec<W>& r, W s, const double* __
 
 int grid_for(int64_t n, int block);
 int state_dot_async(hsv_state a, hsv_state b, double* d_r);   // <a|b> -> d_r[0..1]
+int state_dot_norm2_async(hsv_state a, hsv_state b, double* d_r);   // and <b|b> -> b's norm
 void use_split_table(const hsv_op_s* op, int St, ApplyArgs& a);
 int apply_warps(const hsv_op_s* op);
 // Push (scatter + sort-reduce) K1 for sparse psi; *done = false: use the pull kernel.

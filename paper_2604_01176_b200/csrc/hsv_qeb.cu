@@ -823,12 +823,13 @@ int hsv_eg_backward(hsv_op op, hsv_state psi, hsv_state w, const uint64_t* occ,
   // [0, k): gradients, [k, k + 2): <psi|w>; one copy back at the end (no sync here)
   double* d_grad = nullptr;
   HSV_TRY(dalloc(&d_grad, k + 2));
-  HSV_TRY(state_dot_async(psi, w, d_grad + k));
+  // E = <psi|w>, and <lam|lam> (lam = w) for the drift checks: one pass
+  if (k > 0) HSV_TRY(state_dot_norm2_async(psi, w, d_grad + k));
+  else HSV_TRY(state_dot_async(psi, w, d_grad + k));
   if (tuning().sweep == 0) {   // flags of the per-rotation launches
     HSV_TRY(state_arow_async(psi));
     HSV_TRY(state_arow_async(w));
   }
-  if (k > 0) HSV_TRY(state_norm2_async(w));   // <lam|lam> for the drift checks
   PairScratch sc;
   HSV_TRY(sc.init(sec, 3));
   PairLists pl;

@@ -230,6 +230,37 @@ int upload_amps(const double* re, const double* im, int64_t n, double2** d_out) 
 }
 
 // <a|b> into d_r[0..1] (re, im), stream-ordered
+// <a|b> -> d_r[0..1] and <b|b> -> b's cached norm in one pass over both
+// (the adjoint evaluation needs both; each sum is the one the separate
+// kernels form: same grid, same per-thread order, same block reduction)
+__global__ void k_dot_norm2(const double2* __restrict__ a, const double2* __restrict__ b,
+                            int64_t n, double* __restrict__ part) {
+  double v[3] = {0.0, 0.0, 0.0};
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double2 x = a[i], y = b[i];
+    v[0] += x.x * y.x + x.y * y.y;
+    v[1] += x.x * y.y - x.y * y.x;
+    v[2] += y.x * y.x + y.y * y.y;
+  }
+  block_store<3>(v, part);
+}
+
+int state_dot_norm2_async(hsv_state a, hsv_state b, double* d_r) {
+  const int64_t n = a->sec->dim;
+  const int grid = grid_for(n, 256);
+  double* part = nullptr;
+  HSV_TRY(dalloc(&part, 3 * (int64_t)grid));
+  k_dot_norm2<<<grid, 256, 0, stream()>>>(a->d_amp, b->d_amp, n, part);
+  count_launch();
+  HSV_CHECK_LAUNCH();
+  HSV_TRY(reduce_sum_f64(part, grid, 3, 2, d_r));
+  HSV_TRY(reduce_sum_f64(part + 2, grid, 3, 1, b->d_norm2));
+  dfree(part);
+  b->norm2_valid = true;
+  return HSV_OK;
+}
+
 int state_dot_async(hsv_state a, hsv_state b, double* d_r) {
   const int64_t n = a->sec->dim;
   const int grid = grid_for(n, 256);
