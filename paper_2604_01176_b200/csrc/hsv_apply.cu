@@ -717,6 +717,115 @@ __global__ void __launch_bounds__(256, MINB) k_apply_sell(const SellArgs a) {
   }
 }
 
+// Split-parallel K1a: a work unit is one (chunk, bucket split) segment, so a
+// rank's shard (6.7 k chunks at H12 / 4 against ~4.7 k resident warps) still
+// gives every warp ~11 units instead of 1-2 (0.55 vs 0.41 ms ideal).  Each lane
+// writes its split partial; k_sell_combine sums them in split order, exactly
+// as the chunk-per-warp kernel does in registers.
+template <int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_apply_sell_sp(const SellArgs a, double2* ypart,
+                                                             int64_t pstride) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nch = a.chunk_hi - a.chunk_lo;
+  for (int64_t u = gw; u < nch * a.S; u += nw) {
+    const int sp = (int)(u / nch);                  // split-major: one bucket range at a time
+    const int64_t c = a.chunk_lo + (u - (int64_t)sp * nch);
+    const int64_t li = c * 32 + lane;
+    const bool inr = li < a.rows;
+    const int64_t row = a.row0 + li;
+    const double2 pv = inr ? a.psi[row] : make_double2(0.0, 0.0);
+    if (a.energy_only && !__any_sync(0xffffffffu, pv.x != 0.0 || pv.y != 0.0)) {
+      if (inr) ypart[sp * pstride + li] = make_double2(0.0, 0.0);
+      continue;
+    }
+    const double ds = (sp == 0 && a.diag && inr) ? a.diag[row] : 0.0;
+    double2 acc = make_double2(ds * pv.x, ds * pv.y);
+    const uint32_t L = __ldg(a.len + c * a.S + sp);
+    const uint64_t base = __ldg(a.off + c * a.S + sp) + lane;
+    const uint32_t* __restrict__ cp = a.cols + base;
+    const double* __restrict__ ap = a.amps + base;
+    const uint32_t Lu = L / U * U;
+    uint32_t q[U];
+    double m[U];
+    if (Lu > 0) {
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        q[k] = __ldcs(cp + (uint64_t)k * 32);
+        m[k] = __ldcs(ap + (uint64_t)k * 32);
+      }
+    }
+    for (uint32_t j = 0; j < Lu; j += U) {
+      double2 p[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) p[k] = a.psi[q[k]];
+      uint32_t qn[U];
+      double mn[U];
+      const bool more = j + U < Lu;
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        qn[k] = more ? __ldcs(cp + (uint64_t)(j + U + k) * 32) : 0u;
+        mn[k] = more ? __ldcs(ap + (uint64_t)(j + U + k) * 32) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        acc.x = fma(m[k], p[k].x, acc.x);
+        acc.y = fma(m[k], p[k].y, acc.y);
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) { q[k] = qn[k]; m[k] = mn[k]; }
+    }
+    for (uint32_t j = Lu; j < L; ++j) {
+      const uint32_t qq = __ldcs(cp + (uint64_t)j * 32);
+      const double mm = __ldcs(ap + (uint64_t)j * 32);
+      const double2 pp = a.psi[qq];
+      acc.x = fma(mm, pp.x, acc.x);
+      acc.y = fma(mm, pp.y, acc.y);
+    }
+    if (inr) ypart[sp * pstride + li] = acc;
+  }
+}
+
+// rows of chunks [chunk_lo, chunk_hi): y = part_0 + part_1 + ... (split order),
+// the drop rule, the stores (and peer stores), and each chunk's energy share
+// summed over its 32 rows in lane order (the chunk-per-warp kernel's cpart)
+__global__ void k_sell_combine(const SellArgs a, const double2* __restrict__ ypart,
+                               int64_t pstride) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = a.chunk_lo + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (c >= a.chunk_hi) return;
+  const int64_t li = c * 32 + lane;
+  const bool inr = li < a.rows;
+  const int64_t row = a.row0 + li;
+  double2 y = make_double2(0.0, 0.0);
+  double2 pv = make_double2(0.0, 0.0);
+  if (inr) {
+    pv = a.psi[row];
+    y = ypart[li];
+    for (int sp = 1; sp < a.S; ++sp) {
+      const double2 p = ypart[sp * pstride + li];
+      y.x += p.x;
+      y.y += p.y;
+    }
+    if (a.out && !a.energy_only) {
+      double2 v = y;
+      if (a.prune > 0.0 && sqrt(v.x * v.x + v.y * v.y) < a.prune) v = make_double2(0.0, 0.0);
+      put_row(a.out, a.peer_rows, a.n_peer_rows, row, v);
+    }
+  }
+  if (a.cpart) {
+    double er = 0.0, ei = 0.0;
+    if (inr) {
+      er = pv.x * y.x + pv.y * y.y;
+      ei = pv.x * y.y - pv.y * y.x;
+    }
+    er = warp_sum(er);
+    ei = warp_sum(ei);
+    if (lane == 0) { a.cpart[2 * c] = er; a.cpart[2 * c + 1] = ei; }
+  }
+}
+
 static void free_sell(hsv_op_s::Sell& m) {
   dfree(m.cols); dfree(m.amps); dfree(m.rcnt); dfree(m.off); dfree(m.len);
   m.cols = nullptr; m.amps = nullptr; m.rcnt = nullptr; m.off = nullptr; m.len = nullptr;
@@ -858,6 +967,30 @@ static int run_sell(const hsv_op_s* op, const hsv_op_s::Sell& m, const ApplyArgs
   } else if (a.epart) {
     HSV_TRY(dalloc(&cpart, 2 * std::max<int64_t>(g.n_chunks, 1)));
     g.cpart = cpart;
+  }
+  // auto: split-parallel while the launch has fewer than ~2 chunks per resident
+  // warp (rank shards: H12 / 4 0.514 vs 0.551 ms, / 8 0.269 vs 0.288); the whole
+  // H12 range keeps a chunk per warp (1.639 vs 1.666 ms)
+  const bool sp_auto = nch < 2ll * ctx().num_sms * 32;
+  if (!rlist && S > 1 && (tuning().sell_sp > 0 || (tuning().sell_sp < 0 && sp_auto))) {
+    // split-parallel units + an in-order combine (bitwise the same rows/energy)
+    const int64_t rows_l = g.rows;
+    double2* ypart = nullptr;
+    HSV_TRY(dalloc(&ypart, (int64_t)S * std::max<int64_t>(rows_l, 1)));
+    const int64_t units = nch * S;
+    const int64_t grid_sp = std::max<int64_t>(1, std::min<int64_t>((units + 7) / 8,
+                                                                   (int64_t)ctx().num_sms * 4));
+    {
+      ProfScope prof(scope);
+      k_apply_sell_sp<8, 4><<<(unsigned)grid_sp, 256, 0, stream()>>>(g, ypart, rows_l);
+      k_sell_combine<<<(unsigned)((nch * 32 + 255) / 256), 256, 0, stream()>>>(g, ypart, rows_l);
+    }
+    count_launch(2);
+    HSV_CHECK_LAUNCH();
+    dfree(ypart);
+    if (cpart) HSV_TRY(reduce_sum_f64(cpart, g.n_chunks, 2, 2, a.epart));
+    dfree(cpart);
+    return HSV_OK;
   }
   const int64_t grid = std::max<int64_t>(1, std::min<int64_t>((nch + 7) / 8,
                                                               (int64_t)ctx().num_sms * 16));

@@ -32,6 +32,9 @@ struct Tuning {
                           // the in-map elements, 6.4 ms, write-bound) costs more than the 7
                           // evaluations save (26.3 vs 23.2 ms per iteration; depth 200 15.6
                           // vs 15.8 ms; tools/sup_probe.py)
+  int sell_sp = -1;       // K1a work units: 1 (chunk, split) segments + in-order combine,
+                          // 0 one chunk per warp (all splits in registers), -1 auto (split
+                          // segments below ~2 chunks per resident warp)
   int sell_kernel = 3;    // K1a variant (elements per stage, blocks per SM): 0 (4,4) 1 (4,6)
                           // 2 (8,3) 3 (8,4) 4 (2,8); H12: 1.74 1.70 1.72 1.58 1.85 ms
   int sweep_bar = 0;      // batched sweep barrier: 0 grid.sync(), 1 counting (release/acquire;

@@ -126,6 +126,9 @@ int hsv_set_tuning(const char* key, int64_t value) {
   } else if (k == "sup") {
     HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "sup must be -1, 0 or 1");
     g_tuning.sup = (int)value;
+  } else if (k == "sell_sp") {
+    HSV_REQUIRE(value >= -1 && value <= 1, HSV_ERR_INVALID, "sell_sp must be -1, 0 or 1");
+    g_tuning.sell_sp = (int)value;
   } else if (k == "sell_kernel") {
     HSV_REQUIRE(value >= 0 && value <= 4, HSV_ERR_INVALID, "sell_kernel must be 0..4");
     g_tuning.sell_kernel = (int)value;

@@ -37,7 +37,8 @@ def both(N, fn):
 
 @pytest.mark.parametrize("name", ["h4", "h6", "h8", "h10", "h12"])
 @pytest.mark.parametrize("cplx", [False, True])
-def test_sell_rows_bitwise_equal_k1(hsv, N, name, cplx):
+@pytest.mark.parametrize("sp", [-1, 0, 1])
+def test_sell_rows_bitwise_equal_k1(hsv, N, name, cplx, sp):
     sysm = hsv.MolecularSystem.bundled(name)
     op = hsv.assemble_subspace_hamiltonian(sysm.hamiltonian, sysm.basis)
     rng = np.random.default_rng(5)
@@ -45,7 +46,12 @@ def test_sell_rows_bitwise_equal_k1(hsv, N, name, cplx):
     v = rng.standard_normal(n) + (1j * rng.standard_normal(n) if cplx else 0.0)
     v /= np.linalg.norm(v)
     st = dense(hsv, sysm.basis, v)
-    (w0, e0), (w1, e1) = both(N, lambda: (op.apply_state(st).to_sparse().to_dense(), op.expect(st)))
+    N.call("hsv_set_tuning", b"sell_sp", sp)   # chunk per warp, split segments, auto
+    try:
+        (w0, e0), (w1, e1) = both(N, lambda: (op.apply_state(st).to_sparse().to_dense(),
+                                              op.expect(st)))
+    finally:
+        N.call("hsv_set_tuning", b"sell_sp", -1)
     assert np.array_equal(w0, w1)
     assert abs(e1 - e0) <= 1e-13 * max(1.0, abs(e0))
     # the drop rule on the combined rows

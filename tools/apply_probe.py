@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--system", default="h12")
     ap.add_argument("--variants", nargs="+", default=["sell=0", "sell=1"])
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--shard", type=int, default=1, help="time rows of alpha strings [0, Na/shard)")
     args = ap.parse_args()
     N.init(0)
     sysm = hsv.MolecularSystem.bundled(args.system)
@@ -36,11 +37,22 @@ def main():
         kv = [x.split("=") for x in var.split(",")]
         for key, val in kv:
             N.call("hsv_set_tuning", key.encode(), int(val))
-        op.apply_state(st)                      # warm-up (builds K1a rows)
+        na = sysm.basis._sector.n_alpha_strings
+        hi = na // args.shard
+        from paper_2604_01176_b200.svengine import DeviceState
+        out = DeviceState(sysm.basis)
+
+        def run():
+            if args.shard == 1:
+                op.apply_state(st)
+            else:
+                N.call("hsv_apply_h_rows_async", op.handle, st.device.handle, out.handle, 0, hi, 0.0)
+                N.call("hsv_synchronize")
+        run()                                   # warm-up (builds K1a rows)
         N.call("hsv_prof_reset")
         N.call("hsv_prof_enable", 1)
         for _ in range(args.reps):
-            op.apply_state(st)
+            run()
         N.call("hsv_prof_collect")
         N.call("hsv_prof_enable", 0)
         t, c = N.dbl(), N.i64()
@@ -48,7 +60,8 @@ def main():
         print(json.dumps({"system": args.system, "variant": var, "apply_ms": t.value / max(c.value, 1),
                           "launches": c.value}), flush=True)
         for key, _ in kv:
-            N.call("hsv_set_tuning", key.encode(), {"sell": -1, "sell_budget_mb": 32768}.get(key, 0))
+            N.call("hsv_set_tuning", key.encode(),
+                   {"sell": -1, "sell_budget_mb": 32768, "sell_sp": -1, "sell_kernel": 3}.get(key, 0))
 
 
 if __name__ == "__main__":
