@@ -1226,11 +1226,19 @@ static int launch_apply_sup(const hsv_op_s* cop, const ApplyArgs& a, int S, cons
   *done = false;
   hsv_op_s* op = const_cast<hsv_op_s*>(cop);
   if (!smap || !version || !a.out || a.n_peer_rows > 0 || tuning().sup == 0) return HSV_OK;
-  // auto: a sparse support changes with nearly every appended operator and its
-  // K1r is cheap already; the compacted rows pay from ~8 % of the rows up
-  if (tuning().sup < 0 && support_rows >= 0 &&
-      support_rows * 100 < 8 * (a.a_hi - a.a_lo) * op->sec->Nb)
-    return HSV_OK;
+  // auto: only for a map that outlives its iteration.  While the support grows
+  // the map changes with nearly every appended operator and a rebuild per
+  // iteration costs more than its ~7 evaluations save; on a plateau (H12 free
+  // run: 213,744 rows from depth ~200 to ~325) one build serves every later
+  // evaluation.  A map seen by more than 10 evaluations (about 1.5 iterations)
+  // is taken to be on a plateau; the rows are bitwise K1r's either way.
+  if (tuning().sup < 0) {
+    if (op->sup_seen != version) {
+      op->sup_seen = version;
+      op->sup_seen_evals = 0;
+    }
+    if (++op->sup_seen_evals <= 10 && op->sup_version != version) return HSV_OK;
+  }
   hsv_op_s::Sell* m = nullptr;
   HSV_TRY(get_sell(op, a, S, &m));
   if (!m) return HSV_OK;

@@ -239,6 +239,8 @@ struct hsv_op_s {
   uint32_t* sup_rows = nullptr;      // local rows of the support, ascending
   int64_t sup_n = 0;
   uint64_t sup_version = 0;
+  uint64_t sup_seen = 0;             // the map version the last evaluation used, and
+  int64_t sup_seen_evals = 0;        // how many evaluations in a row used it
 };
 
 struct hsv_pool_s {

@@ -24,14 +24,12 @@ struct Tuning {
                           // stream, as the K1a stream finishes their rows (0/1: serial).
                           // H12 step 2.509 (serial) / 2.435 (2) / 2.494 (4) / 2.561 ms (8):
                           // K1a and K4 contend for L1 and issue, little overlaps
-  int sup = 0;            // K1s (support-compacted assembled rows in the ADAPT evaluation):
-                          // 1 on, -1 auto (when the support map holds >= 8 % of the rows), 0 off.
-                          // Off by default: exact, and the evaluation's H application drops
-                          // from 1.39 to 0.82 ms at H12 depth 400, but the map grows with
-                          // nearly every appended operator and the rebuild (count + copy of
-                          // the in-map elements, 6.4 ms, write-bound) costs more than the 7
-                          // evaluations save (26.3 vs 23.2 ms per iteration; depth 200 15.6
-                          // vs 15.8 ms; tools/sup_probe.py)
+  int sup = -1;           // K1s (support-compacted assembled rows in the ADAPT evaluation):
+                          // 1 always, 0 off, -1 auto: once a support map has served more than
+                          // 10 evaluations (a plateau of the support, not a growing one).  A
+                          // rebuild per iteration costs more than its evaluations save (H12
+                          // depth 400: 26.3 vs 23.2 ms per iteration; depth 200 15.6 vs 15.8;
+                          // tools/sup_probe.py); a map that outlives its iteration pays
   int sell_sp = -1;       // K1a work units: 1 (chunk, split) segments + in-order combine,
                           // 0 one chunk per warp (all splits in registers), -1 auto (split
                           // segments below ~2 chunks per resident warp)

@@ -128,7 +128,7 @@ def test_support_compacted_rows_along_a_growing_list(hsv, N, name):
             assert e1 == e0 and np.array_equal(g1, g0), len(seq)
             assert e1b == e0 and np.array_equal(g1b, g0), len(seq)
     finally:
-        N.call("hsv_set_tuning", b"sup", 0)
+        N.call("hsv_set_tuning", b"sup", -1)
 
 
 @pytest.mark.parametrize("name", ["h10", "h12"])
@@ -154,3 +154,18 @@ def test_overlapped_energy_screen_bitwise_equal_serial(hsv, N, name):
             assert out[ov][0] == out[0][0] and np.array_equal(out[ov][1], out[0][1]), ov
     finally:
         N.call("hsv_set_tuning", b"screen_overlap", 2)
+
+
+def test_support_rows_auto_switch_on_a_plateau(hsv, N):
+    """sup = -1: a support map that serves more than 10 evaluations switches to
+    the compacted assembled rows mid-run; every evaluation stays bitwise equal."""
+    sysm = hsv.MolecularSystem.bundled("h10")
+    eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
+    pool = hsv.build_qeb_pool(sysm.n_qubits, sysm.integrals.nelec)
+    rng = np.random.default_rng(37)
+    ops = [pool.ops[i] for i in rng.integers(0, len(pool), size=40)]
+    th = rng.uniform(-0.4, 0.4, size=40)
+    N.call("hsv_set_tuning", b"sup", -1)
+    res = [eng.energy_and_gradient(ops, th) for _ in range(14)]
+    for e, g in res[1:]:
+        assert e == res[0][0] and np.array_equal(g, res[0][1])

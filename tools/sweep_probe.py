@@ -67,7 +67,7 @@ def main():
                 N.call("hsv_set_tuning", key.encode(),
                        {"sweep": 2, "restrict_rows": -1, "push": -1, "sweep_p2p": 0,
                         "apply_v": 0, "apply_t": 0, "sweep_grid": 0,
-                        "sweep_bar": 0, "sweep_threads": 256, "sup": 0,
+                        "sweep_bar": 0, "sweep_threads": 256, "sup": -1,
                         "sell": -1}.get(key, -1))
 
 
