@@ -615,6 +615,7 @@ struct SellArgs {
   int64_t n_chunks, rows, row0;   // rows of the range (K1s: of the list), first internal row
   int64_t chunk_lo, chunk_hi;      // chunks this launch processes
   const uint32_t* rlist;          // K1s: local rows of the list (nullptr: rows in order)
+  unsigned long long* stats;      // K1s: rows computed -> the K1r row counter (hsv_stats)
   int S;
   const double2* psi;
   const double* diag;
@@ -703,6 +704,10 @@ __global__ void __launch_bounds__(256, MINB) k_apply_sell(const SellArgs a) {
       double2 v = y;
       if (a.prune > 0.0 && sqrt(v.x * v.x + v.y * v.y) < a.prune) v = make_double2(0.0, 0.0);
       put_row(a.out, a.peer_rows, a.n_peer_rows, row, v);
+    }
+    if (a.stats) {
+      const unsigned nr = __popc(__ballot_sync(0xffffffffu, inr));
+      if (lane == 0 && nr) atomicAdd(a.stats + kStatRowsK1r, (unsigned long long)nr);
     }
     if (a.cpart) {   // this chunk's <psi|H psi> share, summed in chunk order
       double er = 0.0, ei = 0.0;
@@ -953,6 +958,7 @@ static int run_sell(const hsv_op_s* op, const hsv_op_s::Sell& m, const ApplyArgs
   g.rows = rlist ? list_n : (a.a_hi - a.a_lo) * op->sec->Nb;
   g.row0 = a.a_lo * op->sec->Nb;
   g.rlist = rlist;
+  g.stats = rlist ? ctx().d_stats : nullptr;
   g.S = S;
   g.psi = a.psi; g.diag = a.diag; g.out = a.out; g.prune = a.prune; g.energy_only = a.energy_only;
   g.peer_rows = a.peer_rows; g.n_peer_rows = a.n_peer_rows;
