@@ -110,6 +110,9 @@ HSV_API int hsv_op_create(hsv_sector s, int n_qubits, const int64_t* xs, const i
 HSV_API int hsv_op_destroy(hsv_op op);
 /* n_terms, n_groups (distinct x incl. diagonal), number of in-sector nonzero
  * matrix elements is not stored (matrix-free). */
+/* Note on the *_async entry points: the first dense H application of an
+ * alpha-row range assembles that range's rows (K1a, below), which synchronizes
+ * once; every later call is asynchronous. */
 /* K1a: stored slots (elements incl. sliced-ELL padding; 12 B each) and split
  * count of the assembled rows for alpha rows [a_lo, a_hi), 0 if not assembled
  * (K1a is built on the first H application of a range whose rows fit
