@@ -181,7 +181,21 @@ class SvAdaptEngine:
         return apply_qeb_exponential(op, theta, state)
 
     def rebuild(self, ops, thetas):
-        return apply_ansatz(self.basis, self.system.hf, ops, thetas)
+        """apply_ansatz (svengine.py:240-244) with the evaluation's cached operator
+        masks (the same fused device sweep)."""
+        from . import _native as N
+        from .svengine import DeviceState
+        ops = list(ops)
+        th = np.ascontiguousarray(thetas, dtype=np.float64)
+        n = min(len(ops), th.size)
+        if n != len(ops) or n != th.size:
+            return apply_ansatz(self.basis, self.system.hf, ops, thetas)
+        occ, virt = self._pool_masks(ops)
+        cs, sn = N.as_f64(np.cos(th)), N.as_f64(np.sin(th))
+        dev = DeviceState(self.basis)
+        N.call("hsv_ansatz_state", self.basis.sector, int(self.system.hf.bits), N.ptr_u64(occ),
+               N.ptr_u64(virt), N.ptr_f64(cs), N.ptr_f64(sn), n, dev.handle)
+        return SvState(self.basis, _dev=dev)
 
     def energy(self, state) -> float:
         return self.matrix.expect(state)
