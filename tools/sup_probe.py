@@ -26,8 +26,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--depth", type=int, default=400)
     ap.add_argument("--iters", type=int, default=3)
+    ap.add_argument("--tune", nargs="*", default=[], help="KEY=V library tuning keys")
     args = ap.parse_args()
     N.init(0)
+    for kv in args.tune:
+        key, v = kv.split("=")
+        N.call("hsv_set_tuning", key.encode(), int(v))
     tr = np.load(ROOT / "tests" / "golden" / "trace_h12_416.npz")
     sysm = hsv.MolecularSystem.bundled("h12")
     eng = hsv.SvAdaptEngine(sysm, hsv.AdaptConfig())
@@ -50,7 +54,7 @@ def main():
         N.call("hsv_prof_get", kn.encode(), N.C.byref(t), N.C.byref(c))
         out[kn] = [round(t.value, 3), c.value]
     wall = np.diff([r.wall_elapsed for r in res.records]) * 1e3
-    print(json.dumps({"depth": k, "iter_ms": [round(float(x), 2) for x in wall], "scopes_ms_count": out}))
+    print(json.dumps({"depth": k, "tune": args.tune, "iter_ms": [round(float(x), 2) for x in wall], "scopes_ms_count": out}))
 
 
 if __name__ == "__main__":
