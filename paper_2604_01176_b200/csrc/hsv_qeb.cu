@@ -802,6 +802,10 @@ int hsv_ansatz_state(hsv_sector s, uint64_t hf_key, const uint64_t* occ, const u
   HSV_TRY(sc.init(s, 2));
   PairLists pl;
   HSV_TRY(forward_psi(s, hf_key, occ, virt, cs, sn, k, psi, sc, pl));
+  // a support far past the push path's source budget: the next H application
+  // goes straight to the pull / assembled path (and the overlapped screen)
+  // instead of first counting sources to find out
+  if (psi->smap_valid && sweep_plan_support(s) > 65536) psi->dense_hint = true;
   const int rc = sc.check();   // synchronizes; drift errors surface here
   dfree(pl.la); dfree(pl.lb);
   sc.release();
