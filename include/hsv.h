@@ -68,7 +68,8 @@ typedef struct hsv_peer_s* hsv_peer;
 HSV_API int hsv_abi_version(void);
 /* Copies the last error message of the calling thread into buf. */
 HSV_API int hsv_last_error(char* buf, size_t n);
-/* Select the CUDA device for subsequent objects (one context per process). */
+/* Select the CUDA device for subsequent objects: one device per process; a
+ * second call with another device fails (HSV_ERR_INVALID). */
 HSV_API int hsv_init(int device);
 /* Enqueue all work on this cudaStream_t (0 = library-owned stream). */
 HSV_API int hsv_set_stream(void* cuda_stream);

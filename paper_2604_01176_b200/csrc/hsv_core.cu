@@ -349,6 +349,11 @@ int hsv_last_error(char* buf, size_t n) {
 
 int hsv_init(int device) {
   if (g_ctx.device == device && g_ctx.stream) return HSV_OK;
+  // one device per process: the device arena, the plans and every handle
+  // belong to the first device
+  HSV_REQUIRE(g_ctx.device < 0, HSV_ERR_INVALID,
+              "libhsv is bound to CUDA device %d; one device per process (got %d)",
+              g_ctx.device, device);
   HSV_TRY_CUDA(cudaSetDevice(device));
   HSV_TRY_CUDA(cudaFree(0));
   cudaDeviceProp prop;
